@@ -1,0 +1,43 @@
+/*
+ * qbfac_gpu_testing.h — kernel-level hooks of libqbfac_gpu.so for the parity tests.
+ * Not part of the drop-in boundary (include/qbfac_gpu.h); device pointers only,
+ * every call synchronizes the context stream before returning.
+ *
+ *   qbfac_gpu_test_gemm      the DMMA GEMM behind every dense product
+ *                            (replaces kernels::gemm_nn / gemm_tn, kernels_drivers.cpp:21-65)
+ *   qbfac_gpu_test_chol      the in-CTA Cholesky + inverse used by CholQR
+ *   qbfac_gpu_test_householder  the Householder panel QR (orth_qr, qr.hpp:15-18)
+ *   qbfac_gpu_test_colsumsq  per-column sums of squares (the indicator's row norms)
+ *   qbfac_gpu_test_csr_spmm  CSR pass Y = alpha A X + beta Y on device arrays
+ *                            (replaces csr_gemm_n, kernels_drivers.cpp:67-79)
+ */
+#ifndef QBFAC_GPU_TESTING_H
+#define QBFAC_GPU_TESTING_H
+
+#include <stdint.h>
+
+#include "qbfac_gpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* C(M x N) = alpha * A(M x K) * B(K x N) + beta * C; *_row selects row-major storage. */
+int qbfac_gpu_test_gemm(qbfac_gpu_ctx* ctx, double alpha, const double* a, int64_t m, int64_t k, int64_t lda,
+                        int a_row, const double* b, int64_t n, int64_t ldb, int b_row, double beta, double* c,
+                        int64_t ldc, int c_row);
+/* b x b Gram (col-major, ld b) -> R, R^{-1} (col-major, ld b); returns breakdown flag in *status. */
+int qbfac_gpu_test_chol(qbfac_gpu_ctx* ctx, const double* g, int b, double* r, double* rinv, int* status);
+/* Householder QR of a column-major m x b panel in place (Q overwrites y); R col-major ld b. */
+int qbfac_gpu_test_householder(qbfac_gpu_ctx* ctx, double* y, int64_t m, int b, int64_t ld, double* r);
+int qbfac_gpu_test_colsumsq(qbfac_gpu_ctx* ctx, const double* x, int64_t rows, int64_t cols, int64_t ld, int row,
+                            double* out);
+int qbfac_gpu_test_csr_spmm(qbfac_gpu_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* rp,
+                            const int32_t* ci, const double* v, const double* x, int64_t ldx, double* y,
+                            int64_t ldy, int w, double alpha, double beta);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QBFAC_GPU_TESTING_H */

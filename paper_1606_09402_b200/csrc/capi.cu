@@ -1,0 +1,352 @@
+// extern "C" boundary (include/qbfac_gpu.h): exception -> status translation over
+// the engine in qb.cu. No C++ exception crosses this layer.
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "../../include/qbfac_gpu.h"
+#include "qb.cuh"
+
+struct qbfac_gpu_ctx {
+    std::unique_ptr<qbgpu::Context> c;
+    std::string last_error;
+};
+struct qbfac_gpu_matrix {
+    qbfac_gpu_ctx* ctx = nullptr;
+    std::unique_ptr<qbgpu::Matrix> m;
+};
+struct qbfac_gpu_result {
+    qbfac_gpu_ctx* ctx = nullptr;
+    std::unique_ptr<qbgpu::Result> r;
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+template <class Fn>
+int guard(qbfac_gpu_ctx* ctx, Fn&& fn, qbfac_info* info = nullptr) {
+    auto fail = [&](int st, const std::string& msg) {
+        if (ctx) ctx->last_error = msg;
+        else g_create_error = msg;
+        if (info) info->status = st;
+        return st;
+    };
+    try {
+        if (ctx && ctx->c) {
+            cudaError_t e = cudaSetDevice(ctx->c->device);
+            if (e != cudaSuccess) return fail(QBFAC_ERROR, cudaGetErrorString(e));
+        }
+        fn();
+        if (info) info->status = QBFAC_OK;
+        return QBFAC_OK;
+    } catch (const qbgpu::QbError& e) {
+        if (info) {
+            info->diag_index = e.diag_index;
+            info->floor = e.floor;
+        }
+        return fail(e.status, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(QBFAC_RESOURCE_ERROR, "host out of memory");
+    } catch (const std::exception& e) {
+        return fail(QBFAC_INTERNAL, e.what());
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int qbfac_gpu_create(int device, qbfac_gpu_ctx** out) { return qbfac_gpu_create_dist(device, 0, 1, nullptr, out); }
+
+int qbfac_gpu_create_dist(int device, int rank, int world, const void* nccl_id, qbfac_gpu_ctx** out) {
+    if (!out) return QBFAC_ERROR;
+    *out = nullptr;
+    auto h = std::make_unique<qbfac_gpu_ctx>();
+    int st = guard(nullptr, [&] {
+        if (world > 1 && !nccl_id) throw qbgpu::QbError(qbgpu::kError, "world > 1 needs an NCCL unique id");
+        h->c = std::make_unique<qbgpu::Context>(device, rank, world, nccl_id);
+    });
+    if (st == QBFAC_OK) *out = h.release();
+    return st;
+}
+
+int qbfac_gpu_nccl_unique_id(void* out128) {
+    return guard(nullptr, [&] { qbgpu::Comm::unique_id(out128); });
+}
+
+void qbfac_gpu_destroy(qbfac_gpu_ctx* ctx) { delete ctx; }
+
+const char* qbfac_gpu_last_error(const qbfac_gpu_ctx* ctx) {
+    return ctx ? ctx->last_error.c_str() : g_create_error.c_str();
+}
+
+int qbfac_gpu_synchronize(qbfac_gpu_ctx* ctx) {
+    return guard(ctx, [&] { QB_CUDA(cudaStreamSynchronize(ctx->c->st)); });
+}
+
+void* qbfac_gpu_stream(qbfac_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c->st) : nullptr; }
+
+int64_t qbfac_gpu_kernel_launches(const qbfac_gpu_ctx*) { return qbgpu::g_kernel_launches.load(); }
+
+// ---- matrices ---------------------------------------------------------------------
+int qbfac_gpu_matrix_dense(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
+                           qbfac_gpu_matrix** out) {
+    return qbfac_gpu_matrix_dense_shard(ctx, m, 0, m, n, a, lda, out);
+}
+
+int qbfac_gpu_matrix_dense_shard(qbfac_gpu_ctx* ctx, int64_t m_global, int64_t row0, int64_t m_local, int64_t n,
+                                 const double* a, int64_t lda, qbfac_gpu_matrix** out) {
+    if (!ctx || !out) return QBFAC_ERROR;
+    *out = nullptr;
+    return guard(ctx, [&] {
+        auto h = std::make_unique<qbfac_gpu_matrix>();
+        h->ctx = ctx;
+        h->m = qbgpu::make_dense(*ctx->c, m_global, row0, m_local, n, a, lda, false);
+        *out = h.release();
+    });
+}
+
+int qbfac_gpu_matrix_dense_device(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, const double* dev_a, int64_t lda,
+                                  qbfac_gpu_matrix** out) {
+    if (!ctx || !out) return QBFAC_ERROR;
+    *out = nullptr;
+    return guard(ctx, [&] {
+        auto h = std::make_unique<qbfac_gpu_matrix>();
+        h->ctx = ctx;
+        h->m = qbgpu::make_dense(*ctx->c, m, 0, m, n, dev_a, lda, true);
+        *out = h.release();
+    });
+}
+
+int qbfac_gpu_matrix_csr(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                         const int32_t* col_idx, const double* values, qbfac_gpu_matrix** out) {
+    return qbfac_gpu_matrix_csr_shard(ctx, m, 0, m, n, nnz, row_ptr, col_idx, values, out);
+}
+
+int qbfac_gpu_matrix_csr_shard(qbfac_gpu_ctx* ctx, int64_t m_global, int64_t row0, int64_t m_local, int64_t n,
+                               int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                               qbfac_gpu_matrix** out) {
+    if (!ctx || !out) return QBFAC_ERROR;
+    *out = nullptr;
+    return guard(ctx, [&] {
+        auto h = std::make_unique<qbfac_gpu_matrix>();
+        h->ctx = ctx;
+        h->m = qbgpu::make_csr(*ctx->c, m_global, row0, m_local, n, nnz, row_ptr, col_idx, values);
+        *out = h.release();
+    });
+}
+
+void qbfac_gpu_matrix_free(qbfac_gpu_matrix* mat) {
+    if (!mat) return;
+    if (mat->ctx && mat->ctx->c) cudaSetDevice(mat->ctx->c->device);
+    delete mat;
+}
+
+int64_t qbfac_gpu_matrix_passes(const qbfac_gpu_matrix* mat) { return mat ? mat->m->passes : 0; }
+
+int qbfac_gpu_frob_norm_sq(qbfac_gpu_ctx* ctx, qbfac_gpu_matrix* mat, double* out) {
+    return guard(ctx, [&] { *out = qbgpu::frob_norm_sq(*ctx->c, *mat->m); });
+}
+
+int qbfac_gpu_multiply(qbfac_gpu_ctx* ctx, qbfac_gpu_matrix* mat, const double* x, int64_t w, int trans, double* y) {
+    return guard(ctx, [&] {
+        auto& c = *ctx->c;
+        auto& a = *mat->m;
+        const int64_t xr = trans ? a.m : a.n;
+        const int64_t yr = trans ? a.n : a.m;
+        qbgpu::DBuf xc(static_cast<size_t>(xr * w), c.st), xrm(static_cast<size_t>(xr * w), c.st);
+        qbgpu::DBuf yrm(static_cast<size_t>(yr * w), c.st), yc(static_cast<size_t>(yr * w), c.st);
+        if (xr * w > 0) QB_CUDA(cudaMemcpyAsync(xc.p, x, sizeof(double) * xr * w, cudaMemcpyHostToDevice, c.st));
+        qbgpu::MatView xcv{xc.p, xr, w, std::max<int64_t>(xr, 1), false};
+        qbgpu::MatView xrv{xrm.p, xr, w, std::max<int64_t>(w, 1), true};
+        qbgpu::MatView yrv{yrm.p, yr, w, std::max<int64_t>(w, 1), true};
+        qbgpu::MatView ycv{yc.p, yr, w, std::max<int64_t>(yr, 1), false};
+        qbgpu::copy_matrix(c.st, xcv, xrv);
+        qbgpu::multiply(c, a, xrv, yrv, trans != 0);
+        qbgpu::copy_matrix(c.st, yrv, ycv);
+        if (yr * w > 0) QB_CUDA(cudaMemcpyAsync(y, yc.p, sizeof(double) * yr * w, cudaMemcpyDeviceToHost, c.st));
+        QB_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int qbfac_gpu_gaussian(qbfac_gpu_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t skip, int64_t rows, int64_t cols,
+                       double* out) {
+    return guard(ctx, [&] {
+        if (rows < 1 || cols < 1) throw qbgpu::QbError(qbgpu::kDimensionError, "gaussian: dimensions must be at least 1");
+        auto& c = *ctx->c;
+        qbgpu::DBuf d(static_cast<size_t>(rows * cols), c.st);
+        qbgpu::gaussian_fill(c.st, c.rng, seed, stream, skip, qbgpu::MatView{d.p, rows, cols, rows, false});
+        QB_CUDA(cudaMemcpyAsync(out, d.p, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, c.st));
+        QB_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int qbfac_gpu_gaussian_device(qbfac_gpu_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t skip, int64_t rows,
+                              int64_t cols, double* dev_out, int64_t ld) {
+    return guard(ctx, [&] {
+        if (rows < 1 || cols < 1) throw qbgpu::QbError(qbgpu::kDimensionError, "gaussian: dimensions must be at least 1");
+        auto& c = *ctx->c;
+        qbgpu::gaussian_fill(c.st, c.rng, seed, stream, skip, qbgpu::MatView{dev_out, rows, cols, ld, false});
+    });
+}
+
+// ---- algorithms ---------------------------------------------------------------------
+int qbfac_gpu_run(qbfac_gpu_ctx* ctx, qbfac_gpu_matrix* mat, const qbfac_params* params, qbfac_gpu_result** out,
+                  qbfac_info* info) {
+    if (!ctx || !mat || !params || !out) return QBFAC_ERROR;
+    *out = nullptr;
+    qbfac_info local{};
+    qbfac_info* inf = info ? info : &local;
+    std::memset(inf, 0, sizeof(*inf));
+    return guard(
+        ctx,
+        [&] {
+            qbgpu::Params p;
+            p.alg = params->alg;
+            p.mode = params->mode;
+            p.b = params->b;
+            p.power = params->power;
+            p.k = params->k;
+            p.s = params->s;
+            p.max_rank = params->max_rank;
+            p.l_budget = params->l_budget;
+            p.max_restarts = params->max_restarts;
+            p.eps_abs = params->eps_abs;
+            p.seed = params->seed;
+            p.stream = params->stream;
+            p.reorth = params->reorth != 0;
+            if (p.power < 0) throw qbgpu::QbError(qbgpu::kDimensionError, "power must be >= 0");
+            auto h = std::make_unique<qbfac_gpu_result>();
+            h->ctx = ctx;
+            h->r = qbgpu::run(*ctx->c, *mat->m, p);
+            const auto& r = *h->r;
+            inf->rank = r.rank;
+            inf->error_indicator = r.e;
+            inf->norm_a_sq = r.norm_a_sq;
+            inf->passes = r.passes;
+            inf->terminated_by = r.terminated_by;
+            inf->m = r.m;
+            inf->n = r.n;
+            inf->blocks = r.blocks;
+            inf->gaussians_used = r.gaussians_used;
+            inf->restarts = r.restarts;
+            inf->householder_fallbacks = r.hh_fallbacks;
+            inf->device_ms = r.device_ms;
+            *out = h.release();
+        },
+        inf);
+}
+
+int qbfac_gpu_result_copy_q(qbfac_gpu_result* res, double* q, int64_t ldq) {
+    if (!res) return QBFAC_ERROR;
+    return guard(res->ctx, [&] {
+        auto& r = *res->r;
+        auto& c = *res->ctx->c;
+        if (r.rank == 0 || r.m == 0) return;
+        if (ldq < r.m) throw qbgpu::QbError(qbgpu::kDimensionError, "copy_q: ldq < m");
+        qbgpu::DBuf t(static_cast<size_t>(r.m * r.rank), c.st);
+        qbgpu::MatView tv{t.p, r.m, r.rank, r.m, false};
+        qbgpu::copy_matrix(c.st, r.q_view(), tv);
+        QB_CUDA(cudaMemcpy2DAsync(q, ldq * sizeof(double), t.p, r.m * sizeof(double), r.m * sizeof(double), r.rank,
+                                  cudaMemcpyDeviceToHost, c.st));
+        QB_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int qbfac_gpu_result_copy_b(qbfac_gpu_result* res, double* b, int64_t ldb) {
+    if (!res) return QBFAC_ERROR;
+    return guard(res->ctx, [&] {
+        auto& r = *res->r;
+        auto& c = *res->ctx->c;
+        if (r.rank == 0 || r.n == 0) return;
+        if (ldb < r.rank) throw qbgpu::QbError(qbgpu::kDimensionError, "copy_b: ldb < rank");
+        // B(i, j) = B^T(j, i): column j of B is row j of the row-major B^T.
+        QB_CUDA(cudaMemcpy2DAsync(b, ldb * sizeof(double), r.bt.p, r.ld * sizeof(double), r.rank * sizeof(double), r.n,
+                                  cudaMemcpyDeviceToHost, c.st));
+        QB_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int64_t qbfac_gpu_result_copy_trace(qbfac_gpu_result* res, double* out, int64_t cap) {
+    if (!res) return 0;
+    const auto& tr = res->r->trace;
+    const int64_t n = std::min<int64_t>(cap, static_cast<int64_t>(tr.size()));
+    if (out && n > 0) std::memcpy(out, tr.data(), sizeof(double) * n);
+    return static_cast<int64_t>(tr.size());
+}
+
+void qbfac_gpu_result_free(qbfac_gpu_result* res) {
+    if (!res) return;
+    if (res->ctx && res->ctx->c) cudaSetDevice(res->ctx->c->device);
+    delete res;
+}
+
+int qbfac_gpu_validate_epsilon(double eps, double frob_a, double delta, double* floor_out) {
+    const double floor = std::sqrt(4.0 * 1.1102230246251565e-16 / delta) * frob_a;
+    if (floor_out) *floor_out = floor;
+    return eps > floor ? 1 : 0;
+}
+
+}  // extern "C"
+
+// ---- kernel-level test hooks (include/qbfac_gpu_testing.h) ------------------------------
+#include "../../include/qbfac_gpu_testing.h"
+
+extern "C" {
+
+int qbfac_gpu_test_gemm(qbfac_gpu_ctx* ctx, double alpha, const double* a, int64_t m, int64_t k, int64_t lda,
+                        int a_row, const double* b, int64_t n, int64_t ldb, int b_row, double beta, double* c,
+                        int64_t ldc, int c_row) {
+    return guard(ctx, [&] {
+        auto& cx = *ctx->c;
+        qbgpu::MatView av{const_cast<double*>(a), m, k, lda, a_row != 0};
+        qbgpu::MatView bv{const_cast<double*>(b), k, n, ldb, b_row != 0};
+        qbgpu::MatView cv{c, m, n, ldc, c_row != 0};
+        qbgpu::gemm(cx.st, cx.ws_gemm, alpha, av, bv, beta, cv);
+        QB_CUDA(cudaStreamSynchronize(cx.st));
+    });
+}
+
+int qbfac_gpu_test_chol(qbfac_gpu_ctx* ctx, const double* g, int b, double* r, double* rinv, int* status) {
+    return guard(ctx, [&] {
+        auto& cx = *ctx->c;
+        qbgpu::chol_small(cx.st, g, b, b, r, rinv, b, cx.d_status);
+        QB_CUDA(cudaMemcpyAsync(cx.h_status, cx.d_status, sizeof(qbgpu::SmallStatus), cudaMemcpyDeviceToHost, cx.st));
+        QB_CUDA(cudaStreamSynchronize(cx.st));
+        *status = cx.h_status->breakdown;
+    });
+}
+
+int qbfac_gpu_test_householder(qbfac_gpu_ctx* ctx, double* y, int64_t m, int b, int64_t ld, double* r) {
+    return guard(ctx, [&] {
+        auto& cx = *ctx->c;
+        qbgpu::householder_panel(cx.st, cx.ws_hh, y, m, b, ld, r, b);
+        QB_CUDA(cudaStreamSynchronize(cx.st));
+    });
+}
+
+int qbfac_gpu_test_colsumsq(qbfac_gpu_ctx* ctx, const double* x, int64_t rows, int64_t cols, int64_t ld, int row,
+                            double* out) {
+    return guard(ctx, [&] {
+        auto& cx = *ctx->c;
+        qbgpu::column_sumsq(cx.st, cx.ws_red, qbgpu::MatView{const_cast<double*>(x), rows, cols, ld, row != 0}, out);
+        QB_CUDA(cudaStreamSynchronize(cx.st));
+    });
+}
+
+int qbfac_gpu_test_csr_spmm(qbfac_gpu_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* rp,
+                            const int32_t* ci, const double* v, const double* x, int64_t ldx, double* y, int64_t ldy,
+                            int w, double alpha, double beta) {
+    return guard(ctx, [&] {
+        auto& cx = *ctx->c;
+        qbgpu::CsrView a{rows, cols, nnz, rp, ci, v};
+        qbgpu::csr_spmm(cx.st, a, x, ldx, y, ldy, w, alpha, beta, cx.sms);
+        QB_CUDA(cudaStreamSynchronize(cx.st));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// NCCL over NVLink/NVSwitch for the row-sharded path: the only
+// collectives are the n x w allreduce after every A^T pass and the small Gram
+// allreduces (k x b, b x b) plus one scalar for ||A||_F^2.
+
+#include "comm.cuh"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace qbgpu {
+
+namespace {
+
+struct NcclApi {
+    void* handle = nullptr;
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) init_rank = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclCommDestroy) destroy = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+NcclApi& api() {
+    static NcclApi a;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            a.handle = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (a.handle) break;
+        }
+        if (!a.handle) return;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(a.handle, "ncclGetUniqueId"));
+        a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(a.handle, "ncclCommInitRank"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(a.handle, "ncclAllReduce"));
+        a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(a.handle, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(a.handle, "ncclGetErrorString"));
+    });
+    if (!a.handle || !a.get_unique_id || !a.init_rank || !a.all_reduce || !a.destroy)
+        throw QbError(kError, "NCCL (libnccl.so.2) is not available");
+    return a;
+}
+
+void check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) {
+        const char* msg = api().error_string ? api().error_string(r) : "nccl error";
+        throw QbError(kError, std::string(what) + ": " + msg);
+    }
+}
+
+}  // namespace
+
+Comm::Comm(int rank, int world, const void* unique_id128) : rank_(rank), world_(world) {
+    if (world < 1 || rank < 0 || rank >= world) throw QbError(kDimensionError, "bad rank/world");
+    if (world == 1) return;
+    ncclUniqueId id;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(&id, unique_id128, sizeof(id));
+    ncclComm_t c = nullptr;
+    check(api().init_rank(&c, world, id, rank), "ncclCommInitRank");
+    comm_ = c;
+}
+
+Comm::~Comm() {
+    if (comm_) api().destroy(static_cast<ncclComm_t>(comm_));
+}
+
+void Comm::allreduce_sum(double* p, std::size_t count, cudaStream_t st) {
+    if (world_ == 1 || count == 0) return;
+    check(api().all_reduce(p, p, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), st),
+          "ncclAllReduce");
+}
+
+void Comm::unique_id(void* out128) {
+    ncclUniqueId id;
+    check(api().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof(id));
+}
+
+}  // namespace qbgpu

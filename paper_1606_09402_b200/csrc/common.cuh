@@ -1,0 +1,78 @@
+// Shared device/host helpers for the qbfac B200 path (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace qbgpu {
+
+// Status codes of the C-ABI (include/qbfac_gpu.h); they mirror the reference's
+// exception hierarchy (/root/reference/proj/include/qbfac/types.hpp:16-66).
+enum Status : int {
+    kOk = 0,
+    kDimensionError = 1,
+    kSingularityError = 2,
+    kToleranceFloorError = 3,
+    kFormatError = 4,
+    kResourceError = 5,
+    kError = 6,
+    kInternal = 7,
+};
+
+struct QbError : std::runtime_error {
+    int status;
+    std::int64_t diag_index = 0;
+    double floor = 0.0;
+    QbError(int st, const std::string& m) : std::runtime_error(m), status(st) {}
+};
+
+[[noreturn]] inline void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    const int st = (e == cudaErrorMemoryAllocation) ? kResourceError : kError;
+    throw QbError(st, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                          std::to_string(line) + ")");
+}
+
+#define QB_CUDA(call)                                                     \
+    do {                                                                  \
+        cudaError_t qb_e_ = (call);                                       \
+        if (qb_e_ != cudaSuccess) ::qbgpu::throw_cuda(qb_e_, #call, __FILE__, __LINE__); \
+    } while (0)
+
+// Every kernel launch of the library is followed by QB_LAUNCH_CHECK(), which
+// also counts it (qbfac_gpu_kernel_launches()).
+extern std::atomic<long long> g_kernel_launches;
+#define QB_LAUNCH_CHECK()                                   \
+    do {                                                    \
+        ::qbgpu::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
+        QB_CUDA(cudaPeekAtLastError());                     \
+    } while (0)
+
+inline std::int64_t round_up(std::int64_t x, std::int64_t a) { return (x + a - 1) / a * a; }
+inline std::int64_t ceil_div(std::int64_t x, std::int64_t a) { return (x + a - 1) / a; }
+
+// A strided view of a logical rows x cols FP64 matrix in device memory.
+// rowmajor == false: element (i, j) at p[i + j*ld]   (column-major, the reference's layout)
+// rowmajor == true : element (i, j) at p[i*ld + j]
+struct MatView {
+    double* p = nullptr;
+    std::int64_t rows = 0, cols = 0, ld = 0;
+    bool rowmajor = false;
+
+    __host__ __device__ double* at(std::int64_t i, std::int64_t j) const {
+        return rowmajor ? p + i * ld + j : p + i + j * ld;
+    }
+    // Logical transpose (no data movement).
+    MatView t() const { return MatView{p, cols, rows, ld, !rowmajor}; }
+    // Sub-block [r0, r0+nr) x [c0, c0+nc).
+    MatView block(std::int64_t r0, std::int64_t c0, std::int64_t nr, std::int64_t nc) const {
+        return MatView{at(r0, c0), nr, nc, ld, rowmajor};
+    }
+    MatView cols_range(std::int64_t c0, std::int64_t nc) const { return block(0, c0, rows, nc); }
+    MatView rows_range(std::int64_t r0, std::int64_t nr) const { return block(r0, 0, nr, cols); }
+};
+
+}  // namespace qbgpu

@@ -1,0 +1,370 @@
+// FP64 tensor-core (DMMA) GEMM for sm_100a.
+//
+// Replaces the reference's blocked CPU drivers gemm_nn / gemm_tn
+// (/root/reference/proj/src/kernels_drivers.cpp:21-65) and every dense product
+// the algorithm layer issues through them (dense_matrix.cpp:68-92,
+// matrix_handle.cpp:12-19): the passes over A (G = A*Omega, H = A^T*G, power
+// products) and the per-block tall-skinny products (Q*M, Q^T*Y, B^T*Omega, ...).
+//
+// tcgen05.mma has no FP64 kind on sm_100a, so the FP64 tensor path is the
+// warp-level mma.sync.m16n8k4.f64 (SASS DMMA.8x8x4). Tiles are staged
+// global -> shared with multi-stage cp.async (LDGSTS) pipelines; every shared
+// tile uses a leading dimension == 4 (mod 16) doubles, which makes all four
+// operand layouts' fragment loads bank-conflict free. Split-K partials are
+// reduced in a fixed order, so results are bitwise reproducible run to run.
+
+#include "gemm.cuh"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace qbgpu {
+
+namespace {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+template <int VEC>
+__device__ __forceinline__ void cp_async(double* dst, const double* src, int valid) {
+    // valid = number of doubles to fetch (0..VEC); the rest is zero-filled.
+    const unsigned d = smem_u32(dst);
+    if constexpr (VEC == 2) {
+        const int bytes = valid * 8;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+    } else {
+        const int bytes = valid * 8;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+    }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%0,%1,%2,%3};\n"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a0), "d"(a1), "d"(b0));
+}
+
+constexpr int pad_to4(int base) { return ((4 - base % 16) + 16) % 16; }
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR>
+struct Tile {
+    static constexpr int NT = WM * WN * 32;
+    static constexpr int WTM = BM / WM, WTN = BN / WN;
+    static constexpr int MI = WTM / 16, NI = WTN / 8;
+    // A shared tile: AR ? [BM][LDA] (m-major) : [BK][LDA] (k-major)
+    static constexpr int A_INNER = AR ? BK : BM;
+    static constexpr int A_OUTER = AR ? BM : BK;
+    static constexpr int LDA = A_INNER + pad_to4(A_INNER);
+    // B shared tile: BR ? [BK][LDB] (k-major) : [BN][LDB] (n-major)
+    static constexpr int B_INNER = BR ? BN : BK;
+    static constexpr int B_OUTER = BR ? BK : BN;
+    static constexpr int LDB = B_INNER + pad_to4(B_INNER);
+    static constexpr int A_STAGE = A_OUTER * LDA;
+    static constexpr int B_STAGE = B_OUTER * LDB;
+    static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
+    static_assert(WTM % 16 == 0 && WTN % 8 == 0 && BK % 4 == 0, "tile shape");
+    static_assert(LDA % 16 == 4 && LDB % 16 == 4, "conflict-free leading dims");
+};
+
+// Loads one (A_OUTER x A_INNER) or (B_OUTER x B_INNER) tile: `outer` segments of
+// `inner` contiguous doubles. Segment s starts at base + s*seg_stride (global);
+// element e of a segment is valid while (inner0 + e) < inner_lim and the
+// segment index (outer0 + s) < outer_lim.
+template <int OUTER, int INNER, int LDS, int NT, int VEC>
+__device__ __forceinline__ void load_tile(double* smem, const double* __restrict__ base,
+                                          std::int64_t seg_stride, std::int64_t inner0,
+                                          std::int64_t inner_lim, std::int64_t outer0,
+                                          std::int64_t outer_lim) {
+    constexpr int CH_PER_SEG = INNER / VEC;
+    constexpr int CHUNKS = OUTER * CH_PER_SEG;
+#pragma unroll
+    for (int it = 0; it < (CHUNKS + NT - 1) / NT; ++it) {
+        const int idx = threadIdx.x + it * NT;
+        if ((CHUNKS % NT) != 0 && idx >= CHUNKS) break;
+        const int s = idx / CH_PER_SEG;
+        const int e = (idx % CH_PER_SEG) * VEC;
+        const std::int64_t gi = inner0 + e;
+        const std::int64_t go = outer0 + s;
+        int valid = 0;
+        if (go < outer_lim) {
+            const std::int64_t rem = inner_lim - gi;
+            valid = rem >= VEC ? VEC : (rem > 0 ? static_cast<int>(rem) : 0);
+        }
+        const double* src = valid ? base + static_cast<std::int64_t>(s) * seg_stride + e : base;
+        cp_async<VEC>(smem + s * LDS + e, src, valid);
+    }
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int VEC>
+__global__ void __launch_bounds__(WM * WN * 32)
+dgemm_kernel(const double* __restrict__ A, std::int64_t lda, const double* __restrict__ B,
+             std::int64_t ldb, double* __restrict__ C, std::int64_t ldc, int c_row, int M, int N,
+             int K, int k_split_len, double alpha, double beta, double* __restrict__ partial) {
+    using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
+    extern __shared__ __align__(16) double smem[];
+    double* sA = smem;
+    double* sB = smem + STAGES * T::A_STAGE;
+
+    const int m0 = blockIdx.x * BM;
+    const int n0 = blockIdx.y * BN;
+    const int kz = blockIdx.z;
+    const int k_begin = kz * k_split_len;
+    const int k_end = min(K, k_begin + k_split_len);
+    const int ntiles = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp % WM, wn = warp / WM;
+    const int g = lane >> 2, t = lane & 3;
+
+    double acc[T::MI][T::NI][4];
+#pragma unroll
+    for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+
+    auto issue = [&](int stage, int kt) {
+        const int k0 = k_begin + kt * BK;
+        double* a_dst = sA + stage * T::A_STAGE;
+        double* b_dst = sB + stage * T::B_STAGE;
+        if constexpr (AR) {  // A(i,k) = A[i*lda + k]: BM segments (rows) of BK
+            load_tile<BM, BK, T::LDA, T::NT, VEC>(a_dst, A + static_cast<std::int64_t>(m0) * lda + k0,
+                                                  lda, k0, k_end, m0, M);
+        } else {             // A(i,k) = A[i + k*lda]: BK segments (columns) of BM
+            load_tile<BK, BM, T::LDA, T::NT, VEC>(a_dst, A + m0 + static_cast<std::int64_t>(k0) * lda,
+                                                  lda, m0, M, k0, k_end);
+        }
+        if constexpr (BR) {  // B(k,j) = B[k*ldb + j]: BK segments of BN
+            load_tile<BK, BN, T::LDB, T::NT, VEC>(b_dst, B + static_cast<std::int64_t>(k0) * ldb + n0,
+                                                  ldb, n0, N, k0, k_end);
+        } else {             // B(k,j) = B[k + j*ldb]: BN segments of BK
+            load_tile<BN, BK, T::LDB, T::NT, VEC>(b_dst, B + k0 + static_cast<std::int64_t>(n0) * ldb,
+                                                  ldb, k0, k_end, n0, N);
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ntiles) issue(s, s);
+        cp_async_commit();
+    }
+
+    for (int kt = 0; kt < ntiles; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int nk = kt + STAGES - 1;
+            if (nk < ntiles) issue(nk % STAGES, nk);
+            cp_async_commit();
+        }
+        const double* a_s = sA + (kt % STAGES) * T::A_STAGE;
+        const double* b_s = sB + (kt % STAGES) * T::B_STAGE;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[T::MI][2];
+            double bf[T::NI];
+#pragma unroll
+            for (int i = 0; i < T::MI; ++i) {
+                const int r = wm * T::WTM + i * 16 + g;
+                if constexpr (AR) {
+                    af[i][0] = a_s[r * T::LDA + kk + t];
+                    af[i][1] = a_s[(r + 8) * T::LDA + kk + t];
+                } else {
+                    af[i][0] = a_s[(kk + t) * T::LDA + r];
+                    af[i][1] = a_s[(kk + t) * T::LDA + r + 8];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < T::NI; ++j) {
+                const int c = wn * T::WTN + j * 8 + g;
+                if constexpr (BR) bf[j] = b_s[(kk + t) * T::LDB + c];
+                else bf[j] = b_s[c * T::LDB + kk + t];
+            }
+#pragma unroll
+            for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                for (int j = 0; j < T::NI; ++j) dmma_16x8x4(acc[i][j], af[i][0], af[i][1], bf[j]);
+        }
+    }
+    cp_async_wait<0>();
+
+    // Epilogue: C fragment rows g / g+8, cols 2t / 2t+1.
+#pragma unroll
+    for (int i = 0; i < T::MI; ++i) {
+#pragma unroll
+        for (int j = 0; j < T::NI; ++j) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int row = m0 + wm * T::WTM + i * 16 + g + (r >= 2 ? 8 : 0);
+                const int col = n0 + wn * T::WTN + j * 8 + 2 * t + (r & 1);
+                if (row < M && col < N) {
+                    if (partial) {
+                        partial[static_cast<std::int64_t>(kz) * M * N + row +
+                                static_cast<std::int64_t>(col) * M] = acc[i][j][r];
+                    } else {
+                        double* cp = c_row ? C + static_cast<std::int64_t>(row) * ldc + col
+                                           : C + row + static_cast<std::int64_t>(col) * ldc;
+                        const double v = alpha * acc[i][j][r];
+                        *cp = beta == 0.0 ? v : v + beta * (*cp);
+                    }
+                }
+            }
+        }
+    }
+}
+
+__global__ void splitk_reduce_kernel(const double* __restrict__ partial, int splits, int M, int N,
+                                     double alpha, double beta, double* __restrict__ C,
+                                     std::int64_t ldc, int c_row) {
+    const std::int64_t total = static_cast<std::int64_t>(M) * N;
+    for (std::int64_t idx = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+         idx < total; idx += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int z = 0; z < splits; ++z) s += partial[z * total + idx];  // fixed order
+        const std::int64_t row = idx % M, col = idx / M;
+        double* cp = c_row ? C + row * ldc + col : C + row + col * ldc;
+        const double v = alpha * s;
+        *cp = beta == 0.0 ? v : v + beta * (*cp);
+    }
+}
+
+struct Launch {
+    int bm, bn, bk;
+    int threads;
+    int smem;
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int VEC>
+void launch_cfg(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc,
+                bool c_row, int M, int N, int K, int splits, int klen, double alpha, double beta,
+                double* partial) {
+    using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
+    auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, AR, BR, VEC>;
+    static bool configured = false;  // per template instance
+    if (!configured) {
+        QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES));
+        configured = true;
+    }
+    dim3 grid(static_cast<unsigned>(ceil_div(M, BM)), static_cast<unsigned>(ceil_div(N, BN)),
+              static_cast<unsigned>(splits));
+    kern<<<grid, T::NT, T::SMEM_BYTES, st>>>(a.p, a.ld, b.p, b.ld, c, ldc, c_row ? 1 : 0, M, N, K,
+                                            klen, alpha, beta, partial);
+    QB_LAUNCH_CHECK();
+}
+
+// Tile families. "wide": 128x128 CTA tiles (warp 64x32) for the passes over A at
+// large widths; "skinny": 128x64 (warp 32x32) for widths ~50-100; "narrow":
+// 64x32 for the thinnest products (b = 20, Gram-like outputs).
+enum class Family { kWide, kSkinny, kNarrow };
+
+template <Family F, bool AR, bool BR, int VEC>
+void launch_family(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc,
+                   bool c_row, int M, int N, int K, int splits, int klen, double alpha, double beta,
+                   double* partial) {
+    if constexpr (F == Family::kWide)
+        launch_cfg<128, 128, 16, 2, 4, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
+                                                       alpha, beta, partial);
+    else if constexpr (F == Family::kSkinny)
+        launch_cfg<128, 64, 16, 4, 2, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
+                                                      alpha, beta, partial);
+    else
+        launch_cfg<64, 32, 32, 2, 2, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
+                                                     alpha, beta, partial);
+}
+
+template <Family F>
+void dispatch_layout(cudaStream_t st, const MatView& a, const MatView& b, double* c,
+                     std::int64_t ldc, bool c_row, int M, int N, int K, int splits, int klen,
+                     double alpha, double beta, double* partial, bool vec2) {
+#define QB_DISPATCH(AR_, BR_)                                                                    \
+    if (vec2) launch_family<F, AR_, BR_, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, \
+                                            beta, partial);                                      \
+    else launch_family<F, AR_, BR_, 1>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, \
+                                       partial);
+    if (a.rowmajor) {
+        if (b.rowmajor) { QB_DISPATCH(true, true) } else { QB_DISPATCH(true, false) }
+    } else {
+        if (b.rowmajor) { QB_DISPATCH(false, true) } else { QB_DISPATCH(false, false) }
+    }
+#undef QB_DISPATCH
+}
+
+bool aligned16(const MatView& v) {
+    return (reinterpret_cast<std::uintptr_t>(v.p) % 16 == 0) && (v.ld % 2 == 0);
+}
+
+}  // namespace
+
+int gemm_num_sms() {
+    static int sms = [] {
+        int dev = 0, n = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n;
+    }();
+    return sms;
+}
+
+void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const MatView& b,
+          double beta, const MatView& c) {
+    const std::int64_t M = a.rows, K = a.cols, N = b.cols;
+    if (b.rows != K || c.rows != M || c.cols != N)
+        throw QbError(kDimensionError, "gemm: inner dimension mismatch");
+    if (M == 0 || N == 0) return;
+    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+        throw QbError(kDimensionError, "gemm: dimension exceeds 2^31");
+    if (K == 0) {
+        // C = beta*C
+        scale_matrix(st, c, beta);
+        return;
+    }
+    Family fam;
+    int bm, bn, bk;
+    if (N >= 96) { fam = Family::kWide; bm = 128; bn = 128; bk = 16; }
+    else if (N > 32) { fam = Family::kSkinny; bm = 128; bn = 64; bk = 16; }
+    else { fam = Family::kNarrow; bm = 64; bn = 32; bk = 32; }
+    const std::int64_t tiles = ceil_div(M, bm) * ceil_div(N, bn);
+    const int sms = gemm_num_sms();
+    // Resident CTAs per SM ~1 for the wide/skinny tiles, ~3 for narrow.
+    const std::int64_t want = (fam == Family::kNarrow ? 3 : 1) * static_cast<std::int64_t>(sms);
+    int splits = 1;
+    if (tiles < want) {
+        const std::int64_t max_by_k = std::max<std::int64_t>(1, K / (4 * bk));  // >= 4 k-tiles/split
+        splits = static_cast<int>(std::min<std::int64_t>(std::min<std::int64_t>(ceil_div(want, tiles), max_by_k), 64));
+    }
+    int klen = static_cast<int>(round_up(ceil_div(K, splits), bk));
+    splits = static_cast<int>(ceil_div(K, klen));
+    double* partial = nullptr;
+    if (splits > 1) partial = ws.get(static_cast<std::size_t>(splits) * M * N);
+    const bool vec2 = aligned16(a) && aligned16(b);
+    switch (fam) {
+        case Family::kWide:
+            dispatch_layout<Family::kWide>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits,
+                                           klen, alpha, beta, partial, vec2);
+            break;
+        case Family::kSkinny:
+            dispatch_layout<Family::kSkinny>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K,
+                                             splits, klen, alpha, beta, partial, vec2);
+            break;
+        default:
+            dispatch_layout<Family::kNarrow>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K,
+                                             splits, klen, alpha, beta, partial, vec2);
+    }
+    if (splits > 1) {
+        const std::int64_t total = M * N;
+        const int threads = 256;
+        const int blocks = static_cast<int>(std::min<std::int64_t>(ceil_div(total, threads), 4L * sms * 8));
+        splitk_reduce_kernel<<<blocks, threads, 0, st>>>(partial, splits, (int)M, (int)N, alpha, beta,
+                                                         c.p, c.ld, c.rowmajor ? 1 : 0);
+        QB_LAUNCH_CHECK();
+    }
+}
+
+}  // namespace qbgpu

@@ -1,0 +1,92 @@
+// Device-side building blocks of the qbfac B200 path: FP64 DMMA GEMM, small
+// dense kernels (CholQR pieces, indicator), reductions. See gemm.cu / small.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace qbgpu {
+
+// Growable device scratch buffer (never shrinks; freed with its owner).
+struct Workspace {
+    double* ptr = nullptr;
+    std::size_t cap = 0;  // doubles
+    double* get(std::size_t n) {
+        if (n > cap) {
+            if (ptr) QB_CUDA(cudaFree(ptr));
+            ptr = nullptr;
+            cap = 0;
+            std::size_t want = n + n / 4 + 1024;
+            QB_CUDA(cudaMalloc(&ptr, want * sizeof(double)));
+            cap = want;
+        }
+        return ptr;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+    ~Workspace() { release(); }
+};
+
+int gemm_num_sms();
+
+// C = alpha * A * B + beta * C, all FP64 views in device memory (any layouts).
+// beta == 0 never reads C. Deterministic (fixed split-K reduction order).
+void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const MatView& b,
+          double beta, const MatView& c);
+
+// ---- small.cu -------------------------------------------------------------------
+void scale_matrix(cudaStream_t st, const MatView& c, double beta);
+void copy_matrix(cudaStream_t st, const MatView& src, const MatView& dst);  // dst = src (any layouts)
+void set_identity(cudaStream_t st, const MatView& c);
+void add_matrix(cudaStream_t st, const MatView& src, const MatView& dst, double alpha);  // dst += alpha*src
+
+// out[0] = sum of squares of all entries of v (deterministic two-stage tree).
+void sum_squares(cudaStream_t st, Workspace& ws, const MatView& v, double* out);
+void sum_squares_vec(cudaStream_t st, Workspace& ws, const double* x, std::int64_t n, double* out);
+// out[j] = sum_i v(i,j)^2 for j < v.cols (deterministic).
+void column_sumsq(cudaStream_t st, Workspace& ws, const MatView& v, double* out);
+
+// Small dense factorization status written by chol_small / cholqr checks.
+struct SmallStatus {
+    int breakdown;        // 1 if Cholesky met a non-positive pivot
+    int bad_index;        // first failing pivot index
+    double diag_min;      // min_j R(j,j)
+    double diag_max;      // max_j R(j,j)
+    double gram_dev;      // max |G(i,j) - delta_ij| of the input Gram (orthogonality of input)
+};
+
+// b x b Gram G (col-major, ld) -> R = chol(G) upper (col-major ldr), Rinv = R^{-1}
+// (upper, col-major). One CTA. b <= kSmallMax.
+constexpr int kSmallMax = 112;  // chol_small keeps [G | I] (b x 2b) in shared memory
+void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, double* r,
+                double* rinv, std::int64_t ldr, SmallStatus* status);
+// C = A * B for upper-triangular b x b (col-major, ld); C must not alias.
+void trmm_upper_small(cudaStream_t st, const double* a, const double* b, double* c, int n,
+                      std::int64_t ld);
+// Rinv = R^{-1} for upper-triangular R (one CTA).
+void tri_inverse_small(cudaStream_t st, const double* r, double* rinv, int n, std::int64_t ld);
+
+// Error-indicator step: for j < b: E -= norms[j]; if check and
+// E < eps2 stop after row j. Writes the new E and the kept row count.
+struct IndicatorOut {
+    double e;
+    int keep;
+    int met;
+};
+void indicator_step(cudaStream_t st, double* e_dev, const double* norms, int b, double eps2,
+                    int check, IndicatorOut* out);
+
+// Householder economic QR of a column-major m x b panel (b <= kSmallMax), diag(R) >= 0:
+// the exact-semantics fallback when CholQR is unreliable. y is overwritten by Q.
+// Cooperative grid; deterministic reductions.
+void householder_panel(cudaStream_t st, Workspace& ws, double* y, std::int64_t m, int b,
+                       std::int64_t ld, double* r, std::int64_t ldr);
+
+}  // namespace qbgpu

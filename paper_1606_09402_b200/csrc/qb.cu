@@ -1,0 +1,645 @@
+// Device drivers of randQB_EI / randQB_FP / single pass on B200.
+//
+// Reference semantics (the reference's src/qb.cpp is missing; restated from
+// /root/reference/SPEC.md:204-363 and PAPER.md, identically to oracle/qb_restated.cpp):
+//   randQB_EI  Alg. 2, with per-block power iteration
+//   randQB_FP  Alg. 4, steps 9a-9c PAPER.md:441-447, restarts SPEC.md:347
+//   Alg. 3     PAPER.md:352-376 (fixed rank), single pass Remark 4.2 PAPER.md:466-467
+//   row-by-row error indicator PAPER.md:206-220, validate_epsilon SPEC.md:327-335
+//
+// Everything between the upload of A and the copy-out of Q/B runs on the GPU:
+// Omega is generated on the device from the reference's stream, the passes over
+// A are DMMA GEMMs (dense) or CSR SpMM (sparse), orth() is CholQR2 with a
+// Householder-panel fallback (same Q, R as the reference's Householder QR with
+// diag(R) >= 0 up to rounding; rank-collapse decisions are taken on the
+// Householder R), and the indicator E -= ||B_i(j,:)||^2 with the row truncation
+// runs in a device kernel. The host only reads a few status words per block.
+//
+// Layouts: A dense column-major (lda padded to a multiple of 8); every block vector
+// (Omega_i, Y_i, Q_i, B_i^T, G, H) and the accumulated Q (m x cap) and B^T (n x cap)
+// are row-major, so CSR passes gather contiguous rows and appending a block is a
+// write into a column slot.
+
+#include "qb.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace qbgpu {
+
+std::atomic<long long> g_kernel_launches{0};
+
+namespace {
+
+constexpr double kRankTol = 1e-12;
+constexpr double kEpsMach = 1.1102230246251565e-16;  // types.hpp:14
+constexpr double kCholRatioMin = 1e-7;      // below: CholQR R not trusted -> Householder
+constexpr double kCholGramDevMax = 0.5;     // second CholQR pass must see a near-identity Gram
+constexpr int kSlot = kSmallMax * kSmallMax;
+enum SmallSlot { kG = 0, kRa, kRainv, kRb, kRbinv, kR1, kR1inv, kR2, kR2inv, kR, kRinv, kTmp, kNorms, kNumSlots };
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------
+Context::Context(int dev, int rank_, int world_, const void* nccl_id) : device(dev), rank(rank_), world(world_) {
+    QB_CUDA(cudaSetDevice(dev));
+    cudaDeviceProp prop{};
+    QB_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+        throw QbError(kError, std::string("qbfac_gpu needs an sm_100 (B200) device, found ") + prop.name);
+    sms = prop.multiProcessorCount;
+    QB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    QB_CUDA(cudaMalloc(&d_small, sizeof(double) * kSlot * kNumSlots + 64 * sizeof(double)));
+    QB_CUDA(cudaMalloc(&d_status, sizeof(SmallStatus) * 4));
+    QB_CUDA(cudaMalloc(&d_ind, sizeof(IndicatorOut)));
+    QB_CUDA(cudaMallocHost(&h_status, sizeof(SmallStatus) * 4));
+    QB_CUDA(cudaMallocHost(&h_ind, sizeof(IndicatorOut)));
+    QB_CUDA(cudaMallocHost(&h_scalar, sizeof(double) * 8));
+    // Grow the stream-ordered pool's retention so per-run buffers are reused.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        std::uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    rng.device();
+    if (world > 1) comm = std::make_unique<Comm>(rank, world, nccl_id);
+}
+
+Context::~Context() {
+    cudaSetDevice(device);
+    if (st) cudaStreamSynchronize(st);
+    comm.reset();
+    ws_gemm.release();
+    ws_red.release();
+    ws_hh.release();
+    if (d_small) cudaFree(d_small);
+    if (d_status) cudaFree(d_status);
+    if (d_ind) cudaFree(d_ind);
+    if (h_status) cudaFreeHost(h_status);
+    if (h_ind) cudaFreeHost(h_ind);
+    if (h_scalar) cudaFreeHost(h_scalar);
+    if (st) cudaStreamDestroy(st);
+}
+
+Matrix::~Matrix() {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (a && owns_a) cudaFree(a);
+    if (rp) cudaFree(rp);
+    if (ci) cudaFree(ci);
+    if (v) cudaFree(v);
+    if (ct_rp) cudaFree(ct_rp);
+    if (ct_ci) cudaFree(ct_ci);
+    if (ct_v) cudaFree(ct_v);
+}
+
+std::unique_ptr<Matrix> make_dense(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
+                                   std::int64_t n, const double* a, std::int64_t lda, bool device_src) {
+    if (m < 0 || n < 0 || lda < std::max<std::int64_t>(1, m))
+        throw QbError(kDimensionError, "matrix_dense: bad dimensions");
+    auto mat = std::make_unique<Matrix>();
+    mat->ctx = &c;
+    mat->m = m;
+    mat->n = n;
+    mat->m_global = m_global;
+    mat->row0 = row0;
+    mat->lda = std::max<std::int64_t>(8, round_up(m, 8));
+    QB_CUDA(cudaMalloc(&mat->a, sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1)));
+    if (mat->lda != m) QB_CUDA(cudaMemsetAsync(mat->a, 0, sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1), c.st));
+    if (m > 0 && n > 0)
+        QB_CUDA(cudaMemcpy2DAsync(mat->a, mat->lda * sizeof(double), a, lda * sizeof(double), m * sizeof(double), n,
+                                  device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.st));
+    // DenseMatrix::from_data rejects non-finite entries (dense_matrix.cpp:17-18).
+    if (m > 0 && n > 0) {
+        sum_squares(c.st, c.ws_red, mat->dense_view(), c.d_small + kSlot * kNumSlots);
+        QB_CUDA(cudaMemcpyAsync(c.h_scalar, c.d_small + kSlot * kNumSlots, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    }
+    QB_CUDA(cudaStreamSynchronize(c.st));
+    if (m > 0 && n > 0 && !std::isfinite(c.h_scalar[0])) throw QbError(kError, "from_data: non-finite entry");
+    return mat;
+}
+
+std::unique_ptr<Matrix> make_csr(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
+                                 std::int64_t n, std::int64_t nnz, const std::int64_t* rp, const std::int32_t* ci,
+                                 const double* v) {
+    if (n > static_cast<std::int64_t>(INT32_MAX))
+        throw QbError(kDimensionError, "csr: column count exceeds 32-bit index range");
+    if (m < 0 || n < 0 || nnz < 0) throw QbError(kFormatError, "csr: inconsistent structure arrays");
+    auto mat = std::make_unique<Matrix>();
+    mat->ctx = &c;
+    mat->sparse = true;
+    mat->m = m;
+    mat->n = n;
+    mat->m_global = m_global;
+    mat->row0 = row0;
+    mat->nnz = nnz;
+    QB_CUDA(cudaMalloc(&mat->rp, sizeof(std::int64_t) * (m + 1)));
+    QB_CUDA(cudaMalloc(&mat->ci, sizeof(std::int32_t) * std::max<std::int64_t>(nnz, 1)));
+    QB_CUDA(cudaMalloc(&mat->v, sizeof(double) * std::max<std::int64_t>(nnz, 1)));
+    QB_CUDA(cudaMalloc(&mat->ct_rp, sizeof(std::int64_t) * (n + 1)));
+    QB_CUDA(cudaMalloc(&mat->ct_ci, sizeof(std::int32_t) * std::max<std::int64_t>(nnz, 1)));
+    QB_CUDA(cudaMalloc(&mat->ct_v, sizeof(double) * std::max<std::int64_t>(nnz, 1)));
+    QB_CUDA(cudaMemcpyAsync(mat->rp, rp, sizeof(std::int64_t) * (m + 1), cudaMemcpyHostToDevice, c.st));
+    if (nnz > 0) {
+        QB_CUDA(cudaMemcpyAsync(mat->ci, ci, sizeof(std::int32_t) * nnz, cudaMemcpyHostToDevice, c.st));
+        QB_CUDA(cudaMemcpyAsync(mat->v, v, sizeof(double) * nnz, cudaMemcpyHostToDevice, c.st));
+    }
+    const int flags = csr_validate(c.st, m, n, nnz, mat->rp, mat->ci, mat->v, c.sms);
+    if (flags & 1) throw QbError(kFormatError, "csr: invalid structure (row_ptr / column indices)");
+    if (flags & 2) throw QbError(kError, "csr: non-finite value");
+    csr_transpose(c.st, m, n, nnz, mat->rp, mat->ci, mat->v, mat->ct_rp, mat->ct_ci, mat->ct_v, c.sms);
+    QB_CUDA(cudaStreamSynchronize(c.st));
+    return mat;
+}
+
+// ---------------------------------------------------------------------------------
+namespace {
+
+class Engine {
+public:
+    Engine(Context& c, Matrix& a) : c_(c), a_(a), st_(c.st) {}
+
+    double* slot(int s) const { return c_.d_small + static_cast<std::size_t>(s) * kSlot; }
+    MatView small(int s, std::int64_t r, std::int64_t cc) const { return MatView{slot(s), r, cc, kSmallMax, false}; }
+
+    void gemm(double alpha, const MatView& a, const MatView& b, double beta, const MatView& c) {
+        qbgpu::gemm(st_, c_.ws_gemm, alpha, a, b, beta, c);
+    }
+
+    // Y (m x w) = A X (X: n x w). Dense: DMMA GEMM; sparse: CSR SpMM.
+    void apply(const MatView& x, const MatView& y, double alpha = 1.0, double beta = 0.0) {
+        if (a_.sparse) {
+            if (!x.rowmajor || !y.rowmajor) throw QbError(kInternal, "sparse pass needs row-major blocks");
+            csr_spmm(st_, a_.csr(), x.p, x.ld, y.p, y.ld, static_cast<int>(x.cols), alpha, beta, c_.sms);
+        } else {
+            gemm(alpha, a_.dense_view(), x, beta, y);
+        }
+    }
+    // Y (n x w) = A^T X (X: m x w), summed over ranks.
+    void apply_t(const MatView& x, const MatView& y) {
+        const bool contiguous = (y.rowmajor && y.ld == y.cols) || (!y.rowmajor && y.ld == y.rows);
+        if (c_.world > 1 && !contiguous) {
+            // allreduce needs a packed buffer: compute there, reduce, scatter into y
+            if (scratch_t_.n < static_cast<std::size_t>(y.rows * y.cols))
+                scratch_t_ = DBuf(static_cast<std::size_t>(y.rows * y.cols), st_);
+            MatView t{scratch_t_.p, y.rows, y.cols, y.cols, true};
+            apply_t(x, t);
+            copy_matrix(st_, t, y);
+            return;
+        }
+        if (a_.sparse) {
+            if (!x.rowmajor || !y.rowmajor) throw QbError(kInternal, "sparse pass needs row-major blocks");
+            csr_spmm(st_, a_.csr_t(), x.p, x.ld, y.p, y.ld, static_cast<int>(x.cols), 1.0, 0.0, c_.sms);
+        } else {
+            gemm(1.0, a_.dense_view().t(), x, 0.0, y);
+        }
+        allreduce_view(y);
+    }
+    void allreduce_view(const MatView& y) {
+        if (c_.world == 1) return;
+        if (!(y.rowmajor && y.ld == y.cols) && !(!y.rowmajor && y.ld == y.rows))
+            throw QbError(kInternal, "allreduce needs a contiguous view");
+        c_.allreduce(y.p, static_cast<std::size_t>(y.rows * y.cols));
+    }
+
+    double frob_device(double* out) {  // ||A||_F^2 into device scalar `out` (+ allreduce)
+        if (a_.sparse) sum_squares_vec(st_, c_.ws_red, a_.v, a_.nnz, out);
+        else sum_squares(st_, c_.ws_red, a_.dense_view(), out);
+        c_.allreduce(out, 1);
+        QB_CUDA(cudaMemcpyAsync(c_.h_scalar, out, sizeof(double), cudaMemcpyDeviceToHost, st_));
+        QB_CUDA(cudaStreamSynchronize(st_));
+        return c_.h_scalar[0];
+    }
+
+    // orth(Y): Q (rows x b, may alias Y) and upper R (slot r_slot) with inverse
+    // (slot rinv_slot), such that Y = Q R, diag(R) > 0. `sharded`: rows are split over
+    // ranks (Grams are allreduced). Returns the leading rank d (first index with
+    // R_jj <= 1e-12 max R_jj, qr.hpp:20-21), b when full rank.
+    int orth_block(const MatView& y, const MatView& qout, int r_slot, int rinv_slot, bool sharded, DBuf& tmp) {
+        const int b = static_cast<int>(y.cols);
+        const std::int64_t rows = y.rows;
+        if (b == 0) return 0;
+        if (b > kSmallMax) throw QbError(kDimensionError, "block size exceeds the device panel limit (112)");
+        MatView t1{tmp.p, rows, b, b, true};
+        // pass 1
+        gemm(1.0, y.t(), y, 0.0, small(kG, b, b));
+        if (sharded) c_.allreduce(slot(kG), kSlot);
+        chol_small(st_, slot(kG), kSmallMax, b, slot(kRa), slot(kRainv), kSmallMax, c_.d_status + 0);
+        gemm(1.0, y, small(kRainv, b, b), 0.0, t1);
+        // pass 2
+        gemm(1.0, t1.t(), t1, 0.0, small(kG, b, b));
+        if (sharded) c_.allreduce(slot(kG), kSlot);
+        chol_small(st_, slot(kG), kSmallMax, b, slot(kRb), slot(kRbinv), kSmallMax, c_.d_status + 1);
+        QB_CUDA(cudaMemcpyAsync(c_.h_status, c_.d_status, sizeof(SmallStatus) * 2, cudaMemcpyDeviceToHost, st_));
+        QB_CUDA(cudaStreamSynchronize(st_));
+        const SmallStatus s0 = c_.h_status[0], s1 = c_.h_status[1];
+        const bool ok = !s0.breakdown && !s1.breakdown && s0.diag_max > 0.0 &&
+                        s0.diag_min >= kCholRatioMin * s0.diag_max && s1.gram_dev <= kCholGramDevMax &&
+                        std::isfinite(s0.diag_max) && std::isfinite(s1.diag_max);
+        if (ok) {
+            gemm(1.0, t1, small(kRbinv, b, b), 0.0, qout);
+            trmm_upper_small(st_, slot(kRb), slot(kRa), slot(r_slot), b, kSmallMax);
+            trmm_upper_small(st_, slot(kRainv), slot(kRbinv), slot(rinv_slot), b, kSmallMax);
+            return b;
+        }
+        // Householder fallback: exact deficiency decisions (qr.hpp:15-21).
+        if (sharded && c_.world > 1)
+            throw QbError(kError, "numerically rank-deficient sketch under row sharding (Householder panel "
+                                  "fallback is single-GPU)");
+        ++hh_fallbacks;
+        MatView ycol{t1.p, rows, b, std::max<std::int64_t>(rows, 1), false};
+        copy_matrix(st_, y, ycol);
+        householder_panel(st_, c_.ws_hh, ycol.p, rows, b, ycol.ld, slot(r_slot), kSmallMax);
+        std::vector<double> rh(static_cast<std::size_t>(kSlot));
+        QB_CUDA(cudaMemcpyAsync(rh.data(), slot(r_slot), sizeof(double) * kSlot, cudaMemcpyDeviceToHost, st_));
+        QB_CUDA(cudaStreamSynchronize(st_));
+        double mx = 0.0;
+        for (int j = 0; j < b; ++j) mx = std::max(mx, std::fabs(rh[j + j * kSmallMax]));
+        int d = b;
+        for (int j = 0; j < b; ++j)
+            if (std::fabs(rh[j + j * kSmallMax]) <= kRankTol * mx) { d = j; break; }
+        copy_matrix(st_, ycol, qout);
+        if (d > 0) tri_inverse_small(st_, slot(r_slot), slot(rinv_slot), d, kSmallMax);
+        return d;
+    }
+
+    // Orthonormal basis of the leading-column spans of X (rows x l) in place:
+    // block Gram-Schmidt with re-orthogonalisation (BCGS2) over CholQR2 panels.
+    void orth_wide(const MatView& x, bool sharded, DBuf& tmp, DBuf& sbuf) {
+        const std::int64_t l = x.cols;
+        const std::int64_t bw = 64;
+        for (std::int64_t j0 = 0; j0 < l; j0 += bw) {
+            const std::int64_t bj = std::min(bw, l - j0);
+            MatView xj = x.cols_range(j0, bj);
+            for (int rep = 0; rep < 2; ++rep) {
+                if (j0 > 0) {
+                    MatView prev = x.cols_range(0, j0);
+                    MatView s{sbuf.p, j0, bj, bj, true};
+                    gemm(1.0, prev.t(), xj, 0.0, s);
+                    if (sharded) allreduce_view(s);
+                    gemm(-1.0, prev, s, 1.0, xj);
+                }
+                orth_block(xj, xj, kR2, kR2inv, sharded, tmp);
+            }
+        }
+    }
+
+    std::int64_t hh_fallbacks = 0;
+
+private:
+    DBuf scratch_t_;
+    Context& c_;
+    Matrix& a_;
+    cudaStream_t st_;
+};
+
+struct Timer {
+    cudaEvent_t e0, e1;
+    cudaStream_t st;
+    explicit Timer(cudaStream_t s) : st(s) {
+        QB_CUDA(cudaEventCreate(&e0));
+        QB_CUDA(cudaEventCreate(&e1));
+        QB_CUDA(cudaEventRecord(e0, st));
+    }
+    double stop() {
+        QB_CUDA(cudaEventRecord(e1, st));
+        QB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        QB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        return ms;
+    }
+    ~Timer() {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+};
+
+void check_eps(double eps, double norm_a_sq) {
+    const double floor = std::sqrt(4.0 * kEpsMach / 0.01) * std::sqrt(norm_a_sq);
+    if (!(eps > floor)) {
+        QbError e(kToleranceFloorError, "epsilon below the Theorem 3 floor " + std::to_string(floor));
+        e.floor = floor;
+        throw e;
+    }
+}
+
+std::int64_t even(std::int64_t x) { return std::max<std::int64_t>(2, round_up(x, 2)); }
+
+// Shared state of one factorization.
+struct State {
+    Context& c;
+    Engine& eng;
+    std::int64_t m, n, cap, ld;
+    std::int64_t k = 0;
+    DBuf q, bt;
+    double* d_e;
+    double eps2 = 0.0;
+    std::vector<double> trace;
+
+    State(Context& cc, Engine& e, std::int64_t m_, std::int64_t n_, std::int64_t cap_)
+        : c(cc), eng(e), m(m_), n(n_), cap(cap_), ld(even(cap_)),
+          q(static_cast<std::size_t>(std::max<std::int64_t>(m_, 1)) * even(cap_), cc.st),
+          bt(static_cast<std::size_t>(std::max<std::int64_t>(n_, 1)) * even(cap_), cc.st),
+          d_e(cc.d_small + static_cast<std::size_t>(kSlot) * kNumSlots + 1) {}
+
+    MatView qk() const { return MatView{q.p, m, k, ld, true}; }
+    MatView btk() const { return MatView{bt.p, n, k, ld, true}; }
+    MatView qslot(std::int64_t w) const { return MatView{q.p + k, m, w, ld, true}; }
+    MatView btslot(std::int64_t w) const { return MatView{bt.p + k, n, w, ld, true}; }
+
+    // Rows of B_i enter E one by one. Returns (keep, met).
+    std::pair<int, bool> indicator(int d, bool check) {
+        double* norms = c.d_small + static_cast<std::size_t>(kNorms) * kSlot;
+        column_sumsq(c.st, c.ws_red, btslot(d), norms);
+        indicator_step(c.st, d_e, norms, d, eps2, check ? 1 : 0, c.d_ind);
+        QB_CUDA(cudaMemcpyAsync(c.h_ind, c.d_ind, sizeof(IndicatorOut), cudaMemcpyDeviceToHost, c.st));
+        QB_CUDA(cudaStreamSynchronize(c.st));
+        trace.push_back(c.h_ind->e);
+        return {c.h_ind->keep, c.h_ind->met != 0};
+    }
+    void set_e(double e) {
+        c.h_scalar[1] = e;
+        QB_CUDA(cudaMemcpyAsync(d_e, c.h_scalar + 1, sizeof(double), cudaMemcpyHostToDevice, c.st));
+        QB_CUDA(cudaStreamSynchronize(c.st));
+    }
+    double get_e() {
+        QB_CUDA(cudaMemcpyAsync(c.h_scalar + 2, d_e, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+        QB_CUDA(cudaStreamSynchronize(c.st));
+        return c.h_scalar[2];
+    }
+};
+
+std::unique_ptr<Result> finish(State& s, Matrix& a, std::int64_t passes0, int term, double norm_a_sq) {
+    auto r = std::make_unique<Result>();
+    r->ctx = &s.c;
+    r->m = s.m;
+    r->n = s.n;
+    r->rank = s.k;
+    r->ld = s.ld;
+    r->q = std::move(s.q);
+    r->bt = std::move(s.bt);
+    r->e = s.get_e();
+    r->norm_a_sq = norm_a_sq;
+    r->passes = a.passes - passes0;
+    r->terminated_by = term;
+    r->trace = s.trace;
+    return r;
+}
+
+// ---- randQB_EI ---------------------------------------------------------------------
+std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
+    if (p.b < 1) throw QbError(kDimensionError, "rand_qb_ei: block size must be >= 1");
+    Engine eng(c, a);
+    const std::int64_t m = a.m, n = a.n;
+    const std::int64_t mg = a.m_global;
+    const bool fixed_prec = p.mode == 1;
+    std::int64_t cap = std::min(mg, n);
+    if (fixed_prec) {
+        if (p.max_rank > 0) cap = std::min(cap, p.max_rank);
+    } else {
+        cap = std::min(cap, p.k + p.s);
+    }
+    const std::int64_t passes0 = a.passes;
+    State s(c, eng, m, n, cap);
+    const bool sharded = c.world > 1;
+    const double norm_a_sq = eng.frob_device(s.d_e);   // Alg. 2 step 2, +1 pass
+    a.passes += 1;
+    s.eps2 = p.eps_abs * p.eps_abs;
+    int term = 0;
+    std::int64_t g_used = 0, blocks = 0;
+    auto wrap = [&](int t) {
+        auto r = finish(s, a, passes0, t, norm_a_sq);
+        r->gaussians_used = g_used;
+        r->blocks = blocks;
+        r->hh_fallbacks = eng.hh_fallbacks;
+        return r;
+    };
+    if (fixed_prec) {
+        check_eps(p.eps_abs, norm_a_sq);
+        if (norm_a_sq < s.eps2) return wrap(1);
+    }
+    const std::int64_t bmax = std::min<std::int64_t>(p.b, std::max<std::int64_t>(cap, 1));
+    const std::int64_t bpad = even(bmax);
+    DBuf om(static_cast<std::size_t>(n) * bpad, c.st);
+    DBuf y(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * bpad, c.st);
+    DBuf tmp(static_cast<std::size_t>(std::max<std::int64_t>(std::max<std::int64_t>(m, n), 1)) * bpad, c.st);
+    DBuf z(p.power > 0 ? static_cast<std::size_t>(n) * bpad : 0, c.st);
+    DBuf mbuf(static_cast<std::size_t>(std::max<std::int64_t>(cap, 1)) * bpad, c.st);
+    while (true) {
+        if (s.k >= cap) { term = 0; break; }
+        const std::int64_t bi = std::min(p.b, cap - s.k);
+        ++blocks;
+        MatView omv{om.p, n, bi, bi, true};
+        gaussian_fill(c.st, c.rng, p.seed, p.stream, static_cast<std::uint64_t>(g_used), omv);  // step 4
+        g_used += n * bi;
+        MatView yv{y.p, m, bi, bi, true};
+        MatView mv{mbuf.p, s.k, bi, bi, true};
+        // step 5: Y = A Omega_i - Q (B Omega_i)
+        eng.apply(omv, yv); a.passes += 1;
+        if (s.k > 0) {
+            eng.gemm(1.0, s.btk().t(), omv, 0.0, mv);
+            eng.gemm(-1.0, s.qk(), mv, 1.0, yv);
+        }
+        // per-block power iteration with deflation at every application
+        for (std::int64_t it = 0; it < p.power; ++it) {
+            eng.orth_block(yv, yv, kR1, kR1inv, sharded, tmp);
+            MatView zv{z.p, n, bi, bi, true};
+            eng.apply_t(yv, zv); a.passes += 1;
+            if (s.k > 0) {
+                eng.gemm(1.0, s.qk().t(), yv, 0.0, mv);
+                eng.allreduce_view(mv);
+                eng.gemm(-1.0, s.btk(), mv, 1.0, zv);
+            }
+            eng.orth_block(zv, zv, kR1, kR1inv, false, tmp);
+            eng.apply(zv, yv); a.passes += 1;
+            if (s.k > 0) {
+                eng.gemm(1.0, s.btk().t(), zv, 0.0, mv);
+                eng.gemm(-1.0, s.qk(), mv, 1.0, yv);
+            }
+        }
+        // orth, then re-orthogonalisation against Q (step 6)
+        MatView qs = s.qslot(bi);
+        int d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp);
+        if (d == 0) { term = 3; break; }
+        if (s.k > 0) {
+            MatView qd = s.qslot(d);
+            MatView md{mbuf.p, s.k, d, d, true};
+            eng.gemm(1.0, s.qk().t(), qd, 0.0, md);
+            eng.allreduce_view(md);
+            eng.gemm(-1.0, s.qk(), md, 1.0, qd);
+            const int d2 = eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp);
+            if (d2 == 0) { term = 3; break; }
+            d = std::min(d, d2);
+        }
+        // step 7: B_i^T = A^T Q_i (+1 pass)
+        eng.apply_t(s.qslot(d), s.btslot(d));
+        a.passes += 1;
+        auto [keep, met] = s.indicator(d, fixed_prec);
+        s.k += keep;
+        if (met) { term = 1; break; }
+        if (d < bi) { term = 3; break; }
+    }
+    return wrap(term);
+}
+
+// ---- randQB_FP / fixed rank / single pass --------------------------------------------
+std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
+    if (p.b < 1) throw QbError(kDimensionError, "rand_qb_fp: block size must be >= 1");
+    Engine eng(c, a);
+    const std::int64_t m = a.m, n = a.n, mg = a.m_global;
+    const bool fixed = p.alg != 1;           // Alg. 3 / single pass: fixed rank l = k + s
+    const bool reorth = p.alg == 1 || p.alg == 3 || p.reorth;
+    std::int64_t cap = std::min(mg, n);
+    if (fixed) {
+        const std::int64_t l = p.k + p.s;
+        if (l < 1 || l > cap) throw QbError(kDimensionError, "rand_qb_fp_fixed_rank: bad l");
+        cap = l;
+    } else {
+        if (p.l_budget < p.b) throw QbError(kDimensionError, "rand_qb_fp: l_budget must be >= b");
+        if (p.max_rank > 0) cap = std::min(cap, p.max_rank);
+    }
+    const std::int64_t passes0 = a.passes;
+    State s(c, eng, m, n, cap);
+    const bool sharded = c.world > 1;
+    s.eps2 = fixed ? 0.0 : p.eps_abs * p.eps_abs;
+    double norm_a_sq = 0.0;
+    int term = 2;
+    std::int64_t g_used = 0, blocks = 0, restarts = 0;
+    auto wrap = [&](int t) {
+        auto r = finish(s, a, passes0, t, norm_a_sq);
+        r->gaussians_used = g_used;
+        r->blocks = blocks;
+        r->restarts = restarts;
+        r->hh_fallbacks = eng.hh_fallbacks;
+        if (p.alg == 3) r->passes = 1;  // one stream consumption
+        return r;
+    };
+    const std::int64_t lmax = fixed ? cap : std::min(p.l_budget, cap);
+    const std::int64_t lpad = even(lmax);
+    const std::int64_t bmax = std::min(p.b, lmax);
+    const std::int64_t bpad = even(bmax);
+    DBuf om(static_cast<std::size_t>(n) * lpad, c.st);
+    DBuf g(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * lpad, c.st);
+    DBuf h(static_cast<std::size_t>(n) * lpad, c.st);
+    DBuf y(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * bpad, c.st);
+    DBuf tmp(static_cast<std::size_t>(std::max<std::int64_t>(std::max<std::int64_t>(m, n), 1)) * bpad, c.st);
+    DBuf ct(static_cast<std::size_t>(n) * bpad, c.st);
+    DBuf m1(static_cast<std::size_t>(std::max<std::int64_t>(cap, 1)) * bpad, c.st);
+    DBuf m2(static_cast<std::size_t>(std::max<std::int64_t>(cap, std::max<std::int64_t>(lpad, 64))) * std::max<std::int64_t>(bpad, 64), c.st);
+    DBuf wtmp(p.power > 0 ? static_cast<std::size_t>(std::max<std::int64_t>(std::max<std::int64_t>(m, n), 1)) * 64 : 0, c.st);
+    for (int restart = 0;; ++restart) {
+        if (s.k >= cap) { term = 0; break; }
+        if (fixed && restart > 0) { term = 0; break; }
+        if (restart > p.max_restarts) { term = 2; break; }
+        if (restart > 0) ++restarts;
+        const std::int64_t l = fixed ? cap : std::min(p.l_budget, cap - s.k);
+        const std::uint64_t stream_id = restart == 0 ? p.stream : p.stream + 1 + static_cast<std::uint64_t>(restart);
+        MatView omv{om.p, n, l, l, true};
+        gaussian_fill(c.st, c.rng, p.seed, stream_id, 0, omv);                   // step 2
+        if (restart == 0) g_used = n * l;
+        MatView gv{g.p, m, l, l, true};
+        MatView hv{h.p, n, l, l, true};
+        for (std::int64_t it = 0; it < p.power; ++it) {                            // steps 3-6
+            eng.apply(omv, gv); a.passes += 1;
+            eng.orth_wide(gv, sharded, wtmp, m2);
+            eng.apply_t(gv, omv); a.passes += 1;
+            eng.orth_wide(omv, false, wtmp, m2);
+        }
+        eng.apply(omv, gv); a.passes += 1;                                         // step 7
+        if (restart == 0) {                                                        // step 9
+            norm_a_sq = eng.frob_device(s.d_e);  // same logical pass (multiply_with_norm)
+            if (!fixed) {
+                check_eps(p.eps_abs, norm_a_sq);
+                if (norm_a_sq < s.eps2) { term = 1; break; }
+            }
+        }
+        eng.apply_t(gv, hv); a.passes += 1;                                        // step 8
+        bool stop = false;
+        for (std::int64_t off = 0; off < l; off += p.b) {                          // steps 10-21
+            const std::int64_t bi = std::min(p.b, l - off);
+            ++blocks;
+            MatView omi = omv.cols_range(off, bi);
+            MatView gi = gv.cols_range(off, bi);
+            MatView hi = hv.cols_range(off, bi);
+            MatView yv{y.p, m, bi, bi, true};
+            MatView m1v{m1.p, s.k, bi, bi, true};
+            copy_matrix(c.st, gi, yv);
+            if (s.k > 0) {                                                         // step 12
+                eng.gemm(1.0, s.btk().t(), omi, 0.0, m1v);
+                eng.gemm(-1.0, s.qk(), m1v, 1.0, yv);
+            }
+            MatView qs = s.qslot(bi);
+            int d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp);            // step 13
+            if (d == 0) { term = 3; stop = true; break; }
+            int r_slot = kR1, rinv_slot = kR1inv;
+            if (reorth && s.k > 0) {                                               // steps 14-15 (9a-9b)
+                MatView qd = s.qslot(d);
+                MatView md{m2.p, s.k, d, d, true};
+                eng.gemm(1.0, s.qk().t(), qd, 0.0, md);
+                eng.allreduce_view(md);
+                eng.gemm(-1.0, s.qk(), md, 1.0, qd);
+                const int d2 = eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp);
+                if (d2 == 0) { term = 3; stop = true; break; }
+                d = std::min(d, d2);
+                trmm_upper_small(c.st, eng.slot(kR2), eng.slot(kR1), eng.slot(kR), d, kSmallMax);
+                trmm_upper_small(c.st, eng.slot(kR1inv), eng.slot(kR2inv), eng.slot(kRinv), d, kSmallMax);
+                r_slot = kR;
+                rinv_slot = kRinv;
+            }
+            (void)r_slot;
+            // step 16 (9c): B_i^T = (H_i - B^T (Q^T Y_i + B Omega_i)) R_i^{-1}
+            //   (Alg. 3 without re-orth: B_i^T = (H_i - B^T (B Omega_i)) R_i^{-1})
+            MatView ctv{ct.p, n, d, d, true};
+            copy_matrix(c.st, hi.cols_range(0, d), ctv);
+            if (s.k > 0) {
+                MatView mm{m2.p, s.k, d, d, true};
+                if (reorth) {
+                    eng.gemm(1.0, s.qk().t(), yv.cols_range(0, d), 0.0, mm);
+                    eng.allreduce_view(mm);
+                    add_matrix(c.st, m1v.cols_range(0, d), mm, 1.0);
+                } else {
+                    copy_matrix(c.st, m1v.cols_range(0, d), mm);
+                }
+                eng.gemm(-1.0, s.btk(), mm, 1.0, ctv);
+            }
+            eng.gemm(1.0, ctv, eng.small(rinv_slot, d, d), 0.0, s.btslot(d));
+            auto [keep, met] = s.indicator(d, !fixed);                              // steps 19-20
+            s.k += keep;
+            if (met) { term = 1; stop = true; break; }
+            if (d < bi) { term = 3; stop = true; break; }
+        }
+        if (stop) break;
+    }
+    return wrap(term);
+}
+
+}  // namespace
+
+// ---- operator layer ------------------------------------------------------------------
+double frob_norm_sq(Context& c, Matrix& a) {
+    Engine eng(c, a);
+    a.passes += 1;
+    return eng.frob_device(c.d_small + static_cast<std::size_t>(kSlot) * kNumSlots + 3);
+}
+
+void multiply(Context& c, Matrix& a, const MatView& x, const MatView& y, bool trans) {
+    Engine eng(c, a);
+    if (trans) eng.apply_t(x, y);
+    else eng.apply(x, y);
+    a.passes += 1;
+}
+
+std::unique_ptr<Result> run(Context& c, Matrix& a, const Params& p) {
+    Timer t(c.st);
+    std::unique_ptr<Result> r;
+    switch (p.alg) {
+        case 0: r = run_ei(c, a, p); break;
+        case 1: case 2: case 3: r = run_fp(c, a, p); break;
+        default: throw QbError(kError, "unknown algorithm id");
+    }
+    r->device_ms = t.stop();
+    return r;
+}
+
+}  // namespace qbgpu

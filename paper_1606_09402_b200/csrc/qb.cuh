@@ -1,0 +1,133 @@
+// Host-side engine of the B200 randQB path: context, device matrix handle,
+// result, and the algorithm drivers (qb.cu). The C-ABI (capi.cu) is a thin
+// exception-to-status layer over these.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "comm.cuh"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "rng.cuh"
+#include "sparse.cuh"
+
+namespace qbgpu {
+
+// Stream-ordered device allocation (cudaMallocAsync pool).
+struct DBuf {
+    double* p = nullptr;
+    std::size_t n = 0;
+    cudaStream_t st = nullptr;
+    DBuf() = default;
+    DBuf(std::size_t count, cudaStream_t s) : n(count), st(s) {
+        if (count) QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(double), s));
+    }
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), st(o.st) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { reset(); p = o.p; n = o.n; st = o.st; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    void reset() {
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr;
+        n = 0;
+    }
+    ~DBuf() { reset(); }
+};
+
+struct Context {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    int sms = 148;
+    Workspace ws_gemm, ws_red, ws_hh;
+    RngTables rng;
+    std::unique_ptr<Comm> comm;
+    int rank = 0, world = 1;
+    std::string last_error;
+    // small device scratch: b x b matrices (ld kSmallMax) and scalars
+    double* d_small = nullptr;
+    SmallStatus* d_status = nullptr;
+    IndicatorOut* d_ind = nullptr;
+    // pinned host mirrors
+    SmallStatus* h_status = nullptr;
+    IndicatorOut* h_ind = nullptr;
+    double* h_scalar = nullptr;
+
+    explicit Context(int dev, int rank_ = 0, int world_ = 1, const void* nccl_id = nullptr);
+    ~Context();
+    void allreduce(double* p, std::size_t count) {
+        if (comm) comm->allreduce_sum(p, count, st);
+    }
+};
+
+struct Matrix {
+    Context* ctx = nullptr;
+    bool sparse = false;
+    std::int64_t m = 0, n = 0;          // local rows, columns
+    std::int64_t m_global = 0, row0 = 0;
+    std::int64_t passes = 0;            // PassCounter (matrix_handle.hpp:20-27)
+    // dense, column-major
+    double* a = nullptr;
+    std::int64_t lda = 0;
+    bool owns_a = true;
+    // CSR + device-built transposed CSR
+    std::int64_t nnz = 0;
+    std::int64_t* rp = nullptr;
+    std::int32_t* ci = nullptr;
+    double* v = nullptr;
+    std::int64_t* ct_rp = nullptr;
+    std::int32_t* ct_ci = nullptr;
+    double* ct_v = nullptr;
+
+    ~Matrix();
+    MatView dense_view() const { return MatView{a, m, n, lda, false}; }
+    CsrView csr() const { return CsrView{m, n, nnz, rp, ci, v}; }
+    CsrView csr_t() const { return CsrView{n, m, nnz, ct_rp, ct_ci, ct_v}; }
+};
+
+std::unique_ptr<Matrix> make_dense(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
+                                   std::int64_t n, const double* a, std::int64_t lda, bool device_src);
+std::unique_ptr<Matrix> make_csr(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
+                                 std::int64_t n, std::int64_t nnz, const std::int64_t* rp,
+                                 const std::int32_t* ci, const double* v);
+
+struct Params {
+    int alg = 0;          // 0 EI, 1 FP, 2 FP fixed rank, 3 single pass
+    int mode = 1;         // 0 fixed rank, 1 fixed precision
+    std::int64_t b = 10, power = 0, k = 0, s = 0, max_rank = 0, l_budget = 0, max_restarts = 8;
+    double eps_abs = 0.0;
+    std::uint64_t seed = 0, stream = 0;
+    bool reorth = true;
+};
+
+struct Result {
+    Context* ctx = nullptr;
+    std::int64_t m = 0, n = 0, rank = 0;
+    DBuf q, bt;            // Q: m x cap row-major (ld), B^T: n x cap row-major (ld)
+    std::int64_t ld = 0;
+    double e = -1.0, norm_a_sq = 0.0;
+    std::int64_t passes = 0;
+    int terminated_by = 0;
+    std::int64_t blocks = 0, gaussians_used = 0, restarts = 0, hh_fallbacks = 0;
+    double device_ms = 0.0;
+    std::vector<double> trace;
+
+    MatView q_view() const { return MatView{q.p, m, rank, ld, true}; }
+    MatView bt_view() const { return MatView{bt.p, n, rank, ld, true}; }
+};
+
+std::unique_ptr<Result> run(Context& c, Matrix& a, const Params& p);
+
+// Operator layer (MatrixHandle::frob_norm_sq / multiply) on device buffers.
+double frob_norm_sq(Context& c, Matrix& a);
+// Y (rows x w, row-major) = op(A) X (row-major), one pass; A^T results are allreduced.
+void multiply(Context& c, Matrix& a, const MatView& x, const MatView& y, bool trans);
+
+}  // namespace qbgpu

@@ -1,0 +1,536 @@
+// Small dense kernels and deterministic reductions for the per-block work of
+// randQB_EI / randQB_FP:
+//  * sum of squares (||A||_F^2, matrix_handle.cpp:104-110 / kernels_avx2.cpp:36-53)
+//  * per-column sums of squares (row norms of B_i, the indicator E -= ||B_i(j,:)||^2,
+//    PAPER.md:206-220)
+//  * CholQR pieces: in-CTA Cholesky of a b x b Gram with R^{-1} from the same
+//    elimination, upper-triangular products (steps 9a-9b)
+//  * Householder panel QR (the exact-semantics fallback of orth_qr, qr.hpp:15-18)
+// All reductions use fixed partitions and fixed combination order, so results
+// are bitwise reproducible.
+
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "gemm.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace qbgpu {
+
+namespace {
+
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum with a fixed tree; result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < NT / 32 ? sh[threadIdx.x] : 0.0;
+        s = warp_sum(s);
+    }
+    __syncthreads();
+    return s;
+}
+
+__global__ void scale_kernel(MatView c, double beta) {
+    const std::int64_t total = c.rows * c.cols;
+    for (std::int64_t idx = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+         idx < total; idx += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        std::int64_t i, j;
+        if (c.rowmajor) { i = idx / c.cols; j = idx % c.cols; }
+        else { i = idx % c.rows; j = idx / c.rows; }
+        double* p = c.at(i, j);
+        *p = beta == 0.0 ? 0.0 : beta * (*p);
+    }
+}
+
+__global__ void copy_kernel(MatView s, MatView d) {
+    const std::int64_t total = s.rows * s.cols;
+    for (std::int64_t idx = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+         idx < total; idx += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        std::int64_t i, j;
+        if (d.rowmajor) { i = idx / d.cols; j = idx % d.cols; }
+        else { i = idx % d.rows; j = idx / d.rows; }
+        *d.at(i, j) = *s.at(i, j);
+    }
+}
+
+__global__ void add_kernel(MatView s, MatView d, double alpha) {
+    const std::int64_t total = s.rows * s.cols;
+    for (std::int64_t idx = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+         idx < total; idx += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        std::int64_t i, j;
+        if (d.rowmajor) { i = idx / d.cols; j = idx % d.cols; }
+        else { i = idx % d.rows; j = idx / d.rows; }
+        *d.at(i, j) = fma(alpha, *s.at(i, j), *d.at(i, j));
+    }
+}
+
+__global__ void identity_kernel(MatView c) {
+    const std::int64_t total = c.rows * c.cols;
+    for (std::int64_t idx = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+         idx < total; idx += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t i = idx % c.rows, j = idx / c.rows;
+        *c.at(i, j) = i == j ? 1.0 : 0.0;
+    }
+}
+
+// Stage 1: each CTA owns a fixed set of segments (outer index s = cta, cta+G, ...);
+// within a segment the lanes stride the contiguous inner dimension.
+__global__ void sumsq_stage1(const double* __restrict__ p, std::int64_t outer, std::int64_t inner,
+                             std::int64_t ld, double* __restrict__ partial) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    const int gsz = gridDim.x;
+    // Split each segment into pieces so that few long segments still spread over CTAs.
+    const std::int64_t piece = 4096;
+    const std::int64_t pieces_per_seg = (inner + piece - 1) / piece;
+    const std::int64_t units = outer * pieces_per_seg;
+    for (std::int64_t u = blockIdx.x; u < units; u += gsz) {
+        const std::int64_t s = u / pieces_per_seg;
+        const std::int64_t i0 = (u % pieces_per_seg) * piece;
+        const std::int64_t i1 = min(inner, i0 + piece);
+        const double* seg = p + s * ld;
+        for (std::int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+            const double v = seg[i];
+            acc = fma(v, v, acc);
+        }
+    }
+    const double s = block_sum<kRedThreads>(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void sumsq_stage2(const double* __restrict__ partial, int n, double* out) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partial[i];
+    const double s = block_sum<kRedThreads>(acc, sh);
+    if (threadIdx.x == 0) *out = s;
+}
+
+// Per-column sums of squares. CTA c owns rows [c*chunk, (c+1)*chunk); thread j owns
+// columns j, j+blockDim, ...
+__global__ void colsumsq_stage1(MatView v, std::int64_t chunk, double* __restrict__ partial) {
+    const std::int64_t r0 = blockIdx.x * chunk;
+    const std::int64_t r1 = min(v.rows, r0 + chunk);
+    for (std::int64_t j = threadIdx.x; j < v.cols; j += blockDim.x) {
+        double acc = 0.0;
+        for (std::int64_t i = r0; i < r1; ++i) {
+            const double x = *v.at(i, j);
+            acc = fma(x, x, acc);
+        }
+        partial[blockIdx.x * v.cols + j] = acc;
+    }
+}
+
+__global__ void colsumsq_stage2(const double* __restrict__ partial, int nblk, std::int64_t cols,
+                                double* __restrict__ out) {
+    for (std::int64_t j = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; j < cols;
+         j += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < nblk; ++c) s += partial[c * cols + j];
+        out[j] = s;
+    }
+}
+
+// Cholesky of the b x b Gram by symmetric Gaussian elimination on [G | I]:
+// after step k row k holds R(k,:) on the left and (R^{-T})(k,:) on the right.
+constexpr int kCholThreads = 1024;
+
+__global__ void __launch_bounds__(kCholThreads)
+chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double* __restrict__ r,
+                  double* __restrict__ rinv, std::int64_t ldr, SmallStatus* status) {
+    extern __shared__ double w[];
+    const int ldw = 2 * b + 1;
+    __shared__ int s_break, s_bad;
+    __shared__ double s_piv;
+    __shared__ double s_dev;
+    if (threadIdx.x == 0) { s_break = 0; s_bad = -1; s_dev = 0.0; }
+    // load [G | I] (symmetrise from the upper triangle so both halves agree bitwise)
+    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+        const int i = idx % b, j = idx / b;
+        const double v = i <= j ? g[i + j * ldg] : g[j + i * ldg];
+        w[i * ldw + j] = v;
+        w[i * ldw + b + j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double dev = 0.0;
+        for (int idx = threadIdx.x; idx < b * b; idx += 32) {
+            const int i = idx % b, j = idx / b;
+            dev = fmax(dev, fabs(w[i * ldw + j] - (i == j ? 1.0 : 0.0)));
+        }
+        for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_down_sync(0xffffffffu, dev, o));
+        if (threadIdx.x == 0) s_dev = dev;
+    }
+    for (int k = 0; k < b; ++k) {
+        if (threadIdx.x == 0) {
+            const double piv = w[k * ldw + k];
+            if (!(piv > 0.0) || !isfinite(piv)) {
+                if (!s_break) { s_break = 1; s_bad = k; }
+                s_piv = 1.0;  // keep going with a harmless pivot; caller falls back
+            } else {
+                s_piv = sqrt(piv);
+            }
+        }
+        __syncthreads();
+        const double s = s_piv;
+        const double inv = 1.0 / s;
+        // scale row k (left cols k..b-1, right cols 0..k)
+        for (int j = threadIdx.x; j < 2 * b; j += blockDim.x) {
+            if ((j >= k && j < b) || (j >= b && j <= b + k)) {
+                if (j == k) w[k * ldw + k] = s;
+                else w[k * ldw + j] *= inv;
+            }
+        }
+        __syncthreads();
+        // eliminate rows i > k: row_i -= R(k,i) * row_k  (R(k,i) = scaled w[k][i])
+        const int rows = b - k - 1;
+        const int cols_left = b - k - 1;   // j in (k, b)
+        const int cols_right = k + 1;      // j in [b, b+k]
+        const int cols = cols_left + cols_right;
+        for (int idx = threadIdx.x; idx < rows * cols; idx += blockDim.x) {
+            const int i = k + 1 + idx / cols;
+            const int jj = idx % cols;
+            const int j = jj < cols_left ? k + 1 + jj : b + (jj - cols_left);
+            const double f = w[k * ldw + i];
+            w[i * ldw + j] = fma(-f, w[k * ldw + j], w[i * ldw + j]);
+        }
+        __syncthreads();
+    }
+    // outputs: R upper (left), Rinv = (right)^T, upper
+    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+        const int i = idx % b, j = idx / b;
+        r[i + j * ldr] = i <= j ? w[i * ldw + j] : 0.0;
+        rinv[i + j * ldr] = i <= j ? w[j * ldw + b + i] : 0.0;
+    }
+    if (threadIdx.x == 0 && status) {
+        double dmin = INFINITY, dmax = 0.0;
+        for (int j = 0; j < b; ++j) {
+            const double d = w[j * ldw + j];
+            dmin = fmin(dmin, d);
+            dmax = fmax(dmax, d);
+        }
+        status->breakdown = s_break;
+        status->bad_index = s_bad;
+        status->diag_min = dmin;
+        status->diag_max = dmax;
+        status->gram_dev = s_dev;
+    }
+}
+
+__global__ void trmm_upper_kernel(const double* __restrict__ a, const double* __restrict__ bm,
+                                  double* __restrict__ c, int n, std::int64_t ld) {
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+        const int i = idx % n, j = idx / n;
+        double s = 0.0;
+        if (i <= j)
+            for (int p = i; p <= j; ++p) s = fma(a[i + p * ld], bm[p + j * ld], s);
+        c[i + j * ld] = s;
+    }
+}
+
+// Column j of R^{-1} by back substitution; one thread per column.
+__global__ void tri_inverse_kernel(const double* __restrict__ r, double* __restrict__ x, int n,
+                                   std::int64_t ld) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        for (int i = n - 1; i >= 0; --i) {
+            double v = 0.0;
+            if (i <= j) {
+                double s = (i == j) ? 1.0 : 0.0;
+                for (int p = i + 1; p <= j; ++p) s = fma(-r[i + p * ld], x[p + j * ld], s);
+                v = s / r[i + i * ld];
+            }
+            x[i + j * ld] = v;
+        }
+    }
+}
+
+__global__ void indicator_kernel(double* e_dev, const double* __restrict__ norms, int b, double eps2,
+                                 int check, IndicatorOut* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double e = *e_dev;
+    int keep = b, met = 0;
+    for (int j = 0; j < b; ++j) {
+        e -= norms[j];
+        if (check && e < eps2) {
+            keep = j + 1;
+            met = 1;
+            break;
+        }
+    }
+    *e_dev = e;
+    out->e = e;
+    out->keep = keep;
+    out->met = met;
+}
+
+// ---- Householder panel (cooperative) -------------------------------------------
+constexpr int kHhThreads = 256;
+
+__device__ double grid_reduce_sum(cg::grid_group& grid, double v, double* part, double* sh) {
+    const double s = block_sum<kHhThreads>(v, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+    grid.sync();
+    double tot = 0.0;
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < static_cast<int>(gridDim.x); ++c) tot += part[c];
+        sh[0] = tot;
+    }
+    __syncthreads();
+    tot = sh[0];
+    __syncthreads();
+    return tot;
+}
+
+// Vector version: partials part[cta * nv + c], totals into out_sh (shared, nv values).
+__device__ void grid_reduce_vec(cg::grid_group& grid, int nv, double* part, double* out_sh) {
+    grid.sync();
+    for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+        double tot = 0.0;
+        for (int q = 0; q < static_cast<int>(gridDim.x); ++q) tot += part[q * nv + c];
+        out_sh[c] = tot;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kHhThreads)
+householder_panel_kernel(double* y, std::int64_t m, int b, std::int64_t ld, double* r,
+                         std::int64_t ldr, double* part, double* qs, double* taus) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[32];
+    __shared__ double wv[kSmallMax];
+    __shared__ double sgn[kSmallMax];
+    const std::int64_t chunk = (m + gridDim.x - 1) / gridDim.x;
+    const std::int64_t r0 = blockIdx.x * chunk;
+    const std::int64_t r1 = min(m, r0 + chunk);
+    // Forward: reflectors H_j = I - tau_j v_j v_j^T, v_j = [1; y(j+1:, j)] (LAPACK dgeqr2 order).
+    for (int j = 0; j < b; ++j) {
+        double* col = y + static_cast<std::int64_t>(j) * ld;
+        const std::int64_t lo = max(r0, static_cast<std::int64_t>(j));
+        double acc = 0.0;
+        for (std::int64_t i = max(lo, static_cast<std::int64_t>(j) + 1) + threadIdx.x; i < r1; i += blockDim.x)
+            acc = fma(col[i], col[i], acc);
+        const double sigma = grid_reduce_sum(grid, acc, part, sh);
+        const double alpha = col[j];
+        double beta, tau, scale;
+        if (sigma == 0.0) {
+            tau = 0.0; beta = alpha; scale = 1.0;
+        } else {
+            const double nrm = sqrt(alpha * alpha + sigma);
+            beta = alpha >= 0.0 ? -nrm : nrm;
+            tau = (beta - alpha) / beta;
+            scale = 1.0 / (alpha - beta);
+        }
+        for (std::int64_t i = max(lo, static_cast<std::int64_t>(j) + 1) + threadIdx.x; i < r1; i += blockDim.x)
+            col[i] *= scale;
+        __syncthreads();
+        const int nv = b - j - 1;
+        // w_c = v^T y(j:, c), the v_j = 1 term taken by the owner of row j
+        for (int c = 0; c < nv; ++c) {
+            const double* yc = y + static_cast<std::int64_t>(j + 1 + c) * ld;
+            double a2 = 0.0;
+            for (std::int64_t i = lo + threadIdx.x; i < r1; i += blockDim.x)
+                a2 = fma(i == j ? 1.0 : col[i], yc[i], a2);
+            const double s = block_sum<kHhThreads>(a2, sh);
+            if (threadIdx.x == 0) part[blockIdx.x * nv + c] = s;
+        }
+        grid_reduce_vec(grid, nv, part, wv);
+        for (int c = 0; c < nv; ++c) {
+            double* yc = y + static_cast<std::int64_t>(j + 1 + c) * ld;
+            const double f = tau * wv[c];
+            for (std::int64_t i = lo + threadIdx.x; i < r1; i += blockDim.x)
+                yc[i] = fma(-f, i == j ? 1.0 : col[i], yc[i]);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            taus[j] = tau;
+            r[j + static_cast<std::int64_t>(j) * ldr] = beta;
+        }
+        grid.sync();
+    }
+    // R strictly-upper part = y(i, c), i < c; zeros below the diagonal.
+    if (blockIdx.x == 0) {
+        for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+            const int i = idx % b, c = idx / b;
+            if (i < c) r[i + static_cast<std::int64_t>(c) * ldr] = y[i + static_cast<std::int64_t>(c) * ld];
+            else if (i > c) r[i + static_cast<std::int64_t>(c) * ldr] = 0.0;
+        }
+    }
+    // Q = H_0 ... H_{b-1} [I; 0] into qs (m x b, ld m), backward accumulation (dorg2r order).
+    for (int c = 0; c < b; ++c)
+        for (std::int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x)
+            qs[i + static_cast<std::int64_t>(c) * m] = (i == c) ? 1.0 : 0.0;
+    grid.sync();
+    for (int j = b - 1; j >= 0; --j) {
+        const double tau = taus[j];
+        const double* v = y + static_cast<std::int64_t>(j) * ld;
+        const std::int64_t lo = max(r0, static_cast<std::int64_t>(j));
+        const int nv = b - j;
+        for (int c = 0; c < nv; ++c) {
+            const double* qc = qs + static_cast<std::int64_t>(j + c) * m;
+            double a2 = 0.0;
+            for (std::int64_t i = lo + threadIdx.x; i < r1; i += blockDim.x)
+                a2 = fma(i == j ? 1.0 : v[i], qc[i], a2);
+            const double s = block_sum<kHhThreads>(a2, sh);
+            if (threadIdx.x == 0) part[blockIdx.x * nv + c] = s;
+        }
+        grid_reduce_vec(grid, nv, part, wv);
+        for (int c = 0; c < nv; ++c) {
+            double* qc = qs + static_cast<std::int64_t>(j + c) * m;
+            const double f = tau * wv[c];
+            for (std::int64_t i = lo + threadIdx.x; i < r1; i += blockDim.x)
+                qc[i] = fma(-f, i == j ? 1.0 : v[i], qc[i]);
+        }
+        grid.sync();
+    }
+    // Sign post-pass (qr.hpp:15-18): diag(R) >= 0. Copy Q back into y.
+    for (int c = threadIdx.x; c < b; c += blockDim.x)
+        sgn[c] = r[c + static_cast<std::int64_t>(c) * ldr] < 0.0 ? -1.0 : 1.0;
+    __syncthreads();
+    for (int c = 0; c < b; ++c)
+        for (std::int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x)
+            y[i + static_cast<std::int64_t>(c) * ld] = sgn[c] * qs[i + static_cast<std::int64_t>(c) * m];
+    if (blockIdx.x == 0) {
+        for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+            const int i = idx % b, c = idx / b;
+            if (i <= c) r[i + static_cast<std::int64_t>(c) * ldr] *= sgn[i];
+        }
+    }
+}
+
+int grid_for(std::int64_t total, int threads) {
+    const std::int64_t want = ceil_div(total, threads);
+    return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, 8L * gemm_num_sms())));
+}
+
+}  // namespace
+
+void scale_matrix(cudaStream_t st, const MatView& c, double beta) {
+    if (c.rows * c.cols == 0) return;
+    scale_kernel<<<grid_for(c.rows * c.cols, 256), 256, 0, st>>>(c, beta);
+    QB_LAUNCH_CHECK();
+}
+
+void copy_matrix(cudaStream_t st, const MatView& s, const MatView& d) {
+    if (s.rows != d.rows || s.cols != d.cols) throw QbError(kDimensionError, "copy_matrix: shape");
+    if (s.rows * s.cols == 0) return;
+    copy_kernel<<<grid_for(s.rows * s.cols, 256), 256, 0, st>>>(s, d);
+    QB_LAUNCH_CHECK();
+}
+
+void add_matrix(cudaStream_t st, const MatView& s, const MatView& d, double alpha) {
+    if (s.rows != d.rows || s.cols != d.cols) throw QbError(kDimensionError, "add_matrix: shape");
+    if (s.rows * s.cols == 0) return;
+    add_kernel<<<grid_for(s.rows * s.cols, 256), 256, 0, st>>>(s, d, alpha);
+    QB_LAUNCH_CHECK();
+}
+
+void set_identity(cudaStream_t st, const MatView& c) {
+    if (c.rows * c.cols == 0) return;
+    identity_kernel<<<grid_for(c.rows * c.cols, 256), 256, 0, st>>>(c);
+    QB_LAUNCH_CHECK();
+}
+
+void sum_squares(cudaStream_t st, Workspace& ws, const MatView& v, double* out) {
+    const std::int64_t outer = v.rowmajor ? v.rows : v.cols;
+    const std::int64_t inner = v.rowmajor ? v.cols : v.rows;
+    if (outer * inner == 0) {
+        QB_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+        return;
+    }
+    const int nblk = static_cast<int>(std::min<std::int64_t>(
+        std::max<std::int64_t>(1, ceil_div(outer * inner, 8 * kRedThreads)), 4L * gemm_num_sms()));
+    double* part = ws.get(static_cast<std::size_t>(nblk));
+    sumsq_stage1<<<nblk, kRedThreads, 0, st>>>(v.p, outer, inner, v.ld, part);
+    QB_LAUNCH_CHECK();
+    sumsq_stage2<<<1, kRedThreads, 0, st>>>(part, nblk, out);
+    QB_LAUNCH_CHECK();
+}
+
+void sum_squares_vec(cudaStream_t st, Workspace& ws, const double* x, std::int64_t n, double* out) {
+    MatView v{const_cast<double*>(x), n, 1, n, false};
+    sum_squares(st, ws, v, out);
+}
+
+void column_sumsq(cudaStream_t st, Workspace& ws, const MatView& v, double* out) {
+    if (v.cols == 0) return;
+    if (v.rows == 0) {
+        QB_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * v.cols, st));
+        return;
+    }
+    const std::int64_t target = 2L * gemm_num_sms();
+    const std::int64_t chunk = std::max<std::int64_t>(64, ceil_div(v.rows, target));
+    const int nblk = static_cast<int>(ceil_div(v.rows, chunk));
+    double* part = ws.get(static_cast<std::size_t>(nblk) * v.cols);
+    const int thr = static_cast<int>(std::min<std::int64_t>(256, round_up(v.cols, 32)));
+    colsumsq_stage1<<<nblk, thr, 0, st>>>(v, chunk, part);
+    QB_LAUNCH_CHECK();
+    colsumsq_stage2<<<static_cast<int>(ceil_div(v.cols, 128)), 128, 0, st>>>(part, nblk, v.cols, out);
+    QB_LAUNCH_CHECK();
+}
+
+void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, double* r, double* rinv,
+                std::int64_t ldr, SmallStatus* status) {
+    if (b < 1 || b > kSmallMax) throw QbError(kDimensionError, "chol_small: block width out of range");
+    const int smem = b * (2 * b + 1) * static_cast<int>(sizeof(double));
+    static bool configured = false;
+    if (!configured) {
+        QB_CUDA(cudaFuncSetAttribute(chol_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSmallMax * (2 * kSmallMax + 1) * 8));
+        configured = true;
+    }
+    chol_small_kernel<<<1, kCholThreads, smem, st>>>(g, ldg, b, r, rinv, ldr, status);
+    QB_LAUNCH_CHECK();
+}
+
+void trmm_upper_small(cudaStream_t st, const double* a, const double* b, double* c, int n,
+                      std::int64_t ld) {
+    trmm_upper_kernel<<<1, 1024, 0, st>>>(a, b, c, n, ld);
+    QB_LAUNCH_CHECK();
+}
+
+void tri_inverse_small(cudaStream_t st, const double* r, double* rinv, int n, std::int64_t ld) {
+    tri_inverse_kernel<<<1, 128, 0, st>>>(r, rinv, n, ld);
+    QB_LAUNCH_CHECK();
+}
+
+void indicator_step(cudaStream_t st, double* e_dev, const double* norms, int b, double eps2, int check,
+                    IndicatorOut* out) {
+    indicator_kernel<<<1, 32, 0, st>>>(e_dev, norms, b, eps2, check, out);
+    QB_LAUNCH_CHECK();
+}
+
+void householder_panel(cudaStream_t st, Workspace& ws, double* y, std::int64_t m, int b, std::int64_t ld,
+                       double* r, std::int64_t ldr) {
+    if (b < 1 || b > kSmallMax) throw QbError(kDimensionError, "householder_panel: width out of range");
+    if (m < b) throw QbError(kDimensionError, "orth_qr: rows < cols");
+    int per_sm = 0;
+    QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, householder_panel_kernel, kHhThreads, 0));
+    int grid = std::max(1, std::min<int>(per_sm * gemm_num_sms(), static_cast<int>(ceil_div(m, 512))));
+    grid = std::min(grid, 2 * gemm_num_sms());
+    const std::size_t part_n = static_cast<std::size_t>(grid) * kSmallMax;
+    double* base = ws.get(part_n + static_cast<std::size_t>(m) * b + kSmallMax);
+    double* part = base;
+    double* qs = base + part_n;
+    double* taus = qs + static_cast<std::size_t>(m) * b;
+    void* args[] = {&y, &m, &b, &ld, &r, &ldr, &part, &qs, &taus};
+    QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(householder_panel_kernel), grid, kHhThreads,
+                                        args, 0, st));
+    QB_LAUNCH_CHECK();
+}
+
+}  // namespace qbgpu

@@ -1,0 +1,240 @@
+// CSR passes over a sparse A for sm_100a.
+//
+// Replaces the reference drivers csr_gemm_n (Y = A X, one column of X at a
+// time, A swept p times; /root/reference/proj/src/kernels_drivers.cpp:67-79 with
+// sparse_dot kernels_avx2.cpp:123-135) and csr_gemm_t (Y += A^T X by scalar
+// scatter, kernels_drivers.cpp:81-94).
+//
+// B200 design: A is read ONCE per pass for all w right-hand sides. Block vectors
+// are row-major so that every nonzero gathers one contiguous row of X (8*w
+// bytes, coalesced across the warp) and every output row is one coalesced store.
+// A warp owns a row; lanes load 32 (col, val) pairs at a time and broadcast them
+// with shuffles. A^T X runs the same gather kernel over a transposed CSR built on
+// the device in a stable (row-ascending) order, so there are no atomics and the
+// result is bitwise reproducible.
+
+#include "sparse.cuh"
+
+#include <algorithm>
+
+namespace qbgpu {
+
+namespace {
+
+template <int NQ>
+__global__ void __launch_bounds__(256)
+csr_spmm_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
+                const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx,
+                double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta) {
+    const int lane = threadIdx.x & 31;
+    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (std::int64_t i = warp; i < rows; i += nwarps) {
+        double acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+        const std::int64_t e0 = rp[i], e1 = rp[i + 1];
+        for (std::int64_t eb = e0; eb < e1; eb += 32) {
+            const int cnt = static_cast<int>(e1 - eb < 32 ? e1 - eb : 32);
+            std::int32_t my_c = 0;
+            double my_v = 0.0;
+            if (lane < cnt) {
+                my_c = __ldg(ci + eb + lane);
+                my_v = __ldg(v + eb + lane);
+            }
+            for (int j = 0; j < cnt; ++j) {
+                const std::int32_t c = __shfl_sync(0xffffffffu, my_c, j);
+                const double a = __shfl_sync(0xffffffffu, my_v, j);
+                const double* xr = x + static_cast<std::int64_t>(c) * ldx;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int col = lane + 32 * q;
+                    if (col < w) acc[q] = fma(a, __ldg(xr + col), acc[q]);
+                }
+            }
+        }
+        double* yr = y + i * ldy;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int col = lane + 32 * q;
+            if (col < w) {
+                const double r = alpha * acc[q];
+                yr[col] = beta == 0.0 ? r : r + beta * yr[col];
+            }
+        }
+    }
+}
+
+// ---- transposed CSR (stable, deterministic) ---------------------------------------
+__global__ void count_cols_kernel(std::int64_t nnz, const std::int32_t* __restrict__ ci, int* __restrict__ cnt) {
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < nnz;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(cnt + ci[e], 1);
+}
+
+// Per-chunk column counts: chunk b owns rows [b*rows_per, (b+1)*rows_per).
+__global__ void chunk_count_kernel(std::int64_t m, std::int64_t rows_per, const std::int64_t* __restrict__ rp,
+                                   const std::int32_t* __restrict__ ci, std::int64_t n, int* __restrict__ cc) {
+    const std::int64_t r0 = blockIdx.x * rows_per;
+    const std::int64_t r1 = min(m, r0 + rows_per);
+    if (r0 >= r1) return;
+    int* mine = cc + static_cast<std::int64_t>(blockIdx.x) * n;
+    for (std::int64_t e = rp[r0] + threadIdx.x; e < rp[r1]; e += blockDim.x) atomicAdd(mine + ci[e], 1);
+}
+
+// Exclusive scan over n column counts -> ct_ptr (single CTA, chunked).
+__global__ void scan_kernel(std::int64_t n, const int* __restrict__ cnt, std::int64_t* __restrict__ ptr) {
+    __shared__ std::int64_t part[1024];
+    const std::int64_t per = (n + blockDim.x - 1) / blockDim.x;
+    const std::int64_t c0 = threadIdx.x * per;
+    const std::int64_t c1 = min(n, c0 + per);
+    std::int64_t s = 0;
+    for (std::int64_t c = c0; c < c1; ++c) s += cnt[c];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        std::int64_t run = 0;
+        for (int t = 0; t < static_cast<int>(blockDim.x); ++t) {
+            const std::int64_t v = part[t];
+            part[t] = run;
+            run += v;
+        }
+        ptr[n] = run;
+    }
+    __syncthreads();
+    std::int64_t run = part[threadIdx.x];
+    for (std::int64_t c = c0; c < c1; ++c) {
+        ptr[c] = run;
+        run += cnt[c];
+    }
+}
+
+// cc[b][c] -> starting offset of chunk b inside column c (in place).
+__global__ void chunk_offsets_kernel(std::int64_t n, int nchunks, const std::int64_t* __restrict__ ptr,
+                                     int* __restrict__ cc, std::int64_t* __restrict__ off) {
+    for (std::int64_t c = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; c < n;
+         c += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        std::int64_t run = ptr[c];
+        for (int b = 0; b < nchunks; ++b) {
+            const int v = cc[static_cast<std::int64_t>(b) * n + c];
+            off[static_cast<std::int64_t>(b) * n + c] = run;
+            run += v;
+        }
+    }
+}
+
+// Stable placement: rows of a chunk are visited in order; within a row every column
+// is distinct, so the chunk's threads can place a row's entries concurrently.
+__global__ void place_kernel(std::int64_t m, std::int64_t rows_per, const std::int64_t* __restrict__ rp,
+                             const std::int32_t* __restrict__ ci, const double* __restrict__ v, std::int64_t n,
+                             std::int64_t* __restrict__ off, std::int32_t* __restrict__ ct_ci,
+                             double* __restrict__ ct_v) {
+    const std::int64_t r0 = blockIdx.x * rows_per;
+    const std::int64_t r1 = min(m, r0 + rows_per);
+    std::int64_t* mine = off + static_cast<std::int64_t>(blockIdx.x) * n;
+    for (std::int64_t i = r0; i < r1; ++i) {
+        for (std::int64_t e = rp[i] + threadIdx.x; e < rp[i + 1]; e += blockDim.x) {
+            const std::int32_t c = ci[e];
+            const std::int64_t pos = mine[c]++;
+            ct_ci[pos] = static_cast<std::int32_t>(i);
+            ct_v[pos] = v[e];
+        }
+        __syncthreads();
+    }
+}
+
+// from_parts validation (sparse_csr.cpp:10-40): flags |= 1 structure, |= 2 non-finite.
+__global__ void validate_kernel(std::int64_t m, std::int64_t n, std::int64_t nnz, const std::int64_t* __restrict__ rp,
+                                const std::int32_t* __restrict__ ci, const double* __restrict__ v,
+                                int* __restrict__ flags) {
+    const std::int64_t tid = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    for (std::int64_t i = tid; i < m; i += stride) {
+        const std::int64_t a = rp[i], b = rp[i + 1];
+        if (a > b || a < 0 || b > nnz) { atomicOr(flags, 1); continue; }
+        for (std::int64_t e = a; e < b; ++e) {
+            const std::int32_t c = ci[e];
+            if (c < 0 || c >= n) atomicOr(flags, 1);
+            if (e > a && c <= ci[e - 1]) atomicOr(flags, 1);
+        }
+    }
+    for (std::int64_t e = tid; e < nnz; e += stride)
+        if (!isfinite(v[e])) atomicOr(flags, 2);
+    if (tid == 0 && (rp[0] != 0 || rp[m] != nnz)) atomicOr(flags, 1);
+}
+
+}  // namespace
+
+void csr_spmm(cudaStream_t st, const CsrView& a, const double* x, std::int64_t ldx, double* y, std::int64_t ldy,
+              int w, double alpha, double beta, int sms) {
+    if (a.rows == 0 || w == 0) return;
+    const int threads = 256;
+    const std::int64_t warps_needed = a.rows;
+    const int blocks = static_cast<int>(std::max<std::int64_t>(
+        1, std::min<std::int64_t>(ceil_div(warps_needed * 32, threads), 16L * sms)));
+    if (w <= 32) csr_spmm_kernel<1><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta);
+    else if (w <= 64) csr_spmm_kernel<2><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta);
+    else if (w <= 128) csr_spmm_kernel<4><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta);
+    else if (w <= 256) csr_spmm_kernel<8><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta);
+    else {
+        // Wide right-hand sides (randQB_FP sketches): column slabs of 256.
+        for (int c0 = 0; c0 < w; c0 += 256) {
+            const int wc = std::min(256, w - c0);
+            csr_spmm_kernel<8><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x + c0, ldx, y + c0, ldy, wc,
+                                                           alpha, beta);
+        }
+    }
+    QB_LAUNCH_CHECK();
+}
+
+int csr_validate(cudaStream_t st, std::int64_t m, std::int64_t n, std::int64_t nnz, const std::int64_t* rp,
+                 const std::int32_t* ci, const double* v, int sms) {
+    int* d_flags = nullptr;
+    QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_flags), sizeof(int), st));
+    QB_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(int), st));
+    const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(std::max(m, nnz), 256), 8L * sms)));
+    validate_kernel<<<blocks, 256, 0, st>>>(m, n, nnz, rp, ci, v, d_flags);
+    QB_LAUNCH_CHECK();
+    int flags = 0;
+    QB_CUDA(cudaMemcpyAsync(&flags, d_flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    QB_CUDA(cudaFreeAsync(d_flags, st));
+    QB_CUDA(cudaStreamSynchronize(st));
+    return flags;
+}
+
+void csr_transpose(cudaStream_t st, std::int64_t m, std::int64_t n, std::int64_t nnz, const std::int64_t* rp,
+                   const std::int32_t* ci, const double* v, std::int64_t* ct_rp, std::int32_t* ct_ci,
+                   double* ct_v, int sms) {
+    if (n == 0) return;
+    int* cnt = nullptr;
+    QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cnt), sizeof(int) * n, st));
+    QB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * n, st));
+    if (nnz > 0) {
+        const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(nnz, 256), 8L * sms)));
+        count_cols_kernel<<<blocks, 256, 0, st>>>(nnz, ci, cnt);
+        QB_LAUNCH_CHECK();
+    }
+    scan_kernel<<<1, 1024, 0, st>>>(n, cnt, ct_rp);
+    QB_LAUNCH_CHECK();
+    QB_CUDA(cudaFreeAsync(cnt, st));
+    if (nnz == 0 || m == 0) return;
+    // Chunked stable placement.
+    const int nchunks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(2L * sms, m)));
+    const std::int64_t rows_per = ceil_div(m, nchunks);
+    int* cc = nullptr;
+    std::int64_t* off = nullptr;
+    QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cc), sizeof(int) * n * nchunks, st));
+    QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&off), sizeof(std::int64_t) * n * nchunks, st));
+    QB_CUDA(cudaMemsetAsync(cc, 0, sizeof(int) * n * nchunks, st));
+    chunk_count_kernel<<<nchunks, 256, 0, st>>>(m, rows_per, rp, ci, n, cc);
+    QB_LAUNCH_CHECK();
+    chunk_offsets_kernel<<<static_cast<int>(std::min<std::int64_t>(ceil_div(n, 256), 8L * sms)), 256, 0, st>>>(
+        n, nchunks, ct_rp, cc, off);
+    QB_LAUNCH_CHECK();
+    place_kernel<<<nchunks, 256, 0, st>>>(m, rows_per, rp, ci, v, n, off, ct_ci, ct_v);
+    QB_LAUNCH_CHECK();
+    QB_CUDA(cudaFreeAsync(cc, st));
+    QB_CUDA(cudaFreeAsync(off, st));
+}
+
+}  // namespace qbgpu

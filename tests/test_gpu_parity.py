@@ -1,0 +1,204 @@
+"""Algorithm parity on the B200 against the CPU oracle (the reference's own kernels
+and RNG + the restated randQB_EI / randQB_FP layer, oracle/_ref/libqbref.so).
+
+Bar (north_star): rank identical; singular values of B, ||A - QB||_F and the error
+indicator E within 1e-10 relative in FP64; pass counts identical.
+Singular values of both B's come from the same numpy SVD so differences reflect B.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _sv(b):
+    if b.shape[0] == 0:
+        return np.zeros(0)
+    return np.linalg.svd(b, compute_uv=False)
+
+
+def _compare(gpu, ref, a=None, csr=None, oracle=None, tol=TOL, sv_floor=1e-6):
+    assert gpu.rank == ref.rank, (gpu.rank, ref.rank)
+    assert gpu.terminated_by == ref.terminated_by
+    assert gpu.passes == ref.passes
+    assert abs(gpu.norm_a_sq - ref.norm_a_sq) <= 1e-13 * ref.norm_a_sq
+    # E = ||A||^2 - sum ||B_i||^2 cancels: the reference's own scalar vs AVX2 lanes differ by
+    # 4.6e-14 ||A||^2 on cfg1, so the absolute floor is the ||A||^2 summation noise.
+    assert abs(gpu.error_indicator - ref.E) <= tol * max(ref.E, 1e-300) + 2e-13 * ref.norm_a_sq
+    s_g, s_r = _sv(gpu.B), _sv(ref.B)
+    if len(s_r):
+        sel = s_r > sv_floor * s_r[0]
+        rel = np.abs(s_g[sel] - s_r[sel]) / s_r[sel]
+        assert rel.max() <= tol, rel.max()
+    if oracle is not None and gpu.rank:
+        e_g = oracle.explicit_error(gpu.Q, gpu.B, a=a, csr=csr)
+        e_r = oracle.explicit_error(ref.Q, ref.B, a=a, csr=csr)
+        assert abs(e_g - e_r) <= tol * e_r + 1e-14 * np.sqrt(ref.norm_a_sq), (e_g, e_r)
+    if gpu.rank:
+        qtq = gpu.Q.T @ gpu.Q
+        assert np.abs(qtq - np.eye(gpu.rank)).max() < 1e-12
+
+
+def _matrix2(n, seed=9):
+    from paper_1606_09402_b200 import matgen
+    return matgen.synthesize(n, n, matgen.spectrum("exp_decay", n, tau=7.0), seed)
+
+
+# ---- randQB_EI ------------------------------------------------------------------------------
+def test_cfg1_ei_dense_full_size(ctx, oracle):
+    """BASELINE config 1 at full size (2000 x 2000, b=20, P=0, eps=1e-2 rel, cap 1000)."""
+    from paper_1606_09402_b200 import matgen, qbfac
+    a = matgen.cfg1_matrix()
+    eps = 1e-2 * np.linalg.norm(a)
+    ref = oracle.run("ei", a, b=20, power=0, eps_abs=eps, max_rank=1000, seed=42)
+    h = qbfac.MatrixHandle.dense(a, ctx)
+    got = qbfac.rand_qb_ei(h, qbfac.StopRule.fixed_precision(eps), 20, 0, qbfac.RngStream(42), max_rank=1000)
+    _compare(got, ref, a=a, oracle=oracle)
+    assert got.terminated_by == "tolerance_met"
+    assert np.sqrt(got.error_indicator) < eps
+
+
+@pytest.mark.parametrize("n,b,P,eps_rel", [(300, 10, 1, 1e-4), (400, 10, 0, 1e-2), (257, 7, 2, 1e-3)])
+def test_ei_matrix2(ctx, oracle, n, b, P, eps_rel):
+    from paper_1606_09402_b200 import qbfac
+    a = _matrix2(n)
+    eps = eps_rel * np.linalg.norm(a)
+    ref = oracle.run("ei", a, b=b, power=P, eps_abs=eps, seed=5)
+    got = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), qbfac.StopRule.fixed_precision(eps), b, P,
+                           qbfac.RngStream(5))
+    _compare(got, ref, a=a, oracle=oracle)
+    np.testing.assert_allclose(got.e_trace, ref.e_trace, rtol=1e-9, atol=2e-13 * ref.norm_a_sq)
+
+
+def test_ei_fixed_rank_and_partial_block(ctx, oracle):
+    from paper_1606_09402_b200 import qbfac
+    a = _matrix2(200)
+    ref = oracle.run("ei", a, b=10, power=1, fixed_rank=(33, 4), seed=3)
+    got = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), qbfac.StopRule.fixed_rank(33, 4), 10, 1,
+                           qbfac.RngStream(3))
+    assert got.rank == 37
+    _compare(got, ref, a=a, oracle=oracle)
+
+
+def test_ei_tolerance_above_norm_gives_empty(ctx, oracle):
+    from paper_1606_09402_b200 import qbfac
+    a = _matrix2(100)
+    eps = 2 * np.linalg.norm(a)
+    got = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), qbfac.StopRule.fixed_precision(eps), 10, 0,
+                           qbfac.RngStream(1))
+    assert got.rank == 0 and got.terminated_by == "tolerance_met" and got.passes == 1
+
+
+def test_ei_tolerance_floor_error(ctx):
+    from paper_1606_09402_b200 import qbfac
+    a = _matrix2(100)
+    with pytest.raises(qbfac.ToleranceFloorError) as ei:
+        qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), qbfac.StopRule.fixed_precision(1e-8 * np.linalg.norm(a)),
+                         10, 0, qbfac.RngStream(1))
+    assert abs(ei.value.floor - np.sqrt(4 * 1.1102230246251565e-16 / 0.01) * np.linalg.norm(a)) < 1e-20
+
+
+def test_ei_exact_low_rank_collapse(ctx, oracle):
+    """Exact rank-15 A with a tiny tolerance: the third block's sketch is rank deficient."""
+    from paper_1606_09402_b200 import matgen, qbfac
+    rs = np.random.default_rng(0)
+    a = np.asfortranarray(rs.standard_normal((120, 15)) @ rs.standard_normal((15, 90)))
+    eps = 1e-6 * np.linalg.norm(a)
+    ref = oracle.run("ei", a, b=10, power=0, eps_abs=eps, seed=8)
+    got = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), qbfac.StopRule.fixed_precision(eps), 10, 0,
+                           qbfac.RngStream(8))
+    assert got.rank == ref.rank and got.terminated_by == ref.terminated_by
+    assert np.linalg.norm(a - got.Q @ got.B) <= 1e-10 * np.linalg.norm(a)
+
+
+@pytest.mark.parametrize("m,n,per_row,b,P,eps_rel,cap", [(3000, 1500, 20, 20, 1, 0.5, 200),
+                                                       (2000, 3000, 10, 16, 0, 0.3, 400)])
+def test_ei_sparse(ctx, oracle, m, n, per_row, b, P, eps_rel, cap):
+    from paper_1606_09402_b200 import matgen, qbfac
+    csr = matgen.csr_uniform(m, n, per_row, seed=m)
+    eps = eps_rel * np.sqrt(oracle.csr_frob_sq(csr))
+    ref = oracle.run("ei", csr=csr, b=b, power=P, eps_abs=eps, max_rank=cap, seed=42)
+    got = qbfac.rand_qb_ei(qbfac.MatrixHandle.csr(*csr, ctx=ctx), qbfac.StopRule.fixed_precision(eps), b, P,
+                           qbfac.RngStream(42), max_rank=cap)
+    _compare(got, ref, csr=csr, oracle=oracle)
+
+
+def test_ei_sparse_vs_dense_same_result(ctx, oracle):
+    """CSR and densified A give the same factorization."""
+    from paper_1606_09402_b200 import matgen, qbfac
+    csr = matgen.csr_uniform(500, 400, 12, seed=2)
+    dense = matgen.csr_to_dense(csr)
+    eps = 0.5 * np.linalg.norm(dense)
+    g1 = qbfac.rand_qb_ei(qbfac.MatrixHandle.csr(*csr, ctx=ctx), qbfac.StopRule.fixed_precision(eps), 10, 1,
+                          qbfac.RngStream(4))
+    g2 = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(dense, ctx), qbfac.StopRule.fixed_precision(eps), 10, 1,
+                          qbfac.RngStream(4))
+    assert g1.rank == g2.rank
+    np.testing.assert_allclose(_sv(g1.B), _sv(g2.B), rtol=1e-10)
+
+
+# ---- randQB_FP ------------------------------------------------------------------------------
+@pytest.mark.parametrize("n,b,P,eps_rel,l", [(400, 10, 1, 1e-2, 200), (300, 10, 0, 1e-4, 300),
+                                            (500, 25, 2, 5e-2, 250)])
+def test_fp_dense(ctx, oracle, n, b, P, eps_rel, l):
+    from paper_1606_09402_b200 import matgen, qbfac
+    a = matgen.synthesize(n, n, matgen.spectrum("inv", n), 11)
+    eps = eps_rel * np.linalg.norm(a)
+    ref = oracle.run("fp", a, b=b, power=P, eps_abs=eps, l_budget=l, seed=6)
+    got = qbfac.rand_qb_fp(qbfac.MatrixHandle.dense(a, ctx), eps, b, P, l, qbfac.RngStream(6))
+    _compare(got, ref, a=a, oracle=oracle)
+
+
+def test_fp_restart(ctx, oracle):
+    """Sketch budget too small -> fresh Omega from rng.substream(r)."""
+    from paper_1606_09402_b200 import qbfac
+    a = _matrix2(300)
+    eps = 1e-5 * np.linalg.norm(a)
+    ref = oracle.run("fp", a, b=10, power=1, eps_abs=eps, l_budget=30, seed=2)
+    got = qbfac.rand_qb_fp(qbfac.MatrixHandle.dense(a, ctx), eps, 10, 1, 30, qbfac.RngStream(2))
+    assert got.info["restarts"] >= 1
+    _compare(got, ref, a=a, oracle=oracle)
+
+
+@pytest.mark.parametrize("reorth", [True, False])
+def test_fp_fixed_rank(ctx, oracle, reorth):
+    from paper_1606_09402_b200 import qbfac
+    a = _matrix2(300)
+    ref = oracle.run("fp_fixed_rank", a, b=10, fixed_rank=(60, 10), reorth=reorth, seed=1)
+    got = qbfac.rand_qb_fp_fixed_rank(qbfac.MatrixHandle.dense(a, ctx), 60, 10, 10, reorth, qbfac.RngStream(1))
+    assert got.passes == 2 and got.rank == 70
+    _compare(got, ref, a=a, oracle=oracle, tol=1e-8 if not reorth else TOL)
+
+
+def test_single_pass_cfg4_shape_small(ctx, oracle):
+    """Config-4 recipe at reduced size (rank-60 factors + 1e-6 noise), single pass l=60, b=20."""
+    from paper_1606_09402_b200 import matgen, qbfac
+    a = matgen.cfg4_matrix(m=1200, n=800, r=60, seed=4)
+    ref = oracle.run("single_pass", a, b=20, fixed_rank=(60, 0), seed=42)
+    got = qbfac.single_pass_fp(qbfac.MatrixHandle.dense(a, ctx), 60, 20, qbfac.RngStream(42))
+    assert got.passes == 1 and ref.passes == 1
+    _compare(got, ref, a=a, oracle=oracle)
+
+
+def test_fp_ei_equivalence(ctx):
+    """Propositions 1-2: EI and FP fixed rank with the same Omega span the same subspace."""
+    from paper_1606_09402_b200 import qbfac
+    a = _matrix2(300)
+    ei = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), qbfac.StopRule.fixed_rank(60, 0), 10, 0,
+                          qbfac.RngStream(7))
+    fp = qbfac.rand_qb_fp_fixed_rank(qbfac.MatrixHandle.dense(a, ctx), 60, 0, 10, True, qbfac.RngStream(7))
+    p1 = ei.Q @ ei.Q.T
+    p2 = fp.Q @ fp.Q.T
+    assert np.linalg.norm(p1 - p2) <= 1e-6
+    assert np.linalg.norm(ei.Q @ ei.B - fp.Q @ fp.B) <= 1e-6 * np.linalg.norm(a)
+
+
+def test_determinism(ctx):
+    from paper_1606_09402_b200 import qbfac
+    a = _matrix2(300)
+    eps = 1e-4 * np.linalg.norm(a)
+    r1 = qbfac.rand_qb_fp(qbfac.MatrixHandle.dense(a, ctx), eps, 10, 1, 100, qbfac.RngStream(3))
+    r2 = qbfac.rand_qb_fp(qbfac.MatrixHandle.dense(a, ctx), eps, 10, 1, 100, qbfac.RngStream(3))
+    assert np.array_equal(r1.Q, r2.Q) and np.array_equal(r1.B, r2.B)
