@@ -145,6 +145,10 @@ int qbfac_gpu_frob_norm_sq(qbfac_gpu_ctx* ctx, qbfac_gpu_matrix* mat, double* ou
 /* Y = A X (trans = 0) or A^T X (trans = 1), host column-major buffers; one pass. */
 int qbfac_gpu_multiply(qbfac_gpu_ctx* ctx, qbfac_gpu_matrix* mat, const double* x, int64_t w, int trans,
                        double* y);
+/* Same product on device buffers: X (w columns) and Y row-major with leading dimensions
+ * ldx, ldy (the layout of the engine's block vectors); ordered on qbfac_gpu_stream(). */
+int qbfac_gpu_multiply_device(qbfac_gpu_ctx* ctx, qbfac_gpu_matrix* mat, const double* x, int64_t ldx, int64_t w,
+                              int trans, double* y, int64_t ldy);
 /* gaussian(rows, cols, rng) after `skip` earlier draws, into a host column-major buffer. */
 int qbfac_gpu_gaussian(qbfac_gpu_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t skip, int64_t rows,
                        int64_t cols, double* out);

@@ -173,6 +173,18 @@ int qbfac_gpu_multiply(qbfac_gpu_ctx* ctx, qbfac_gpu_matrix* mat, const double* 
     });
 }
 
+int qbfac_gpu_multiply_device(qbfac_gpu_ctx* ctx, qbfac_gpu_matrix* mat, const double* x, int64_t ldx, int64_t w,
+                              int trans, double* y, int64_t ldy) {
+    return guard(ctx, [&] {
+        auto& a = *mat->m;
+        const int64_t xr = trans ? a.m : a.n;
+        const int64_t yr = trans ? a.n : a.m;
+        qbgpu::MatView xv{const_cast<double*>(x), xr, w, ldx, true};
+        qbgpu::MatView yv{y, yr, w, ldy, true};
+        qbgpu::multiply(*ctx->c, a, xv, yv, trans != 0);
+    });
+}
+
 int qbfac_gpu_gaussian(qbfac_gpu_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t skip, int64_t rows, int64_t cols,
                        double* out) {
     return guard(ctx, [&] {

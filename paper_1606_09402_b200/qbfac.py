@@ -124,6 +124,7 @@ def lib():
         L.qbfac_gpu_matrix_passes.restype = I64
         L.qbfac_gpu_frob_norm_sq.argtypes = [P, P, P]
         L.qbfac_gpu_multiply.argtypes = [P, P, P, I64, I, P]
+        L.qbfac_gpu_multiply_device.argtypes = [P, P, P, I64, I64, I, P, I64]
         L.qbfac_gpu_gaussian.argtypes = [P, U64, U64, U64, I64, I64, P]
         L.qbfac_gpu_gaussian_device.argtypes = [P, U64, U64, U64, I64, I64, P, I64]
         L.qbfac_gpu_run.argtypes = [P, P, P, PP, P]
@@ -375,6 +376,11 @@ class MatrixHandle:
         self.ctx.check(lib().qbfac_gpu_multiply(self.ctx.handle, self._h, _p(x), x.shape[1], int(transpose_a),
                                                 _p(y)))
         return y
+
+    def multiply_device(self, x_ptr: int, ldx: int, w: int, transpose_a: bool, y_ptr: int, ldy: int):
+        """Device-buffer product (row-major X, Y) on the context stream; one pass."""
+        self.ctx.check(lib().qbfac_gpu_multiply_device(self.ctx.handle, self._h, C.c_void_p(x_ptr), ldx, w,
+                                                       int(transpose_a), C.c_void_p(y_ptr), ldy))
 
     def free(self):
         if getattr(self, "_h", None):
