@@ -7,6 +7,7 @@
  *                            (replaces kernels::gemm_nn / gemm_tn, kernels_drivers.cpp:21-65)
  *   qbfac_gpu_test_chol      the in-CTA Cholesky + inverse used by CholQR
  *   qbfac_gpu_test_householder  the Householder panel QR (orth_qr, qr.hpp:15-18)
+ *   qbfac_gpu_test_orth_wide the power step's orth() of a wide sketch (CholQR2 or BCGS2)
  *   qbfac_gpu_test_colsumsq  per-column sums of squares (the indicator's row norms)
  *   qbfac_gpu_test_csr_spmm  CSR pass Y = alpha A X + beta Y on device arrays
  *                            (replaces csr_gemm_n, kernels_drivers.cpp:67-79)
@@ -30,6 +31,8 @@ int qbfac_gpu_test_gemm(qbfac_gpu_ctx* ctx, double alpha, const double* a, int64
 int qbfac_gpu_test_chol(qbfac_gpu_ctx* ctx, const double* g, int b, double* r, double* rinv, int* status);
 /* Householder QR of a column-major m x b panel in place (Q overwrites y); R col-major ld b. */
 int qbfac_gpu_test_householder(qbfac_gpu_ctx* ctx, double* y, int64_t m, int b, int64_t ld, double* r);
+/* Orthonormalise a wide row-major rows x l panel in place (CholQR2 / BCGS2, the power step's orth). */
+int qbfac_gpu_test_orth_wide(qbfac_gpu_ctx* ctx, double* x, int64_t rows, int64_t l, int force_bcgs2);
 int qbfac_gpu_test_colsumsq(qbfac_gpu_ctx* ctx, const double* x, int64_t rows, int64_t cols, int64_t ld, int row,
                             double* out);
 int qbfac_gpu_test_csr_spmm(qbfac_gpu_ctx* ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* rp,

@@ -341,6 +341,12 @@ int qbfac_gpu_test_householder(qbfac_gpu_ctx* ctx, double* y, int64_t m, int b, 
     });
 }
 
+int qbfac_gpu_test_orth_wide(qbfac_gpu_ctx* ctx, double* x, int64_t rows, int64_t l, int force_bcgs2) {
+    return guard(ctx, [&] {
+        qbgpu::test_orth_wide(*ctx->c, qbgpu::MatView{x, rows, l, l, true}, force_bcgs2 != 0);
+    });
+}
+
 int qbfac_gpu_test_colsumsq(qbfac_gpu_ctx* ctx, const double* x, int64_t rows, int64_t cols, int64_t ld, int row,
                             double* out) {
     return guard(ctx, [&] {

@@ -105,7 +105,7 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, 
 __global__ void __launch_bounds__(WM * WN * 32)
 dgemm_kernel(const double* __restrict__ A, std::int64_t lda, const double* __restrict__ B,
              std::int64_t ldb, double* __restrict__ C, std::int64_t ldc, int c_row, int M, int N,
-             int K, int k_split_len, double alpha, double beta, double* __restrict__ partial) {
+             int K, int k_split_len, double alpha, double beta, double* __restrict__ partial, int flags) {
     using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
     extern __shared__ __align__(16) double smem[];
     double* sA = smem;
@@ -114,8 +114,10 @@ dgemm_kernel(const double* __restrict__ A, std::int64_t lda, const double* __res
     const int m0 = blockIdx.x * BM;
     const int n0 = blockIdx.y * BN;
     const int kz = blockIdx.z;
+    if ((flags & kGemmUpperC) && m0 >= n0 + BN) return;  // tile strictly below the diagonal
     const int k_begin = kz * k_split_len;
-    const int k_end = min(K, k_begin + k_split_len);
+    int k_end = min(K, k_begin + k_split_len);
+    if (flags & kGemmTriB) k_end = min(k_end, n0 + BN);   // B upper triangular: rows >= n0+BN are 0
     const int ntiles = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -220,17 +222,28 @@ dgemm_kernel(const double* __restrict__ A, std::int64_t lda, const double* __res
     }
 }
 
-__global__ void splitk_reduce_kernel(const double* __restrict__ partial, int splits, int M, int N,
-                                     double alpha, double beta, double* __restrict__ C,
-                                     std::int64_t ldc, int c_row) {
+// Deterministic split-K reduction: a CTA owns 32 consecutive outputs (lanes); warp g
+// sums splits g, g+8, ... in order, then warp 0 adds the 8 group sums in order.
+__global__ void __launch_bounds__(256)
+splitk_reduce_kernel(const double* __restrict__ partial, int splits, int M, int N, double alpha, double beta,
+                     double* __restrict__ C, std::int64_t ldc, int c_row, int flags, int bm, int bn) {
+    __shared__ double sh[8][33];
     const std::int64_t total = static_cast<std::int64_t>(M) * N;
-    for (std::int64_t idx = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-         idx < total; idx += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        double s = 0.0;
-        for (int z = 0; z < splits; ++z) s += partial[z * total + idx];  // fixed order
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const std::int64_t idx = static_cast<std::int64_t>(blockIdx.x) * 32 + lane;
+    double s = 0.0;
+    if (idx < total)
+        for (int z = g; z < splits; z += 8) s += partial[z * total + idx];
+    sh[g][lane] = s;
+    __syncthreads();
+    if (g == 0 && idx < total) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t += sh[q][lane];
         const std::int64_t row = idx % M, col = idx / M;
+        if ((flags & kGemmUpperC) && (row / bm) * bm >= (col / bn) * bn + bn) return;
         double* cp = c_row ? C + row * ldc + col : C + row + col * ldc;
-        const double v = alpha * s;
+        const double v = alpha * t;
         *cp = beta == 0.0 ? v : v + beta * (*cp);
     }
 }
@@ -244,7 +257,7 @@ struct Launch {
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int VEC>
 void launch_cfg(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc,
                 bool c_row, int M, int N, int K, int splits, int klen, double alpha, double beta,
-                double* partial) {
+                double* partial, int flags) {
     using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
     auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, AR, BR, VEC>;
     static bool configured = false;  // per template instance
@@ -255,7 +268,7 @@ void launch_cfg(cudaStream_t st, const MatView& a, const MatView& b, double* c, 
     dim3 grid(static_cast<unsigned>(ceil_div(M, BM)), static_cast<unsigned>(ceil_div(N, BN)),
               static_cast<unsigned>(splits));
     kern<<<grid, T::NT, T::SMEM_BYTES, st>>>(a.p, a.ld, b.p, b.ld, c, ldc, c_row ? 1 : 0, M, N, K,
-                                            klen, alpha, beta, partial);
+                                            klen, alpha, beta, partial, flags);
     QB_LAUNCH_CHECK();
 }
 
@@ -267,27 +280,27 @@ enum class Family { kWide, kSkinny, kNarrow };
 template <Family F, bool AR, bool BR, int VEC>
 void launch_family(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc,
                    bool c_row, int M, int N, int K, int splits, int klen, double alpha, double beta,
-                   double* partial) {
+                   double* partial, int flags) {
     if constexpr (F == Family::kWide)
         launch_cfg<128, 128, 16, 2, 4, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
-                                                       alpha, beta, partial);
+                                                       alpha, beta, partial, flags);
     else if constexpr (F == Family::kSkinny)
         launch_cfg<128, 64, 16, 4, 2, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
-                                                      alpha, beta, partial);
+                                                      alpha, beta, partial, flags);
     else
         launch_cfg<64, 32, 32, 2, 2, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
-                                                     alpha, beta, partial);
+                                                     alpha, beta, partial, flags);
 }
 
 template <Family F>
 void dispatch_layout(cudaStream_t st, const MatView& a, const MatView& b, double* c,
                      std::int64_t ldc, bool c_row, int M, int N, int K, int splits, int klen,
-                     double alpha, double beta, double* partial, bool vec2) {
+                     double alpha, double beta, double* partial, bool vec2, int flags) {
 #define QB_DISPATCH(AR_, BR_)                                                                    \
     if (vec2) launch_family<F, AR_, BR_, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, \
-                                            beta, partial);                                      \
+                                            beta, partial, flags);                               \
     else launch_family<F, AR_, BR_, 1>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, \
-                                       partial);
+                                       partial, flags);
     if (a.rowmajor) {
         if (b.rowmajor) { QB_DISPATCH(true, true) } else { QB_DISPATCH(true, false) }
     } else {
@@ -313,7 +326,7 @@ int gemm_num_sms() {
 }
 
 void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const MatView& b,
-          double beta, const MatView& c) {
+          double beta, const MatView& c, int flags) {
     const std::int64_t M = a.rows, K = a.cols, N = b.cols;
     if (b.rows != K || c.rows != M || c.cols != N)
         throw QbError(kDimensionError, "gemm: inner dimension mismatch");
@@ -337,7 +350,8 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     int splits = 1;
     if (tiles < want) {
         const std::int64_t max_by_k = std::max<std::int64_t>(1, K / (4 * bk));  // >= 4 k-tiles/split
-        splits = static_cast<int>(std::min<std::int64_t>(std::min<std::int64_t>(ceil_div(want, tiles), max_by_k), 64));
+        const std::int64_t cap = (M * N <= 65536) ? 512 : 64;  // small outputs (Grams): deep split-K
+        splits = static_cast<int>(std::min<std::int64_t>(std::min<std::int64_t>(ceil_div(want, tiles), max_by_k), cap));
     }
     int klen = static_cast<int>(round_up(ceil_div(K, splits), bk));
     splits = static_cast<int>(ceil_div(K, klen));
@@ -347,22 +361,20 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     switch (fam) {
         case Family::kWide:
             dispatch_layout<Family::kWide>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits,
-                                           klen, alpha, beta, partial, vec2);
+                                           klen, alpha, beta, partial, vec2, flags);
             break;
         case Family::kSkinny:
             dispatch_layout<Family::kSkinny>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K,
-                                             splits, klen, alpha, beta, partial, vec2);
+                                             splits, klen, alpha, beta, partial, vec2, flags);
             break;
         default:
             dispatch_layout<Family::kNarrow>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K,
-                                             splits, klen, alpha, beta, partial, vec2);
+                                             splits, klen, alpha, beta, partial, vec2, flags);
     }
     if (splits > 1) {
         const std::int64_t total = M * N;
-        const int threads = 256;
-        const int blocks = static_cast<int>(std::min<std::int64_t>(ceil_div(total, threads), 4L * sms * 8));
-        splitk_reduce_kernel<<<blocks, threads, 0, st>>>(partial, splits, (int)M, (int)N, alpha, beta,
-                                                         c.p, c.ld, c.rowmajor ? 1 : 0);
+        splitk_reduce_kernel<<<static_cast<unsigned>(ceil_div(total, 32)), 256, 0, st>>>(
+            partial, splits, (int)M, (int)N, alpha, beta, c.p, c.ld, c.rowmajor ? 1 : 0, flags, bm, bn);
         QB_LAUNCH_CHECK();
     }
 }

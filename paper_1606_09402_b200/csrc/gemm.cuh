@@ -38,8 +38,13 @@ int gemm_num_sms();
 
 // C = alpha * A * B + beta * C, all FP64 views in device memory (any layouts).
 // beta == 0 never reads C. Deterministic (fixed split-K reduction order).
+// flags: kGemmTriB   - B is upper triangular (K range of an output tile limited);
+//        kGemmUpperC - only tiles touching the upper triangle of C are computed
+//                      (symmetric results such as Grams; the strict lower part is untouched).
+constexpr int kGemmTriB = 1;
+constexpr int kGemmUpperC = 2;
 void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const MatView& b,
-          double beta, const MatView& c);
+          double beta, const MatView& c, int flags = 0);
 
 // ---- small.cu -------------------------------------------------------------------
 void scale_matrix(cudaStream_t st, const MatView& c, double beta);
@@ -70,6 +75,9 @@ void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, doubl
 // C = A * B for upper-triangular b x b (col-major, ld); C must not alias.
 void trmm_upper_small(cudaStream_t st, const double* a, const double* b, double* c, int n,
                       std::int64_t ld);
+// c0 = a0*b0 and (if c1) c1 = a1*b1 for upper-triangular n x n, one launch.
+void trmm_upper_pair(cudaStream_t st, const double* a0, const double* b0, double* c0, const double* a1,
+                     const double* b1, double* c1, int n, std::int64_t ld);
 // Rinv = R^{-1} for upper-triangular R (one CTA).
 void tri_inverse_small(cudaStream_t st, const double* r, double* rinv, int n, std::int64_t ld);
 

@@ -239,8 +239,8 @@ public:
                         std::isfinite(s0.diag_max) && std::isfinite(s1.diag_max);
         if (ok) {
             gemm(1.0, t1, small(kRbinv, b, b), 0.0, qout);
-            trmm_upper_small(st_, slot(kRb), slot(kRa), slot(r_slot), b, kSmallMax);
-            trmm_upper_small(st_, slot(kRainv), slot(kRbinv), slot(rinv_slot), b, kSmallMax);
+            trmm_upper_pair(st_, slot(kRb), slot(kRa), slot(r_slot), slot(kRainv), slot(kRbinv), slot(rinv_slot), b,
+                            kSmallMax);
             return b;
         }
         // Householder fallback: exact deficiency decisions (qr.hpp:15-21).
@@ -264,9 +264,99 @@ public:
         return d;
     }
 
+    // Blocked right-looking Cholesky of the l x l SPD matrix W (column-major, upper
+    // triangle read, overwritten) into R (upper) and R^{-1}, both column-major (ld l).
+    // Diagonal blocks use chol_small (which also returns their inverses); the row panel
+    // is R_kk^{-T} W_k,rest and the trailing update a DMMA SYRK on upper tiles only.
+    // Off-diagonal blocks of R^{-1} follow column by column:
+    //   Rinv[:j, j] = -(Rinv[:j,:j] R[:j, j]) Rinv_jj.
+    // Returns false on breakdown or when min diag(R) < kCholRatioMin * max diag(R).
+    bool chol_blocked(double* w, int l, double* r, double* rinv, double max_gram_dev) {
+        const int nb = 64;
+        const int nt = static_cast<int>(ceil_div(l, nb));
+        QB_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * l * l, st_));
+        QB_CUDA(cudaMemsetAsync(rinv, 0, sizeof(double) * l * l, st_));
+        if (stat_.n < static_cast<std::size_t>(nt) * 4) stat_ = DBuf(static_cast<std::size_t>(nt) * 4, st_);
+        auto* stats = reinterpret_cast<SmallStatus*>(stat_.p);
+        static_assert(sizeof(SmallStatus) <= 4 * sizeof(double), "status size");
+        for (int kb = 0; kb < nt; ++kb) {
+            const int k0 = kb * nb, w0 = std::min(nb, l - k0), rest = l - k0 - w0;
+            chol_small(st_, w + k0 + static_cast<std::int64_t>(k0) * l, l, w0, r + k0 + static_cast<std::int64_t>(k0) * l,
+                       rinv + k0 + static_cast<std::int64_t>(k0) * l, l,
+                       reinterpret_cast<SmallStatus*>(reinterpret_cast<double*>(stats) + 4 * kb));
+            if (rest > 0) {
+                MatView rkk_inv{rinv + k0 + static_cast<std::int64_t>(k0) * l, w0, w0, l, false};
+                MatView wp{w + k0 + static_cast<std::int64_t>(k0 + w0) * l, w0, rest, l, false};
+                MatView rp{r + k0 + static_cast<std::int64_t>(k0 + w0) * l, w0, rest, l, false};
+                gemm(1.0, rkk_inv.t(), wp, 0.0, rp);
+                MatView wt{w + (k0 + w0) + static_cast<std::int64_t>(k0 + w0) * l, rest, rest, l, false};
+                qbgpu::gemm(st_, c_.ws_gemm, -1.0, rp.t(), rp, 1.0, wt, kGemmUpperC);
+            }
+        }
+        for (int jb = 1; jb < nt; ++jb) {
+            const int j0 = jb * nb, wj = std::min(nb, l - j0);
+            if (tri_.n < static_cast<std::size_t>(j0) * nb) tri_ = DBuf(static_cast<std::size_t>(l) * nb, st_);
+            MatView t{tri_.p, j0, wj, j0, false};
+            MatView rinv_tl{rinv, j0, j0, l, false};
+            MatView r_col{r + static_cast<std::int64_t>(j0) * l, j0, wj, l, false};
+            gemm(1.0, rinv_tl, r_col, 0.0, t);
+            MatView rinv_jj{rinv + j0 + static_cast<std::int64_t>(j0) * l, wj, wj, l, false};
+            MatView rinv_col{rinv + static_cast<std::int64_t>(j0) * l, j0, wj, l, false};
+            gemm(-1.0, t, rinv_jj, 0.0, rinv_col);
+        }
+        std::vector<SmallStatus> hs(static_cast<std::size_t>(nt));
+        for (int kb = 0; kb < nt; ++kb)
+            QB_CUDA(cudaMemcpyAsync(&hs[kb], reinterpret_cast<double*>(stats) + 4 * kb, sizeof(SmallStatus),
+                                    cudaMemcpyDeviceToHost, st_));
+        QB_CUDA(cudaStreamSynchronize(st_));
+        double dmin = INFINITY, dmax = 0.0, dev = 0.0;
+        for (const auto& s : hs) {
+            if (s.breakdown || !std::isfinite(s.diag_max)) return false;
+            dmin = std::min(dmin, s.diag_min);
+            dmax = std::max(dmax, s.diag_max);
+            dev = std::max(dev, s.gram_dev);
+        }
+        return dmax > 0.0 && dmin >= kCholRatioMin * dmax && dev <= max_gram_dev;
+    }
+
+    // CholQR2 of a wide panel X (rows x l, row-major) in place with one l x l Gram per
+    // pass (DMMA SYRK), blocked Cholesky, and X R^{-1} as a triangular-B GEMM.
+    // Returns false (X unchanged or already orthonormalised once) when the Gram is
+    // too ill-conditioned; orth_wide then falls back to BCGS2.
+    bool orth_wide_cholqr2(const MatView& x, bool sharded) {
+        const int l = static_cast<int>(x.cols);
+        const std::size_t ll = static_cast<std::size_t>(l) * l;
+        if (wide_.n < 3 * ll) wide_ = DBuf(3 * ll, st_);
+        if (wide_y_.n < static_cast<std::size_t>(x.rows) * l) wide_y_ = DBuf(static_cast<std::size_t>(x.rows) * l, st_);
+        double* g = wide_.p;
+        double* r = wide_.p + ll;
+        double* rinv = wide_.p + 2 * ll;
+        MatView y{wide_y_.p, x.rows, l, l, true};
+        MatView gv{g, l, l, l, false};
+        MatView rinv_v{rinv, l, l, l, false};
+        for (int pass = 0; pass < 2; ++pass) {
+            const MatView& src = pass == 0 ? x : y;
+            const MatView& dst = pass == 0 ? y : x;
+            qbgpu::gemm(st_, c_.ws_gemm, 1.0, src.t(), src, 0.0, gv, kGemmUpperC);
+            if (sharded) c_.allreduce(g, ll);
+            if (!chol_blocked(g, l, r, rinv, pass == 0 ? INFINITY : kCholGramDevMax)) {
+                if (pass == 1) copy_matrix(st_, y, x);
+                return false;
+            }
+            qbgpu::gemm(st_, c_.ws_gemm, 1.0, src, rinv_v, 0.0, dst, kGemmTriB);
+        }
+        return true;
+    }
+
     // Orthonormal basis of the leading-column spans of X (rows x l) in place:
-    // block Gram-Schmidt with re-orthogonalisation (BCGS2) over CholQR2 panels.
+    // CholQR2 with one wide Gram when well conditioned, else block Gram-Schmidt with
+    // re-orthogonalisation (BCGS2) over CholQR2 panels.
     void orth_wide(const MatView& x, bool sharded, DBuf& tmp, DBuf& sbuf) {
+        if (x.cols > kSmallMax && x.rowmajor && x.ld == x.cols && orth_wide_cholqr2(x, sharded)) return;
+        orth_wide_bcgs2(x, sharded, tmp, sbuf);
+    }
+
+    void orth_wide_bcgs2(const MatView& x, bool sharded, DBuf& tmp, DBuf& sbuf) {
         const std::int64_t l = x.cols;
         const std::int64_t bw = 64;
         for (std::int64_t j0 = 0; j0 < l; j0 += bw) {
@@ -288,7 +378,7 @@ public:
     std::int64_t hh_fallbacks = 0;
 
 private:
-    DBuf scratch_t_;
+    DBuf scratch_t_, stat_, tri_, wide_, wide_y_;
     Context& c_;
     Matrix& a_;
     cudaStream_t st_;
@@ -582,8 +672,8 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
                 const int d2 = eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp);
                 if (d2 == 0) { term = 3; stop = true; break; }
                 d = std::min(d, d2);
-                trmm_upper_small(c.st, eng.slot(kR2), eng.slot(kR1), eng.slot(kR), d, kSmallMax);
-                trmm_upper_small(c.st, eng.slot(kR1inv), eng.slot(kR2inv), eng.slot(kRinv), d, kSmallMax);
+                trmm_upper_pair(c.st, eng.slot(kR2), eng.slot(kR1), eng.slot(kR), eng.slot(kR1inv), eng.slot(kR2inv),
+                                eng.slot(kRinv), d, kSmallMax);
                 r_slot = kR;
                 rinv_slot = kRinv;
             }
@@ -615,6 +705,17 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
 }
 
 }  // namespace
+
+// ---- test hook: the wide orthonormalisation used by the power iteration ----------------
+void test_orth_wide(Context& c, const MatView& x, bool force_bcgs2) {
+    Matrix dummy;
+    Engine eng(c, dummy);
+    DBuf tmp(static_cast<std::size_t>(std::max<std::int64_t>(x.rows, 1)) * 64, c.st);
+    DBuf sbuf(static_cast<std::size_t>(std::max<std::int64_t>(x.cols, 64)) * 64, c.st);
+    if (force_bcgs2) eng.orth_wide_bcgs2(x, false, tmp, sbuf);
+    else eng.orth_wide(x, false, tmp, sbuf);
+    QB_CUDA(cudaStreamSynchronize(c.st));
+}
 
 // ---- operator layer ------------------------------------------------------------------
 double frob_norm_sq(Context& c, Matrix& a) {

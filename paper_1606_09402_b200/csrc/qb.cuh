@@ -125,6 +125,9 @@ struct Result {
 
 std::unique_ptr<Result> run(Context& c, Matrix& a, const Params& p);
 
+// Kernel-level hook (include/qbfac_gpu_testing.h): orthonormalise a wide row-major panel.
+void test_orth_wide(Context& c, const MatView& x, bool force_bcgs2);
+
 // Operator layer (MatrixHandle::frob_norm_sq / multiply) on device buffers.
 double frob_norm_sq(Context& c, Matrix& a);
 // Y (rows x w, row-major) = op(A) X (row-major), one pass; A^T results are allreduced.

@@ -147,101 +147,130 @@ __global__ void colsumsq_stage2(const double* __restrict__ partial, int nblk, st
     }
 }
 
-// Cholesky of the b x b Gram by symmetric Gaussian elimination on [G | I]:
-// after step k row k holds R(k,:) on the left and (R^{-T})(k,:) on the right.
-constexpr int kCholThreads = 1024;
+// Cholesky of the b x b Gram by symmetric Gaussian elimination on [G | I]
+// (shared memory, b x (2b+1) doubles). Step k eliminates rows i > k with the
+// UNSCALED row k over the contiguous column range [k+1, b+k] (left part of G plus
+// the lower-triangular right part), while row k-1 is scaled by 1/sqrt(pivot) in the
+// same phase (disjoint rows), so each step costs one barrier. At the end row k holds
+// R(k,:) on the left and (R^{-T})(k,:) on the right. 32 x 32 threads, no integer
+// division in the inner loops.
+constexpr int kCholTx = 32, kCholTy = 32;
 
-__global__ void __launch_bounds__(kCholThreads)
+__global__ void __launch_bounds__(kCholTx * kCholTy)
 chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double* __restrict__ r,
                   double* __restrict__ rinv, std::int64_t ldr, SmallStatus* status) {
     extern __shared__ double w[];
     const int ldw = 2 * b + 1;
-    __shared__ int s_break, s_bad;
-    __shared__ double s_piv;
-    __shared__ double s_dev;
-    if (threadIdx.x == 0) { s_break = 0; s_bad = -1; s_dev = 0.0; }
-    // load [G | I] (symmetrise from the upper triangle so both halves agree bitwise)
-    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
-        const int i = idx % b, j = idx / b;
-        const double v = i <= j ? g[i + j * ldg] : g[j + i * ldg];
-        w[i * ldw + j] = v;
-        w[i * ldw + b + j] = (i == j) ? 1.0 : 0.0;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = ty * kCholTx + tx;
+    __shared__ double s_red[kCholTy];
+    __shared__ int s_bad;
+    if (tid == 0) s_bad = -1;
+    double dev = 0.0;
+    for (int j = ty; j < b; j += kCholTy) {
+        for (int i = tx; i < b; i += kCholTx) {
+            const double v = i <= j ? g[i + j * ldg] : g[j + i * ldg];
+            w[i * ldw + j] = v;
+            w[i * ldw + b + j] = (i == j) ? 1.0 : 0.0;
+            dev = fmax(dev, fabs(v - (i == j ? 1.0 : 0.0)));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_down_sync(0xffffffffu, dev, o));
+    if (tx == 0) s_red[ty] = dev;
+    __syncthreads();
+    double prev_s = 1.0;
+    for (int k = 0; k < b; ++k) {
+        const double piv = w[k * ldw + k];
+        const bool bad = !(piv > 0.0) || !isfinite(piv);
+        const double p = bad ? 1.0 : piv;
+        const double pinv = 1.0 / p;
+        if (bad && tid == 0 && s_bad < 0) s_bad = k;
+        // eliminate rows i > k with the unscaled row k
+        for (int i = k + 1 + ty; i < b; i += kCholTy) {
+            const double f = w[k * ldw + i] * pinv;
+            double* wi = w + i * ldw;
+            const double* wk = w + k * ldw;
+            for (int j = k + 1 + tx; j <= b + k; j += kCholTx) wi[j] = fma(-f, wk[j], wi[j]);
+        }
+        // deferred scaling of row k-1 (columns [k, b+k-1]) and its diagonal
+        if (k > 0) {
+            const double inv = 1.0 / prev_s;
+            double* wr = w + (k - 1) * ldw;
+            for (int j = k + tid; j <= b + k - 1; j += kCholTx * kCholTy) wr[j] *= inv;
+            if (tid == 0) wr[k - 1] = prev_s;
+        }
+        prev_s = sqrt(p);
+        __syncthreads();
+    }
+    {
+        const double inv = 1.0 / prev_s;
+        double* wr = w + (b - 1) * ldw;
+        for (int j = b + tid; j <= 2 * b - 1; j += kCholTx * kCholTy) wr[j] *= inv;
+        if (tid == 0) wr[b - 1] = prev_s;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
-        double dev = 0.0;
-        for (int idx = threadIdx.x; idx < b * b; idx += 32) {
-            const int i = idx % b, j = idx / b;
-            dev = fmax(dev, fabs(w[i * ldw + j] - (i == j ? 1.0 : 0.0)));
+    for (int j = ty; j < b; j += kCholTy) {
+        for (int i = tx; i < b; i += kCholTx) {
+            r[i + j * ldr] = i <= j ? w[i * ldw + j] : 0.0;
+            rinv[i + j * ldr] = i <= j ? w[j * ldw + b + i] : 0.0;
         }
-        for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_down_sync(0xffffffffu, dev, o));
-        if (threadIdx.x == 0) s_dev = dev;
     }
-    for (int k = 0; k < b; ++k) {
-        if (threadIdx.x == 0) {
-            const double piv = w[k * ldw + k];
-            if (!(piv > 0.0) || !isfinite(piv)) {
-                if (!s_break) { s_break = 1; s_bad = k; }
-                s_piv = 1.0;  // keep going with a harmless pivot; caller falls back
-            } else {
-                s_piv = sqrt(piv);
-            }
-        }
-        __syncthreads();
-        const double s = s_piv;
-        const double inv = 1.0 / s;
-        // scale row k (left cols k..b-1, right cols 0..k)
-        for (int j = threadIdx.x; j < 2 * b; j += blockDim.x) {
-            if ((j >= k && j < b) || (j >= b && j <= b + k)) {
-                if (j == k) w[k * ldw + k] = s;
-                else w[k * ldw + j] *= inv;
-            }
-        }
-        __syncthreads();
-        // eliminate rows i > k: row_i -= R(k,i) * row_k  (R(k,i) = scaled w[k][i])
-        const int rows = b - k - 1;
-        const int cols_left = b - k - 1;   // j in (k, b)
-        const int cols_right = k + 1;      // j in [b, b+k]
-        const int cols = cols_left + cols_right;
-        for (int idx = threadIdx.x; idx < rows * cols; idx += blockDim.x) {
-            const int i = k + 1 + idx / cols;
-            const int jj = idx % cols;
-            const int j = jj < cols_left ? k + 1 + jj : b + (jj - cols_left);
-            const double f = w[k * ldw + i];
-            w[i * ldw + j] = fma(-f, w[k * ldw + j], w[i * ldw + j]);
-        }
-        __syncthreads();
-    }
-    // outputs: R upper (left), Rinv = (right)^T, upper
-    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
-        const int i = idx % b, j = idx / b;
-        r[i + j * ldr] = i <= j ? w[i * ldw + j] : 0.0;
-        rinv[i + j * ldr] = i <= j ? w[j * ldw + b + i] : 0.0;
-    }
-    if (threadIdx.x == 0 && status) {
+    if (ty == 0 && status) {
         double dmin = INFINITY, dmax = 0.0;
-        for (int j = 0; j < b; ++j) {
+        for (int j = tx; j < b; j += kCholTx) {
             const double d = w[j * ldw + j];
             dmin = fmin(dmin, d);
             dmax = fmax(dmax, d);
         }
-        status->breakdown = s_break;
-        status->bad_index = s_bad;
-        status->diag_min = dmin;
-        status->diag_max = dmax;
-        status->gram_dev = s_dev;
+        double dv = tx < kCholTy ? s_red[tx] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) {
+            dmin = fmin(dmin, __shfl_down_sync(0xffffffffu, dmin, o));
+            dmax = fmax(dmax, __shfl_down_sync(0xffffffffu, dmax, o));
+            dv = fmax(dv, __shfl_down_sync(0xffffffffu, dv, o));
+        }
+        if (tx == 0) {
+            status->breakdown = s_bad >= 0 ? 1 : 0;
+            status->bad_index = s_bad;
+            status->diag_min = dmin;
+            status->diag_max = dmax;
+            status->gram_dev = dv;
+        }
     }
 }
 
-__global__ void trmm_upper_kernel(const double* __restrict__ a, const double* __restrict__ bm,
-                                  double* __restrict__ c, int n, std::int64_t ld) {
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-        const int i = idx % n, j = idx / n;
-        double s = 0.0;
-        if (i <= j)
-            for (int p = i; p <= j; ++p) s = fma(a[i + p * ld], bm[p + j * ld], s);
-        c[i + j * ld] = s;
-    }
+// C = A * B for upper-triangular n x n operands staged in shared memory; blockIdx.x
+// selects one of two independent products so R = Rb*Ra and Rinv = Ra^{-1} Rb^{-1}
+// are formed in one launch.
+struct TrmmPair {
+    const double* a[2];
+    const double* b[2];
+    double* c[2];
+};
+
+__global__ void __launch_bounds__(1024) trmm_upper_kernel(TrmmPair prm, int n, std::int64_t ld) {
+    extern __shared__ double sm[];
+    const int z = blockIdx.x;
+    const double* __restrict__ a = prm.a[z];
+    const double* __restrict__ bm = prm.b[z];
+    double* __restrict__ c = prm.c[z];
+    if (!c) return;
+    const int lds = n + 1;
+    double* sa = sm;              // sa[i * lds + p] = A(i, p)
+    double* sb = sm + n * lds;    // sb[j * lds + p] = B(p, j)
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int j = ty; j < n; j += 32)
+        for (int i = tx; i < n; i += 32) {
+            sa[i * lds + j] = a[i + j * ld];
+            sb[j * lds + i] = bm[i + j * ld];
+        }
+    __syncthreads();
+    for (int j = ty; j < n; j += 32)
+        for (int i = tx; i < n; i += 32) {
+            double s = 0.0;
+            if (i <= j)
+                for (int p = i; p <= j; ++p) s = fma(sa[i * lds + p], sb[j * lds + p], s);
+            c[i + j * ld] = s;
+        }
 }
 
 // Column j of R^{-1} by back substitution; one thread per column.
@@ -493,13 +522,27 @@ void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, doubl
                                      kSmallMax * (2 * kSmallMax + 1) * 8));
         configured = true;
     }
-    chol_small_kernel<<<1, kCholThreads, smem, st>>>(g, ldg, b, r, rinv, ldr, status);
+    chol_small_kernel<<<1, dim3(kCholTx, kCholTy), smem, st>>>(g, ldg, b, r, rinv, ldr, status);
     QB_LAUNCH_CHECK();
 }
 
 void trmm_upper_small(cudaStream_t st, const double* a, const double* b, double* c, int n,
                       std::int64_t ld) {
-    trmm_upper_kernel<<<1, 1024, 0, st>>>(a, b, c, n, ld);
+    trmm_upper_pair(st, a, b, c, nullptr, nullptr, nullptr, n, ld);
+}
+
+void trmm_upper_pair(cudaStream_t st, const double* a0, const double* b0, double* c0, const double* a1,
+                     const double* b1, double* c1, int n, std::int64_t ld) {
+    if (n < 1 || n > kSmallMax) throw QbError(kDimensionError, "trmm_upper: size out of range");
+    static bool configured = false;
+    if (!configured) {
+        QB_CUDA(cudaFuncSetAttribute(trmm_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     2 * kSmallMax * (kSmallMax + 1) * 8));
+        configured = true;
+    }
+    TrmmPair p{{a0, a1}, {b0, b1}, {c0, c1}};
+    const int smem = 2 * n * (n + 1) * static_cast<int>(sizeof(double));
+    trmm_upper_kernel<<<c1 ? 2 : 1, 1024, smem, st>>>(p, n, ld);
     QB_LAUNCH_CHECK();
 }
 

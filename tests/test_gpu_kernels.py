@@ -286,3 +286,28 @@ def test_csr_validation_errors(ctx, oracle, bad):
     assert expect == ("Error" if bad == "nan" else "FormatError")
     with pytest.raises(exc):
         qbfac.MatrixHandle.csr(m, n, rp, ci, v, ctx=ctx)
+
+
+@pytest.mark.parametrize("rows,l,bcgs2", [(3000, 300, 0), (3000, 300, 1), (8000, 2000, 0), (500, 130, 0)])
+def test_orth_wide_matches_householder(ctx, oracle, rows, l, bcgs2):
+    """orth() of the power step (Alg. 4 steps 4-5): same Q as the reference's Householder
+    QR with diag(R) >= 0 (qr.hpp:15-18), up to u * cond."""
+    L = _lib()
+    L.qbfac_gpu_test_orth_wide.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int]
+    rs = np.random.default_rng(rows + l)
+    # moderately ill-conditioned sketch: columns scaled over 4 decades
+    x = rs.standard_normal((rows, l)) * np.logspace(0, -4, l)
+    xd = _dev(x)  # row-major
+    import torch
+    torch.cuda.synchronize()
+    assert L.qbfac_gpu_test_orth_wide(ctx.handle, _ptr(xd), rows, l, bcgs2) == 0, L.qbfac_gpu_last_error(ctx.handle)
+    q = xd.cpu().numpy()
+    assert np.abs(q.T @ q - np.eye(l)).max() < 1e-13
+    if rows * l <= 1_000_000:
+        q_ref, _ = oracle.orth_qr(x)
+        assert np.abs(q - q_ref).max() < 1e-9
+    else:
+        # R = Q^T X must be upper triangular with a positive diagonal (same QR factor)
+        r = q.T @ x
+        assert np.abs(np.tril(r, -1)).max() <= 1e-10 * np.abs(r).max()
+        assert np.all(np.diag(r) > 0)
