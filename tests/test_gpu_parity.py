@@ -55,8 +55,10 @@ def _compare(gpu, ref, a=None, csr=None, oracle=None, tol=TOL, sv_floor=1e-6, la
             x_tol += 10 * abs(oracle.explicit_error(lane.Q, lane.B, a=a, csr=csr) - e_r)
         assert abs(e_g - e_r) <= x_tol, (e_g, e_r)
     if gpu.rank:
-        qtq = gpu.Q.T @ gpu.Q
-        assert np.abs(qtq - np.eye(gpu.rank)).max() < 1e-12
+        # orthogonality_loss (qr.hpp:28-29); Alg. 3 without re-orth loses it by design
+        loss_g = np.abs(gpu.Q.T @ gpu.Q - np.eye(gpu.rank)).sum(axis=1).max()
+        loss_r = np.abs(ref.Q.T @ ref.Q - np.eye(ref.rank)).sum(axis=1).max() if ref.rank else 0.0
+        assert loss_g < max(1e-12, 10 * loss_r), (loss_g, loss_r)
     if a is not None and gpu.rank and ref.rank:
         # B must be as faithful to Q^T A as the reference's own B is (FP's B_i formula
         # never touches A; this is its accuracy, independent of parity).
