@@ -18,6 +18,11 @@
 #include <algorithm>
 #include <cstdio>
 
+#ifndef QB_WIDE_BK
+#define QB_WIDE_BK 32
+#define QB_WIDE_STAGES 3
+#endif
+
 namespace qbgpu {
 
 namespace {
@@ -281,8 +286,12 @@ template <Family F, bool AR, bool BR, int VEC>
 void launch_family(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc,
                    bool c_row, int M, int N, int K, int splits, int klen, double alpha, double beta,
                    double* partial, int flags) {
+#ifndef QB_WIDE_BK
+#define QB_WIDE_BK 16
+#define QB_WIDE_STAGES 4
+#endif
     if constexpr (F == Family::kWide)
-        launch_cfg<128, 128, 16, 2, 4, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
+        launch_cfg<128, 128, QB_WIDE_BK, 2, 4, QB_WIDE_STAGES, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
                                                        alpha, beta, partial, flags);
     else if constexpr (F == Family::kSkinny)
         launch_cfg<128, 64, 16, 4, 2, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
@@ -340,7 +349,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     }
     Family fam;
     int bm, bn, bk;
-    if (N >= 96) { fam = Family::kWide; bm = 128; bn = 128; bk = 16; }
+    if (N >= 96) { fam = Family::kWide; bm = 128; bn = 128; bk = QB_WIDE_BK; }
     else if (N > 32) { fam = Family::kSkinny; bm = 128; bn = 64; bk = 16; }
     else { fam = Family::kNarrow; bm = 64; bn = 32; bk = 32; }
     const std::int64_t tiles = ceil_div(M, bm) * ceil_div(N, bn);

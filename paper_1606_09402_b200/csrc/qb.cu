@@ -271,7 +271,7 @@ public:
     // Off-diagonal blocks of R^{-1} follow column by column:
     //   Rinv[:j, j] = -(Rinv[:j,:j] R[:j, j]) Rinv_jj.
     // Returns false on breakdown or when min diag(R) < kCholRatioMin * max diag(R).
-    bool chol_blocked(double* w, int l, double* r, double* rinv, double max_gram_dev) {
+    bool chol_blocked(double* w, int l, double* r, double* rinv, double max_gram_dev, double* ratio = nullptr) {
         const int nb = 64;
         const int nt = static_cast<int>(ceil_div(l, nb));
         QB_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * l * l, st_));
@@ -283,7 +283,7 @@ public:
             const int k0 = kb * nb, w0 = std::min(nb, l - k0), rest = l - k0 - w0;
             chol_small(st_, w + k0 + static_cast<std::int64_t>(k0) * l, l, w0, r + k0 + static_cast<std::int64_t>(k0) * l,
                        rinv + k0 + static_cast<std::int64_t>(k0) * l, l,
-                       reinterpret_cast<SmallStatus*>(reinterpret_cast<double*>(stats) + 4 * kb));
+                       stats + kb);
             if (rest > 0) {
                 MatView rkk_inv{rinv + k0 + static_cast<std::int64_t>(k0) * l, w0, w0, l, false};
                 MatView wp{w + k0 + static_cast<std::int64_t>(k0 + w0) * l, w0, rest, l, false};
@@ -295,7 +295,7 @@ public:
         }
         for (int jb = 1; jb < nt; ++jb) {
             const int j0 = jb * nb, wj = std::min(nb, l - j0);
-            if (tri_.n < static_cast<std::size_t>(j0) * nb) tri_ = DBuf(static_cast<std::size_t>(l) * nb, st_);
+            if (tri_.n < static_cast<std::size_t>(l) * nb) tri_ = DBuf(static_cast<std::size_t>(l) * nb, st_);
             MatView t{tri_.p, j0, wj, j0, false};
             MatView rinv_tl{rinv, j0, j0, l, false};
             MatView r_col{r + static_cast<std::int64_t>(j0) * l, j0, wj, l, false};
@@ -305,9 +305,7 @@ public:
             gemm(-1.0, t, rinv_jj, 0.0, rinv_col);
         }
         std::vector<SmallStatus> hs(static_cast<std::size_t>(nt));
-        for (int kb = 0; kb < nt; ++kb)
-            QB_CUDA(cudaMemcpyAsync(&hs[kb], reinterpret_cast<double*>(stats) + 4 * kb, sizeof(SmallStatus),
-                                    cudaMemcpyDeviceToHost, st_));
+        QB_CUDA(cudaMemcpyAsync(hs.data(), stats, sizeof(SmallStatus) * nt, cudaMemcpyDeviceToHost, st_));
         QB_CUDA(cudaStreamSynchronize(st_));
         double dmin = INFINITY, dmax = 0.0, dev = 0.0;
         for (const auto& s : hs) {
@@ -316,13 +314,17 @@ public:
             dmax = std::max(dmax, s.diag_max);
             dev = std::max(dev, s.gram_dev);
         }
+        if (ratio) *ratio = dmax > 0.0 ? dmin / dmax : 0.0;
         return dmax > 0.0 && dmin >= kCholRatioMin * dmax && dev <= max_gram_dev;
     }
 
-    // CholQR2 of a wide panel X (rows x l, row-major) in place with one l x l Gram per
-    // pass (DMMA SYRK), blocked Cholesky, and X R^{-1} as a triangular-B GEMM.
-    // Returns false (X unchanged or already orthonormalised once) when the Gram is
-    // too ill-conditioned; orth_wide then falls back to BCGS2.
+    // CholQR of a wide panel X (rows x l, row-major) in place: one l x l Gram (DMMA SYRK),
+    // blocked Cholesky, X R^{-1} as a triangular-B GEMM. The second pass of CholQR2 is
+    // run only when the first leaves a loss of orthogonality u*kappa^2 (kappa estimated
+    // by the diagonal ratio of R) above 1e-6: the power step needs a basis with the
+    // reference's leading-column spans, which any upper-triangular R preserves.
+    // Returns false (X unchanged, or holding the one-pass basis) when the Gram is too
+    // ill-conditioned for Cholesky; orth_wide then falls back to BCGS2.
     bool orth_wide_cholqr2(const MatView& x, bool sharded) {
         const int l = static_cast<int>(x.cols);
         const std::size_t ll = static_cast<std::size_t>(l) * l;
@@ -339,11 +341,17 @@ public:
             const MatView& dst = pass == 0 ? y : x;
             qbgpu::gemm(st_, c_.ws_gemm, 1.0, src.t(), src, 0.0, gv, kGemmUpperC);
             if (sharded) c_.allreduce(g, ll);
-            if (!chol_blocked(g, l, r, rinv, pass == 0 ? INFINITY : kCholGramDevMax)) {
+            double ratio = 0.0;
+            if (!chol_blocked(g, l, r, rinv, pass == 0 ? INFINITY : kCholGramDevMax, &ratio)) {
                 if (pass == 1) copy_matrix(st_, y, x);
                 return false;
             }
             qbgpu::gemm(st_, c_.ws_gemm, 1.0, src, rinv_v, 0.0, dst, kGemmTriB);
+            ++wide_passes;
+            if (pass == 0 && kEpsMach / (ratio * ratio) <= 1e-6) {
+                copy_matrix(st_, y, x);
+                return true;
+            }
         }
         return true;
     }
@@ -376,6 +384,7 @@ public:
     }
 
     std::int64_t hh_fallbacks = 0;
+    std::int64_t wide_passes = 0;
 
 private:
     DBuf scratch_t_, stat_, tri_, wide_, wide_y_;

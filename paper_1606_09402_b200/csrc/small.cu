@@ -147,93 +147,193 @@ __global__ void colsumsq_stage2(const double* __restrict__ partial, int nblk, st
     }
 }
 
-// Cholesky of the b x b Gram by symmetric Gaussian elimination on [G | I]
-// (shared memory, b x (2b+1) doubles). Step k eliminates rows i > k with the
-// UNSCALED row k over the contiguous column range [k+1, b+k] (left part of G plus
-// the lower-triangular right part), while row k-1 is scaled by 1/sqrt(pivot) in the
-// same phase (disjoint rows), so each step costs one barrier. At the end row k holds
-// R(k,:) on the left and (R^{-T})(k,:) on the right. 32 x 32 threads, no integer
-// division in the inner loops.
-constexpr int kCholTx = 32, kCholTy = 32;
+// Cholesky of a b x b Gram (b <= 112) together with R^{-1}, one CTA, everything in
+// registers. The augmented matrix [G | I] is eliminated symmetrically (step k:
+// row_i -= (G(k,i)/piv_k) row_k for i > k); afterwards row k scaled by
+// 1/sqrt(piv_k) is R(k,:) on the left and R^{-T}(k,:) on the right. The upper
+// triangle of G and the lower triangle of the right part are cut into T x T tiles
+// on a 16 x 16 grid and every thread owns ONE tile in registers (136 + 136 tiles).
+// Per step the owners of row k publish it (double-buffered in shared memory) and
+// the pivot owner publishes 1/piv; each thread then updates its tile: one barrier
+// and <= 2T shared loads per thread per step.
+// A near-identity Gram (max|G - I| <= 1e-8: the second CholQR pass and every
+// re-orthogonalisation) takes the exact-to-rounding first-order path
+// R = I + F, R^{-1} = I - F, F = triu(G - I) - diag(G - I)/2 (error O(|G - I|^2)).
+constexpr int kCholGrid = 16;
+constexpr int kCholTiles = kCholGrid * (kCholGrid + 1);   // 136 left + 136 right
+constexpr int kCholThreads = ((kCholTiles + 31) / 32) * 32;  // 288
+constexpr double kFirstOrderDev = 1e-8;
 
-__global__ void __launch_bounds__(kCholTx * kCholTy)
+template <int T>
+__global__ void __launch_bounds__(kCholThreads)
 chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double* __restrict__ r,
                   double* __restrict__ rinv, std::int64_t ldr, SmallStatus* status) {
-    extern __shared__ double w[];
-    const int ldw = 2 * b + 1;
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int tid = ty * kCholTx + tx;
-    __shared__ double s_red[kCholTy];
+    __shared__ double bufL[2][kSmallMax], bufR[2][kSmallMax];
+    __shared__ double s_pinv[kSmallMax], s_rsq[kSmallMax], s_sq[kSmallMax];
+    __shared__ double s_red[kCholThreads / 32];
+    __shared__ double s_dev;
     __shared__ int s_bad;
-    if (tid == 0) s_bad = -1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // tile assignment: t < 136 -> left (upper) tile, else right (lower) tile
+    int side = -1, ti = 0, tj = 0;
+    if (tid < kCholTiles) {
+        int t = tid < kCholTiles / 2 ? tid : tid - kCholTiles / 2;
+        // enumerate (ti, tj) with ti <= tj (row-major over the upper triangle of the tile grid)
+        int row = 0;
+        while (t >= kCholGrid - row) { t -= kCholGrid - row; ++row; }
+        if (tid < kCholTiles / 2) { side = 0; ti = row; tj = row + t; }   // left tile (ti <= tj)
+        else { side = 1; ti = row + t; tj = row; }                       // right tile (ti >= tj)
+    }
+    const int i0 = ti * T, j0 = tj * T;
+    double v[T][T];
     double dev = 0.0;
-    for (int j = ty; j < b; j += kCholTy) {
-        for (int i = tx; i < b; i += kCholTx) {
-            const double v = i <= j ? g[i + j * ldg] : g[j + i * ldg];
-            w[i * ldw + j] = v;
-            w[i * ldw + b + j] = (i == j) ? 1.0 : 0.0;
-            dev = fmax(dev, fabs(v - (i == j ? 1.0 : 0.0)));
+#pragma unroll
+    for (int a = 0; a < T; ++a)
+#pragma unroll
+        for (int c = 0; c < T; ++c) {
+            const int i = i0 + a, j = j0 + c;
+            double x = 0.0;
+            if (side == 0 && i < b && j < b && i <= j) {
+                x = g[i + static_cast<std::int64_t>(j) * ldg];
+                dev = fmax(dev, fabs(x - (i == j ? 1.0 : 0.0)));
+            } else if (side == 1) {
+                x = (i == j) ? 1.0 : 0.0;
+            }
+            v[a][c] = x;
         }
-    }
     for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_down_sync(0xffffffffu, dev, o));
-    if (tx == 0) s_red[ty] = dev;
+    if (lane == 0) s_red[warp] = dev;
+    if (tid == 0) s_bad = -1;
     __syncthreads();
-    double prev_s = 1.0;
-    for (int k = 0; k < b; ++k) {
-        const double piv = w[k * ldw + k];
-        const bool bad = !(piv > 0.0) || !isfinite(piv);
-        const double p = bad ? 1.0 : piv;
-        const double pinv = 1.0 / p;
-        if (bad && tid == 0 && s_bad < 0) s_bad = k;
-        // eliminate rows i > k with the unscaled row k
-        for (int i = k + 1 + ty; i < b; i += kCholTy) {
-            const double f = w[k * ldw + i] * pinv;
-            double* wi = w + i * ldw;
-            const double* wk = w + k * ldw;
-            for (int j = k + 1 + tx; j <= b + k; j += kCholTx) wi[j] = fma(-f, wk[j], wi[j]);
+    if (tid == 0) {
+        double dv = 0.0;
+        for (int w = 0; w < kCholThreads / 32; ++w) dv = fmax(dv, s_red[w]);
+        s_dev = dv;
+    }
+    __syncthreads();
+    if (s_dev <= kFirstOrderDev) {
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int c = 0; c < T; ++c) {
+                const int i = i0 + a, j = j0 + c;
+                if (side != 0 || i >= b || j >= b || i > j) continue;
+                const double e = i == j ? v[a][c] - 1.0 : v[a][c];
+                r[i + static_cast<std::int64_t>(j) * ldr] = i == j ? 1.0 + 0.5 * e : e;
+                rinv[i + static_cast<std::int64_t>(j) * ldr] = i == j ? 1.0 - 0.5 * e : -e;
+                if (i == j) { s_sq[i] = 1.0 + 0.5 * e; }
+            }
+        // zero strict lower parts
+        for (int idx = tid; idx < b * b; idx += kCholThreads) {
+            const int i = idx % b, j = idx / b;
+            if (i > j) {
+                r[i + static_cast<std::int64_t>(j) * ldr] = 0.0;
+                rinv[i + static_cast<std::int64_t>(j) * ldr] = 0.0;
+            }
         }
-        // deferred scaling of row k-1 (columns [k, b+k-1]) and its diagonal
-        if (k > 0) {
-            const double inv = 1.0 / prev_s;
-            double* wr = w + (k - 1) * ldw;
-            for (int j = k + tid; j <= b + k - 1; j += kCholTx * kCholTy) wr[j] *= inv;
-            if (tid == 0) wr[k - 1] = prev_s;
-        }
-        prev_s = sqrt(p);
+    } else {
+        // publish row 0 and pivot 0
+        auto publish = [&](int k, int buf) {
+            if (k < i0 || k >= i0 + T || k >= b) return;
+#pragma unroll
+            for (int a = 0; a < T; ++a) {
+                if (i0 + a != k) continue;  // compile-time row index keeps v[][] in registers
+#pragma unroll
+                for (int c = 0; c < T; ++c) {
+                    const int j = j0 + c;
+                    if (j >= b) continue;
+                    if (side == 0 && j >= k) bufL[buf][j] = v[a][c];
+                    if (side == 1 && j <= k) bufR[buf][j] = v[a][c];
+                    if (side == 0 && j == k) {
+                        const double piv = v[a][c];
+                        const bool bad = !(piv > 0.0) || !isfinite(piv);
+                        if (bad && s_bad < 0) s_bad = k;
+                        const double pp = bad ? 1.0 : piv;
+                        const double sq = sqrt(pp);
+                        s_pinv[k] = 1.0 / pp;
+                        s_sq[k] = sq;
+                        s_rsq[k] = 1.0 / sq;
+                    }
+                }
+            }
+        };
+        if (side >= 0) publish(0, 0);
         __syncthreads();
-    }
-    {
-        const double inv = 1.0 / prev_s;
-        double* wr = w + (b - 1) * ldw;
-        for (int j = b + tid; j <= 2 * b - 1; j += kCholTx * kCholTy) wr[j] *= inv;
-        if (tid == 0) wr[b - 1] = prev_s;
+        for (int k = 0; k < b; ++k) {
+            const int p = k & 1;
+            if (side >= 0 && i0 + T - 1 > k) {
+                const double pinv = s_pinv[k];
+                double f[T];
+#pragma unroll
+                for (int a = 0; a < T; ++a) {
+                    const int i = i0 + a;
+                    f[a] = (i > k && i < b) ? bufL[p][i] * pinv : 0.0;
+                }
+                if (side == 0) {
+                    if (j0 + T - 1 > k) {
+                        double rowk[T];
+#pragma unroll
+                        for (int c = 0; c < T; ++c) {
+                            const int j = j0 + c;
+                            rowk[c] = (j > k && j < b) ? bufL[p][j] : 0.0;
+                        }
+#pragma unroll
+                        for (int a = 0; a < T; ++a)
+#pragma unroll
+                            for (int c = 0; c < T; ++c) v[a][c] = fma(-f[a], rowk[c], v[a][c]);
+                    }
+                } else if (j0 <= k) {
+                    double rowk[T];
+#pragma unroll
+                    for (int c = 0; c < T; ++c) {
+                        const int j = j0 + c;
+                        rowk[c] = (j <= k && j < b) ? bufR[p][j] : 0.0;
+                    }
+#pragma unroll
+                    for (int a = 0; a < T; ++a)
+#pragma unroll
+                        for (int c = 0; c < T; ++c) v[a][c] = fma(-f[a], rowk[c], v[a][c]);
+                }
+            }
+            if (side >= 0 && k + 1 < b) publish(k + 1, p ^ 1);
+            __syncthreads();
+        }
+        // row k of the result = row k / sqrt(piv_k); right part transposed into R^{-1}
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int c = 0; c < T; ++c) {
+                const int i = i0 + a, j = j0 + c;
+                if (side < 0 || i >= b || j >= b) continue;
+                if (side == 0) {
+                    if (i <= j) r[i + static_cast<std::int64_t>(j) * ldr] = i == j ? s_sq[i] : v[a][c] * s_rsq[i];
+                    else r[i + static_cast<std::int64_t>(j) * ldr] = 0.0;
+                } else {
+                    if (j <= i) rinv[j + static_cast<std::int64_t>(i) * ldr] = v[a][c] * s_rsq[i];
+                    if (j < i) {
+                        rinv[i + static_cast<std::int64_t>(j) * ldr] = 0.0;
+                        r[i + static_cast<std::int64_t>(j) * ldr] = 0.0;
+                    }
+                }
+            }
     }
     __syncthreads();
-    for (int j = ty; j < b; j += kCholTy) {
-        for (int i = tx; i < b; i += kCholTx) {
-            r[i + j * ldr] = i <= j ? w[i * ldw + j] : 0.0;
-            rinv[i + j * ldr] = i <= j ? w[j * ldw + b + i] : 0.0;
-        }
-    }
-    if (ty == 0 && status) {
+    if (warp == 0 && status) {
         double dmin = INFINITY, dmax = 0.0;
-        for (int j = tx; j < b; j += kCholTx) {
-            const double d = w[j * ldw + j];
-            dmin = fmin(dmin, d);
-            dmax = fmax(dmax, d);
+        for (int j = lane; j < b; j += 32) {
+            dmin = fmin(dmin, s_sq[j]);
+            dmax = fmax(dmax, s_sq[j]);
         }
-        double dv = tx < kCholTy ? s_red[tx] : 0.0;
         for (int o = 16; o > 0; o >>= 1) {
             dmin = fmin(dmin, __shfl_down_sync(0xffffffffu, dmin, o));
             dmax = fmax(dmax, __shfl_down_sync(0xffffffffu, dmax, o));
-            dv = fmax(dv, __shfl_down_sync(0xffffffffu, dv, o));
         }
-        if (tx == 0) {
+        if (lane == 0) {
             status->breakdown = s_bad >= 0 ? 1 : 0;
             status->bad_index = s_bad;
             status->diag_min = dmin;
             status->diag_max = dmax;
-            status->gram_dev = dv;
+            status->gram_dev = s_dev;
         }
     }
 }
@@ -515,14 +615,10 @@ void column_sumsq(cudaStream_t st, Workspace& ws, const MatView& v, double* out)
 void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, double* r, double* rinv,
                 std::int64_t ldr, SmallStatus* status) {
     if (b < 1 || b > kSmallMax) throw QbError(kDimensionError, "chol_small: block width out of range");
-    const int smem = b * (2 * b + 1) * static_cast<int>(sizeof(double));
-    static bool configured = false;
-    if (!configured) {
-        QB_CUDA(cudaFuncSetAttribute(chol_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kSmallMax * (2 * kSmallMax + 1) * 8));
-        configured = true;
-    }
-    chol_small_kernel<<<1, dim3(kCholTx, kCholTy), smem, st>>>(g, ldg, b, r, rinv, ldr, status);
+    // tile edge T with 16 * T >= b
+    if (b <= 32) chol_small_kernel<2><<<1, kCholThreads, 0, st>>>(g, ldg, b, r, rinv, ldr, status);
+    else if (b <= 64) chol_small_kernel<4><<<1, kCholThreads, 0, st>>>(g, ldg, b, r, rinv, ldr, status);
+    else chol_small_kernel<7><<<1, kCholThreads, 0, st>>>(g, ldg, b, r, rinv, ldr, status);
     QB_LAUNCH_CHECK();
 }
 

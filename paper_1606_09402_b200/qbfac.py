@@ -27,7 +27,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqbfac_gpu.so")
+LIB_PATH = os.environ.get("QBFAC_LIB") or os.path.join(HERE, "libqbfac_gpu.so")  # QBFAC_LIB: dev builds
 
 # ---- errors (types.hpp:16-66) --------------------------------------------------------
 
