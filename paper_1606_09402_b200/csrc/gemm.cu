@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #ifndef QB_WIDE_BK
 #define QB_WIDE_BK 32
@@ -253,6 +254,39 @@ splitk_reduce_kernel(const double* __restrict__ partial, int splits, int M, int 
     }
 }
 
+#include "gemm_ws.cuh"
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int NP>
+void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc, bool c_row, int M,
+               int N, int K, int splits, int klen, double alpha, double beta, double* partial, int flags) {
+    using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
+    auto kern = dgemm_ws_kernel<BM, BN, BK, WM, WN, STAGES, AR, BR, NP>;
+    constexpr int smem = T::SMEM_BYTES + 2 * STAGES * 8;
+    static int per_sm = 0;
+    if (!per_sm) {
+        QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (WM * WN + NP) * 32, smem));
+        if (per_sm < 1) per_sm = 1;
+    }
+    WsArgs p{a.p, a.ld, b.p, b.ld, c, ldc, c_row ? 1 : 0, M, N, K, klen, splits,
+             static_cast<int>(ceil_div(M, BM)), static_cast<int>(ceil_div(N, BN)), flags, alpha, beta, partial};
+    const std::int64_t items = static_cast<std::int64_t>(p.tiles_m) * p.tiles_n * splits;
+    const int grid = static_cast<int>(std::min<std::int64_t>(items, static_cast<std::int64_t>(per_sm) * gemm_num_sms()));
+    kern<<<grid, (WM * WN + NP) * 32, smem, st>>>(p);
+    QB_LAUNCH_CHECK();
+}
+
+template <bool AR, bool BR>
+bool dispatch_ws(int fam, cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc, bool c_row,
+                 int M, int N, int K, int splits, int klen, double alpha, double beta, double* partial, int flags) {
+    // one producer warp when both operands move by bulk TMA, two when cp.async chunks are involved
+    constexpr int NP = (!AR && BR) ? 1 : 2;
+    if (fam == 0) launch_ws<128, 128, 32, 2, 4, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
+    else if (fam == 1) launch_ws<128, 64, 32, 4, 2, 4, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
+    else launch_ws<64, 32, 32, 2, 2, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
+    return true;
+}
+
 struct Launch {
     int bm, bn, bk;
     int threads;
@@ -352,6 +386,15 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     if (N >= 96) { fam = Family::kWide; bm = 128; bn = 128; bk = QB_WIDE_BK; }
     else if (N > 32) { fam = Family::kSkinny; bm = 128; bn = 64; bk = 16; }
     else { fam = Family::kNarrow; bm = 64; bn = 32; bk = 32; }
+    const bool vec2 = aligned16(a) && aligned16(b);
+    static const bool use_ws = [] {
+        const char* e = std::getenv("QBFAC_GEMM_LEGACY");
+        return !(e && e[0] == '1');
+    }();
+    // Warp-specialised TMA path where it measured faster (tools/gemm_bench.py): A column-major
+    // (long bulk segments), or both operands row-major with wide tiles (A^T G passes).
+    const bool ws_path = use_ws && vec2 && (!a.rowmajor || (b.rowmajor && N >= 96));
+    if (ws_path) bk = 32;  // the warp-specialised kernels use BK = 32 in every family
     const std::int64_t tiles = ceil_div(M, bm) * ceil_div(N, bn);
     const int sms = gemm_num_sms();
     // Resident CTAs per SM ~1 for the wide/skinny tiles, ~3 for narrow.
@@ -366,7 +409,19 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     splits = static_cast<int>(ceil_div(K, klen));
     double* partial = nullptr;
     if (splits > 1) partial = ws.get(static_cast<std::size_t>(splits) * M * N);
-    const bool vec2 = aligned16(a) && aligned16(b);
+    if (ws_path) {
+        // warp-specialised TMA/mbarrier pipeline (gemm_ws.cuh)
+        const int famid = fam == Family::kWide ? 0 : (fam == Family::kSkinny ? 1 : 2);
+        {
+            if (a.rowmajor) {
+                if (b.rowmajor) dispatch_ws<true, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);
+                else dispatch_ws<true, false>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);
+            } else {
+                if (b.rowmajor) dispatch_ws<false, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);
+                else dispatch_ws<false, false>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);
+            }
+        }
+    } else {
     switch (fam) {
         case Family::kWide:
             dispatch_layout<Family::kWide>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits,
@@ -379,6 +434,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
         default:
             dispatch_layout<Family::kNarrow>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K,
                                              splits, klen, alpha, beta, partial, vec2, flags);
+    }
     }
     if (splits > 1) {
         const std::int64_t total = M * N;
