@@ -6,6 +6,7 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/qbfac_gpu.h"
 #include "qb.cuh"
@@ -361,8 +362,14 @@ int qbfac_gpu_test_csr_spmm(qbfac_gpu_ctx* ctx, int64_t rows, int64_t cols, int6
                             int w, double alpha, double beta) {
     return guard(ctx, [&] {
         auto& cx = *ctx->c;
-        qbgpu::CsrView a{rows, cols, nnz, rp, ci, v};
-        qbgpu::csr_spmm(cx.st, a, x, ldx, y, ldy, w, alpha, beta, cx.sms);
+        qbgpu::CsrView a{rows, cols, nnz, rp, ci, v, {}};
+        std::vector<int64_t> rph(static_cast<size_t>(rows + 1));
+        QB_CUDA(cudaMemcpy(rph.data(), rp, sizeof(int64_t) * (rows + 1), cudaMemcpyDeviceToHost));
+        a.heavy = qbgpu::make_heavy_plan(rph.data(), rows, cx.st);
+        double* part = a.heavy.nseg ? cx.ws_sp.get(qbgpu::csr_spmm_scratch(a, std::min(w, 256))) : nullptr;
+        qbgpu::csr_spmm(cx.st, a, x, ldx, y, ldy, w, alpha, beta, cx.sms, part);
+        QB_CUDA(cudaStreamSynchronize(cx.st));
+        qbgpu::free_heavy_plan(a.heavy);
         QB_CUDA(cudaStreamSynchronize(cx.st));
     });
 }

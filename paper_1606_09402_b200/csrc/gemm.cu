@@ -283,6 +283,7 @@ bool dispatch_ws(int fam, cudaStream_t st, const MatView& a, const MatView& b, d
     constexpr int NP = (!AR && BR) ? 1 : 2;
     if (fam == 0) launch_ws<128, 128, 32, 2, 4, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
     else if (fam == 1) launch_ws<128, 64, 32, 4, 2, 4, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
+    else if (fam == 3) launch_ws<128, 56, 32, 8, 1, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
     else launch_ws<64, 32, 32, 2, 2, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
     return true;
 }
@@ -314,7 +315,7 @@ void launch_cfg(cudaStream_t st, const MatView& a, const MatView& b, double* c, 
 // Tile families. "wide": 128x128 CTA tiles (warp 64x32) for the passes over A at
 // large widths; "skinny": 128x64 (warp 32x32) for widths ~50-100; "narrow":
 // 64x32 for the thinnest products (b = 20, Gram-like outputs).
-enum class Family { kWide, kSkinny, kNarrow };
+enum class Family { kWide, kSkinny, kNarrow, kSkinny56 };
 
 template <Family F, bool AR, bool BR, int VEC>
 void launch_family(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc,
@@ -329,6 +330,9 @@ void launch_family(cudaStream_t st, const MatView& a, const MatView& b, double* 
                                                        alpha, beta, partial, flags);
     else if constexpr (F == Family::kSkinny)
         launch_cfg<128, 64, 16, 4, 2, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
+                                                      alpha, beta, partial, flags);
+    else if constexpr (F == Family::kSkinny56)  // b = 50-56: 7 n8 tiles per warp, no 64-column padding
+        launch_cfg<128, 56, 16, 8, 1, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
                                                       alpha, beta, partial, flags);
     else
         launch_cfg<64, 32, 32, 2, 2, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
@@ -384,6 +388,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     Family fam;
     int bm, bn, bk;
     if (N >= 96) { fam = Family::kWide; bm = 128; bn = 128; bk = QB_WIDE_BK; }
+    else if (N > 48 && N <= 56) { fam = Family::kSkinny56; bm = 128; bn = 56; bk = 16; }
     else if (N > 32) { fam = Family::kSkinny; bm = 128; bn = 64; bk = 16; }
     else { fam = Family::kNarrow; bm = 64; bn = 32; bk = 32; }
     const bool vec2 = aligned16(a) && aligned16(b);
@@ -395,6 +400,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     // (long bulk segments), or both operands row-major with wide tiles (A^T G passes).
     const bool ws_path = use_ws && vec2 && (!a.rowmajor || (b.rowmajor && N >= 96));
     if (ws_path) bk = 32;  // the warp-specialised kernels use BK = 32 in every family
+    if (ws_path && fam == Family::kSkinny56) bn = 64;
     const std::int64_t tiles = ceil_div(M, bm) * ceil_div(N, bn);
     const int sms = gemm_num_sms();
     // Resident CTAs per SM ~1 for the wide/skinny tiles, ~3 for narrow.
@@ -411,7 +417,8 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     if (splits > 1) partial = ws.get(static_cast<std::size_t>(splits) * M * N);
     if (ws_path) {
         // warp-specialised TMA/mbarrier pipeline (gemm_ws.cuh)
-        const int famid = fam == Family::kWide ? 0 : (fam == Family::kSkinny ? 1 : 2);
+        // the 56-wide tile measured slower than 64 on the TMA path (tools/gemm_bench.py): use 64 there
+        const int famid = fam == Family::kWide ? 0 : (fam == Family::kSkinny || fam == Family::kSkinny56) ? 1 : 2;
         {
             if (a.rowmajor) {
                 if (b.rowmajor) dispatch_ws<true, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);
@@ -430,6 +437,10 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
         case Family::kSkinny:
             dispatch_layout<Family::kSkinny>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K,
                                              splits, klen, alpha, beta, partial, vec2, flags);
+            break;
+        case Family::kSkinny56:
+            dispatch_layout<Family::kSkinny56>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K,
+                                               splits, klen, alpha, beta, partial, vec2, flags);
             break;
         default:
             dispatch_layout<Family::kNarrow>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K,

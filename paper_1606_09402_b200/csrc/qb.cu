@@ -73,6 +73,7 @@ Context::~Context() {
     ws_gemm.release();
     ws_red.release();
     ws_hh.release();
+    ws_sp.release();
     if (d_small) cudaFree(d_small);
     if (d_status) cudaFree(d_status);
     if (d_ind) cudaFree(d_ind);
@@ -92,6 +93,8 @@ Matrix::~Matrix() {
     if (ct_rp) cudaFree(ct_rp);
     if (ct_ci) cudaFree(ct_ci);
     if (ct_v) cudaFree(ct_v);
+    free_heavy_plan(heavy);
+    free_heavy_plan(heavy_t);
 }
 
 std::unique_ptr<Matrix> make_dense(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
@@ -149,7 +152,11 @@ std::unique_ptr<Matrix> make_csr(Context& c, std::int64_t m_global, std::int64_t
     if (flags & 1) throw QbError(kFormatError, "csr: invalid structure (row_ptr / column indices)");
     if (flags & 2) throw QbError(kError, "csr: non-finite value");
     csr_transpose(c.st, m, n, nnz, mat->rp, mat->ci, mat->v, mat->ct_rp, mat->ct_ci, mat->ct_v, c.sms);
+    mat->heavy = make_heavy_plan(rp, m, c.st);
+    std::vector<std::int64_t> ct_rp_host(static_cast<std::size_t>(n + 1));
+    QB_CUDA(cudaMemcpyAsync(ct_rp_host.data(), mat->ct_rp, sizeof(std::int64_t) * (n + 1), cudaMemcpyDeviceToHost, c.st));
     QB_CUDA(cudaStreamSynchronize(c.st));
+    mat->heavy_t = make_heavy_plan(ct_rp_host.data(), n, c.st);
     return mat;
 }
 
@@ -171,7 +178,9 @@ public:
     void apply(const MatView& x, const MatView& y, double alpha = 1.0, double beta = 0.0) {
         if (a_.sparse) {
             if (!x.rowmajor || !y.rowmajor) throw QbError(kInternal, "sparse pass needs row-major blocks");
-            csr_spmm(st_, a_.csr(), x.p, x.ld, y.p, y.ld, static_cast<int>(x.cols), alpha, beta, c_.sms);
+            const CsrView av = a_.csr();
+            double* part = av.heavy.nseg ? c_.ws_sp.get(csr_spmm_scratch(av, std::min<int>(static_cast<int>(x.cols), 256))) : nullptr;
+            csr_spmm(st_, av, x.p, x.ld, y.p, y.ld, static_cast<int>(x.cols), alpha, beta, c_.sms, part);
         } else {
             gemm(alpha, a_.dense_view(), x, beta, y);
         }
@@ -190,7 +199,9 @@ public:
         }
         if (a_.sparse) {
             if (!x.rowmajor || !y.rowmajor) throw QbError(kInternal, "sparse pass needs row-major blocks");
-            csr_spmm(st_, a_.csr_t(), x.p, x.ld, y.p, y.ld, static_cast<int>(x.cols), 1.0, 0.0, c_.sms);
+            const CsrView av = a_.csr_t();
+            double* part = av.heavy.nseg ? c_.ws_sp.get(csr_spmm_scratch(av, std::min<int>(static_cast<int>(x.cols), 256))) : nullptr;
+            csr_spmm(st_, av, x.p, x.ld, y.p, y.ld, static_cast<int>(x.cols), 1.0, 0.0, c_.sms, part);
         } else {
             gemm(1.0, a_.dense_view().t(), x, 0.0, y);
         }

@@ -46,7 +46,7 @@ struct Context {
     int device = 0;
     cudaStream_t st = nullptr;
     int sms = 148;
-    Workspace ws_gemm, ws_red, ws_hh;
+    Workspace ws_gemm, ws_red, ws_hh, ws_sp;
     RngTables rng;
     std::unique_ptr<Comm> comm;
     int rank = 0, world = 1;
@@ -85,11 +85,12 @@ struct Matrix {
     std::int64_t* ct_rp = nullptr;
     std::int32_t* ct_ci = nullptr;
     double* ct_v = nullptr;
+    HeavyPlan heavy, heavy_t;  // heavy-row segment plans of the CSR and its transpose
 
     ~Matrix();
     MatView dense_view() const { return MatView{a, m, n, lda, false}; }
-    CsrView csr() const { return CsrView{m, n, nnz, rp, ci, v}; }
-    CsrView csr_t() const { return CsrView{n, m, nnz, ct_rp, ct_ci, ct_v}; }
+    CsrView csr() const { return CsrView{m, n, nnz, rp, ci, v, heavy}; }
+    CsrView csr_t() const { return CsrView{n, m, nnz, ct_rp, ct_ci, ct_v, heavy_t}; }
 };
 
 std::unique_ptr<Matrix> make_dense(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,

@@ -149,19 +149,44 @@ struct GenArgs {
     MatView out;
 };
 
+// The jump matrices T^(64 * 2^j), j < 8, used by the in-CTA doubling scan are staged
+// in shared memory (64 KB); the CTA anchor jumps from the call's base state (computed
+// on the host) by blockIdx * 2^14 u64 steps, i.e. only the bits of blockIdx.
+constexpr int kScanLevels = 8;  // 2^8 = kGenThreads
+constexpr int kGenSmem = kScanLevels * 1024 * 8 + kGenThreads * 4 * 8;
+
+__device__ __forceinline__ void smem_matvec(const std::uint64_t* m, const std::uint64_t* x, std::uint64_t* y) {
+    std::uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        std::uint64_t bits = x[w];
+        while (bits) {
+            const int b = __ffsll(static_cast<long long>(bits)) - 1;
+            bits &= bits - 1;
+            const std::uint64_t* col = m + (w * 64 + b) * 4;
+            r0 ^= col[0]; r1 ^= col[1]; r2 ^= col[2]; r3 ^= col[3];
+        }
+    }
+    y[0] = r0; y[1] = r1; y[2] = r2; y[3] = r3;
+}
+
 __global__ void __launch_bounds__(kGenThreads)
 gaussian_kernel(GenArgs a, const std::uint64_t* __restrict__ tables) {
-    __shared__ std::uint64_t st[kGenThreads][4];
+    extern __shared__ std::uint64_t gsm[];
+    std::uint64_t* stab = gsm;                              // kScanLevels x 1024 words
+    std::uint64_t (*st)[4] = reinterpret_cast<std::uint64_t (*)[4]>(gsm + kScanLevels * 1024);
     const std::uint64_t p_first = a.g0 >> 1;
     const std::uint64_t g_end = a.g0 + static_cast<std::uint64_t>(a.count);  // exclusive
     const std::uint64_t cta_pair0 = p_first + static_cast<std::uint64_t>(blockIdx.x) * kGenThreads * kPairsPerThread;
-    // CTA anchor: T^(2*cta_pair0) s0, by warp 0.
+    for (int i = threadIdx.x; i < kScanLevels * 1024; i += kGenThreads)
+        stab[i] = __ldg(tables + static_cast<std::size_t>(kThreadJumpLevel0) * 1024 + i);
+    // CTA anchor: T^(2 * 8192 * blockIdx) * base, by warp 0 (levels 14 + bit of blockIdx).
     if (threadIdx.x < 32) {
         std::uint64_t x[4] = {a.s0[0], a.s0[1], a.s0[2], a.s0[3]};
-        std::uint64_t e = 2 * cta_pair0;
-        int k = 0;
+        unsigned e = blockIdx.x;
+        int k = kThreadJumpLevel0 + kScanLevels;
         while (e) {
-            if (e & 1ULL) {
+            if (e & 1u) {
                 std::uint64_t y[4];
                 warp_matvec(tables + static_cast<std::size_t>(k) * 1024, x, y);
                 x[0] = y[0]; x[1] = y[1]; x[2] = y[2]; x[3] = y[3];
@@ -174,10 +199,9 @@ gaussian_kernel(GenArgs a, const std::uint64_t* __restrict__ tables) {
     __syncthreads();
     // Doubling scan: st[t] = T^(64 t) st[0].
 #pragma unroll 1
-    for (int j = 0; (1 << j) < kGenThreads; ++j) {
+    for (int j = 0; j < kScanLevels; ++j) {
         const int t = threadIdx.x;
-        if (t >= (1 << j) && t < (2 << j))
-            thread_matvec(tables + static_cast<std::size_t>(kThreadJumpLevel0 + j) * 1024, st[t - (1 << j)], st[t]);
+        if (t >= (1 << j) && t < (2 << j)) smem_matvec(stab + j * 1024, st[t - (1 << j)], st[t]);
         __syncthreads();
     }
     std::uint64_t s[4] = {st[threadIdx.x][0], st[threadIdx.x][1], st[threadIdx.x][2], st[threadIdx.x][3]};
@@ -237,6 +261,22 @@ void gaussian_fill(cudaStream_t st, RngTables& tables, std::uint64_t seed, std::
     if (count == 0) return;
     GenArgs a{};
     stream_origin(seed, stream, a.s0);
+    {
+        // base state of this call: T^(2 * p_first) s0, jumped on the host
+        const auto& tab = jump_tables_host();
+        std::uint64_t e = 2 * (g0 >> 1);
+        int k = 0;
+        while (e) {
+            if (e & 1ULL) {
+                std::uint64_t y[4];
+                Mat256 m(tab.begin() + static_cast<std::size_t>(k) * 1024, tab.begin() + static_cast<std::size_t>(k + 1) * 1024);
+                matvec_host(m, a.s0, y);
+                std::memcpy(a.s0, y, sizeof(y));
+            }
+            e >>= 1;
+            ++k;
+        }
+    }
     a.g0 = g0;
     a.count = count;
     a.rows = out.rows;
@@ -246,7 +286,12 @@ void gaussian_fill(cudaStream_t st, RngTables& tables, std::uint64_t seed, std::
     const std::uint64_t pairs = p_last - p_first + 1;
     const std::uint64_t per_cta = static_cast<std::uint64_t>(kGenThreads) * kPairsPerThread;
     const unsigned grid = static_cast<unsigned>((pairs + per_cta - 1) / per_cta);
-    gaussian_kernel<<<grid, kGenThreads, 0, st>>>(a, tables.device());
+    static bool configured = false;
+    if (!configured) {
+        QB_CUDA(cudaFuncSetAttribute(gaussian_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGenSmem));
+        configured = true;
+    }
+    gaussian_kernel<<<grid, kGenThreads, kGenSmem, st>>>(a, tables.device());
     QB_LAUNCH_CHECK();
 }
 

@@ -137,14 +137,17 @@ __global__ void colsumsq_stage1(MatView v, std::int64_t chunk, double* __restric
     }
 }
 
+// One warp per column: lanes take partials lane, lane+32, ... in order, then a fixed
+// shuffle tree (deterministic).
 __global__ void colsumsq_stage2(const double* __restrict__ partial, int nblk, std::int64_t cols,
                                 double* __restrict__ out) {
-    for (std::int64_t j = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; j < cols;
-         j += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        double s = 0.0;
-        for (int c = 0; c < nblk; ++c) s += partial[c * cols + j];
-        out[j] = s;
-    }
+    const int lane = threadIdx.x & 31;
+    const std::int64_t j = blockIdx.x * static_cast<std::int64_t>(blockDim.x / 32) + (threadIdx.x >> 5);
+    if (j >= cols) return;
+    double s = 0.0;
+    for (int c = lane; c < nblk; c += 32) s += partial[c * cols + j];
+    s = warp_sum(s);
+    if (lane == 0) out[j] = s;
 }
 
 // Cholesky of a b x b Gram (b <= 112) together with R^{-1}, one CTA, everything in
@@ -608,7 +611,7 @@ void column_sumsq(cudaStream_t st, Workspace& ws, const MatView& v, double* out)
     const int thr = static_cast<int>(std::min<std::int64_t>(256, round_up(v.cols, 32)));
     colsumsq_stage1<<<nblk, thr, 0, st>>>(v, chunk, part);
     QB_LAUNCH_CHECK();
-    colsumsq_stage2<<<static_cast<int>(ceil_div(v.cols, 128)), 128, 0, st>>>(part, nblk, v.cols, out);
+    colsumsq_stage2<<<static_cast<int>(ceil_div(v.cols, 4)), 128, 0, st>>>(part, nblk, v.cols, out);
     QB_LAUNCH_CHECK();
 }
 

@@ -16,10 +16,75 @@
 #include "sparse.cuh"
 
 #include <algorithm>
+#include <vector>
 
 namespace qbgpu {
 
 namespace {
+
+// acc += sum_{e in [e0, e1)} v[e] * X[ci[e], :] for this lane's columns.
+template <int NQ>
+__device__ __forceinline__ void row_dot(const std::int32_t* __restrict__ ci, const double* __restrict__ v,
+                                        const double* __restrict__ x, std::int64_t ldx, int w, std::int64_t e0,
+                                        std::int64_t e1, int lane, double (&acc)[NQ]) {
+    for (std::int64_t eb = e0; eb < e1; eb += 32) {
+        const int cnt = static_cast<int>(e1 - eb < 32 ? e1 - eb : 32);
+        std::int32_t my_c = 0;
+        double my_v = 0.0;
+        if (lane < cnt) {
+            my_c = __ldg(ci + eb + lane);
+            my_v = __ldg(v + eb + lane);
+        }
+        for (int j = 0; j < cnt; ++j) {
+            const std::int32_t c = __shfl_sync(0xffffffffu, my_c, j);
+            const double a = __shfl_sync(0xffffffffu, my_v, j);
+            const double* xr = x + static_cast<std::int64_t>(c) * ldx;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int col = lane + 32 * q;
+                if (col < w) acc[q] = fma(a, __ldg(xr + col), acc[q]);
+            }
+        }
+    }
+}
+
+// Heavy-row segments: warp per segment, partial row into partial[seg * w + col].
+template <int NQ>
+__global__ void __launch_bounds__(256)
+csr_segment_kernel(std::int64_t nseg, const std::int64_t* __restrict__ seg, const std::int32_t* __restrict__ ci,
+                   const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx, int w,
+                   double* __restrict__ partial) {
+    const int lane = threadIdx.x & 31;
+    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (std::int64_t s = warp; s < nseg; s += nwarps) {
+        double acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+        row_dot<NQ>(ci, v, x, ldx, w, seg[nseg + s], seg[2 * nseg + s], lane, acc);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int col = lane + 32 * q;
+            if (col < w) partial[s * w + col] = acc[q];
+        }
+    }
+}
+
+// Heavy rows: y[row] = alpha * sum over its segments (in order) + beta * y[row].
+__global__ void csr_heavy_combine_kernel(std::int64_t nrows, const std::int64_t* __restrict__ hr,
+                                         const double* __restrict__ partial, double* __restrict__ y, std::int64_t ldy,
+                                         int w, double alpha, double beta) {
+    for (std::int64_t h = blockIdx.x; h < nrows; h += gridDim.x) {
+        const std::int64_t row = hr[h], s0 = hr[nrows + h], ns = hr[2 * nrows + h];
+        for (int col = threadIdx.x; col < w; col += blockDim.x) {
+            double s = 0.0;
+            for (std::int64_t q = 0; q < ns; ++q) s += partial[(s0 + q) * w + col];
+            double* yp = y + row * ldy + col;
+            const double r = alpha * s;
+            *yp = beta == 0.0 ? r : r + beta * (*yp);
+        }
+    }
+}
 
 template <int NQ>
 __global__ void __launch_bounds__(256)
@@ -34,6 +99,7 @@ csr_spmm_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const st
 #pragma unroll
         for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
         const std::int64_t e0 = rp[i], e1 = rp[i + 1];
+        if (e1 - e0 > kHeavyRow) continue;  // heavy rows: segment kernels
         for (std::int64_t eb = e0; eb < e1; eb += 32) {
             const int cnt = static_cast<int>(e1 - eb < 32 ? e1 - eb : 32);
             std::int32_t my_c = 0;
@@ -165,26 +231,79 @@ __global__ void validate_kernel(std::int64_t m, std::int64_t n, std::int64_t nnz
 
 }  // namespace
 
-void csr_spmm(cudaStream_t st, const CsrView& a, const double* x, std::int64_t ldx, double* y, std::int64_t ldy,
-              int w, double alpha, double beta, int sms) {
-    if (a.rows == 0 || w == 0) return;
-    const int threads = 256;
-    const std::int64_t warps_needed = a.rows;
-    const int blocks = static_cast<int>(std::max<std::int64_t>(
-        1, std::min<std::int64_t>(ceil_div(warps_needed * 32, threads), 16L * sms)));
-    if (w <= 32) csr_spmm_kernel<1><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta);
-    else if (w <= 64) csr_spmm_kernel<2><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta);
-    else if (w <= 128) csr_spmm_kernel<4><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta);
-    else if (w <= 256) csr_spmm_kernel<8><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta);
-    else {
-        // Wide right-hand sides (randQB_FP sketches): column slabs of 256.
-        for (int c0 = 0; c0 < w; c0 += 256) {
-            const int wc = std::min(256, w - c0);
-            csr_spmm_kernel<8><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x + c0, ldx, y + c0, ldy, wc,
-                                                           alpha, beta);
+HeavyPlan make_heavy_plan(const std::int64_t* rp, std::int64_t rows, cudaStream_t st) {
+    std::vector<std::int64_t> sr, slo, shi, hr, hs0, hns;
+    for (std::int64_t i = 0; i < rows; ++i) {
+        const std::int64_t len = rp[i + 1] - rp[i];
+        if (len <= kHeavyRow) continue;
+        hr.push_back(i);
+        hs0.push_back(static_cast<std::int64_t>(sr.size()));
+        std::int64_t cnt = 0;
+        for (std::int64_t e = rp[i]; e < rp[i + 1]; e += kHeavyRow, ++cnt) {
+            sr.push_back(i);
+            slo.push_back(e);
+            shi.push_back(std::min(rp[i + 1], e + kHeavyRow));
         }
+        hns.push_back(cnt);
     }
+    HeavyPlan p;
+    p.nseg = static_cast<std::int64_t>(sr.size());
+    p.nrows = static_cast<std::int64_t>(hr.size());
+    if (p.nseg == 0) return p;
+    std::vector<std::int64_t> seg(3 * p.nseg), hrows(3 * p.nrows);
+    std::copy(sr.begin(), sr.end(), seg.begin());
+    std::copy(slo.begin(), slo.end(), seg.begin() + p.nseg);
+    std::copy(shi.begin(), shi.end(), seg.begin() + 2 * p.nseg);
+    std::copy(hr.begin(), hr.end(), hrows.begin());
+    std::copy(hs0.begin(), hs0.end(), hrows.begin() + p.nrows);
+    std::copy(hns.begin(), hns.end(), hrows.begin() + 2 * p.nrows);
+    QB_CUDA(cudaMalloc(&p.seg, sizeof(std::int64_t) * seg.size()));
+    QB_CUDA(cudaMalloc(&p.rows, sizeof(std::int64_t) * hrows.size()));
+    QB_CUDA(cudaMemcpyAsync(p.seg, seg.data(), sizeof(std::int64_t) * seg.size(), cudaMemcpyHostToDevice, st));
+    QB_CUDA(cudaMemcpyAsync(p.rows, hrows.data(), sizeof(std::int64_t) * hrows.size(), cudaMemcpyHostToDevice, st));
+    QB_CUDA(cudaStreamSynchronize(st));
+    return p;
+}
+
+void free_heavy_plan(HeavyPlan& p) {
+    if (p.seg) cudaFree(p.seg);
+    if (p.rows) cudaFree(p.rows);
+    p = HeavyPlan{};
+}
+
+namespace {
+template <int NQ>
+void spmm_launch(cudaStream_t st, const CsrView& a, const double* x, std::int64_t ldx, double* y, std::int64_t ldy,
+                 int w, double alpha, double beta, int sms, double* partial) {
+    const int threads = 256;
+    const int blocks = static_cast<int>(std::max<std::int64_t>(
+        1, std::min<std::int64_t>(ceil_div(a.rows * 32, threads), 16L * sms)));
+    csr_spmm_kernel<NQ><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta);
     QB_LAUNCH_CHECK();
+    if (a.heavy.nseg > 0) {
+        const int sb = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(a.heavy.nseg * 32, threads), 16L * sms)));
+        csr_segment_kernel<NQ><<<sb, threads, 0, st>>>(a.heavy.nseg, a.heavy.seg, a.ci, a.v, x, ldx, w, partial);
+        QB_LAUNCH_CHECK();
+        csr_heavy_combine_kernel<<<static_cast<int>(std::min<std::int64_t>(a.heavy.nrows, 65535)), 128, 0, st>>>(
+            a.heavy.nrows, a.heavy.rows, partial, y, ldy, w, alpha, beta);
+        QB_LAUNCH_CHECK();
+    }
+}
+}  // namespace
+
+void csr_spmm(cudaStream_t st, const CsrView& a, const double* x, std::int64_t ldx, double* y, std::int64_t ldy,
+              int w, double alpha, double beta, int sms, double* partial) {
+    if (a.rows == 0 || w == 0) return;
+    if (a.heavy.nseg > 0 && !partial) throw QbError(kInternal, "csr_spmm: heavy rows need scratch");
+    if (w <= 32) return spmm_launch<1>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
+    if (w <= 64) return spmm_launch<2>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
+    if (w <= 128) return spmm_launch<4>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
+    if (w <= 256) return spmm_launch<8>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
+    // Wide right-hand sides (randQB_FP sketches): column slabs of 256.
+    for (int c0 = 0; c0 < w; c0 += 256) {
+        const int wc = std::min(256, w - c0);
+        spmm_launch<8>(st, a, x + c0, ldx, y + c0, ldy, wc, alpha, beta, sms, partial);
+    }
 }
 
 int csr_validate(cudaStream_t st, std::int64_t m, std::int64_t n, std::int64_t nnz, const std::int64_t* rp,

@@ -311,3 +311,21 @@ def test_orth_wide_matches_householder(ctx, oracle, rows, l, bcgs2):
         r = q.T @ x
         assert np.abs(np.tril(r, -1)).max() <= 1e-10 * np.abs(r).max()
         assert np.all(np.diag(r) > 0)
+
+
+@pytest.mark.parametrize("w", [7, 50, 100, 300])
+def test_csr_heavy_rows_and_columns(ctx, oracle, w):
+    """Zipf rows/columns longer than the 4096-entry segment limit (dense rows of A and
+    popular columns = heavy rows of the transposed CSR) against the reference kernels."""
+    from paper_1606_09402_b200 import matgen, qbfac
+    csr = matgen.csr_zipf(20000, 5000, alpha=1.1, target_nnz=300000, seed=7)
+    lens = np.diff(csr[2])
+    assert lens.max() > 4096 and np.bincount(csr[3]).max() > 4096
+    h = qbfac.MatrixHandle.csr(*csr, ctx=ctx)
+    rs = np.random.default_rng(w)
+    x = np.asfortranarray(rs.standard_normal((csr[1], w)))
+    xt = np.asfortranarray(rs.standard_normal((csr[0], w)))
+    y, yt = h.multiply(x, False), h.multiply(xt, True)
+    y_ref, yt_ref = oracle.csr_multiply(csr, x, False), oracle.csr_multiply(csr, xt, True)
+    assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < 1e-14
+    assert np.linalg.norm(yt - yt_ref) / np.linalg.norm(yt_ref) < 1e-14

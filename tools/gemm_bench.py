@@ -31,6 +31,10 @@ def main():
         ("Q*M 1e5x1000x50", 100000, 50, 1000, 1, 1, 1),
         ("Q^T*Y 1e5x1000x50", 1000, 50, 100000, 0, 1, 1),
         ("cfg1 A*Om 2000x20", 2000, 20, 2000, 0, 1, 1),
+        ("Bt^T*Om 5e4x500x50", 500, 50, 50000, 0, 1, 1),
+        ("Bt*M 5e4x500x50", 50000, 50, 500, 1, 1, 1),
+        ("Y*Rinv 1e5x50x50", 100000, 50, 50, 1, 0, 1),
+        ("gram Y^T Y 1e5x50", 50, 50, 100000, 0, 1, 0),
     ]
     res = {}
     for name, M, N, K, ar, br, cr in shapes:

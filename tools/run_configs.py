@@ -1,0 +1,156 @@
+"""Run the BASELINE configs on one GPU: time-to-epsilon (CUDA events, A resident),
+per-pass throughput, and parity against the oracle where the oracle finishes in a
+bounded time (config 1 and 3 in full; config 4 at reduced size).
+
+  python tools/run_configs.py [--configs 1,3,4,5] [--oracle]
+
+Writes gpurun_out/configs.json. The oracle is used only as the checker.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def timed(fn, reps):
+    import torch
+    out, ts = None, []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = fn()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+        if _ < reps - 1 and hasattr(out, "free"):
+            out.free()
+    return out, ts
+
+
+def sv(b):
+    return np.linalg.svd(b, compute_uv=False) if b.shape[0] else np.zeros(0)
+
+
+def pass_rate(h, w, trans, reps=3):
+    import torch
+    from paper_1606_09402_b200 import qbfac  # noqa: F401
+    rows_in = h.m if trans else h.n
+    rows_out = h.n if trans else h.m
+    x = torch.randn((rows_in, w), dtype=torch.float64, device="cuda")
+    y = torch.empty((rows_out, w), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    h.multiply_device(x.data_ptr(), w, w, trans, y.data_ptr(), w)
+    h.ctx.synchronize()
+    stream = torch.cuda.ExternalStream(h.ctx.stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        h.multiply_device(x.data_ptr(), w, w, trans, y.data_ptr(), w)
+    e1.record(stream)
+    h.ctx.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,3,4,5")
+    ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+
+    from paper_1606_09402_b200 import matgen, qbfac
+    ctx = qbfac.default_context()
+    cfgs = [int(c) for c in args.configs.split(",")]
+    res = {}
+    peak_hbm = 6554.9
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
+        peak_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", peak_hbm)
+    for c in cfgs:
+        t0 = time.perf_counter()
+        r = {"config": c}
+        if c == 1:
+            a = matgen.cfg1_matrix()
+            h = qbfac.MatrixHandle.dense(a, ctx)
+            eps = 1e-2 * float(np.linalg.norm(a))
+            run = lambda: qbfac.run_device(h, alg=0, b=20, power=0, max_rank=1000, eps_abs=eps, seed=42)
+            w, dense, nnz, kind = 20, True, 0, "EI dense 2000x2000 b=20 P=0 eps=1e-2"
+        elif c == 3:
+            csr = matgen.csr_uniform(100000, 50000, 50, seed=3)
+            h = qbfac.MatrixHandle.csr(*csr, ctx=ctx)
+            eps = 0.5 * float(np.sqrt((csr[4] ** 2).sum()))
+            run = lambda: qbfac.run_device(h, alg=0, b=50, power=1, max_rank=1000, eps_abs=eps, seed=42)
+            w, dense, nnz, kind = 50, False, len(csr[4]), "EI CSR 1e5x5e4 5M nnz b=50 P=1 eps=0.5 cap 1000"
+        elif c == 4:
+            m, n = 40000, 20000
+            at = matgen.synthesize_torch(m, n, np.exp(-np.arange(1, 401) / 60.0), 4, noise=1e-6)
+            h = qbfac.MatrixHandle.dense_device(at.data_ptr(), m, n, m, ctx)
+            del at
+            torch.cuda.empty_cache()
+            run = lambda: qbfac.run_device(h, alg=3, mode=0, b=100, k=400, s=0, seed=42)
+            w, dense, nnz, kind = 400, True, 0, "single-pass FP 40000x20000 l=400 b=100"
+        elif c == 5:
+            csr = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=3e8, seed=5)  # ~2e8 after de-dup
+            r["gen_s"] = time.perf_counter() - t0
+            r["nnz"] = len(csr[4])
+            h = qbfac.MatrixHandle.csr(*csr, ctx=ctx)
+            eps = 0.6 * float(np.sqrt((csr[4] ** 2).sum()))
+            run = lambda: qbfac.run_device(h, alg=0, b=100, power=2, max_rank=2000, eps_abs=eps, seed=42)
+            w, dense, nnz, kind = 100, False, len(csr[4]), "EI CSR 2e6x5e5 Zipf b=100 P=2 eps=0.6 cap 2000"
+        else:
+            continue
+        r["workload"] = kind
+        out, ts = timed(run, args.reps)
+        info = qbfac.info_dict(out.info)
+        r.update({"time_to_eps_s": float(np.median(ts)), "times": ts, "rank": info["rank"],
+                  "E": info["error_indicator"], "norm_a_sq": info["norm_a_sq"], "passes": info["passes"],
+                  "terminated_by": qbfac.TERMINATION[info["terminated_by"]], "blocks": info["blocks"],
+                  "device_ms": info["device_ms"], "hh_fallbacks": info["householder_fallbacks"]})
+        # per-pass throughput at the block width
+        t_n = pass_rate(h, w, False)
+        t_t = pass_rate(h, w, True)
+        if dense:
+            fl = 2.0 * h.m * h.n * w
+            r["pass_nn_tflops"] = fl / t_n / 1e12
+            r["pass_tn_tflops"] = fl / t_t / 1e12
+        else:
+            byt_n = 12 * nnz + 8 * (h.m + 1) + 8 * h.n * w + 8 * h.m * w
+            byt_t = 12 * nnz + 8 * (h.n + 1) + 8 * h.m * w + 8 * h.n * w
+            r["pass_n_gbs"] = byt_n / t_n / 1e9
+            r["pass_t_gbs"] = byt_t / t_t / 1e9
+            r["pass_n_frac_hbm"] = r["pass_n_gbs"] / peak_hbm
+            r["pass_t_frac_hbm"] = r["pass_t_gbs"] / peak_hbm
+        if args.oracle and c in (1, 3):
+            from oracle import oracle as O
+            q, b = out.q(), out.b()
+            t1 = time.perf_counter()
+            if c == 1:
+                ref = O.run("ei", a, b=20, power=0, eps_abs=eps, max_rank=1000, seed=42)
+                err_g, err_r = O.explicit_error(q, b, a=a), O.explicit_error(ref.Q, ref.B, a=a)
+            else:
+                ref = O.run("ei", csr=csr, b=50, power=1, eps_abs=eps, max_rank=1000, seed=42)
+                err_g, err_r = O.explicit_error(q, b, csr=csr), O.explicit_error(ref.Q, ref.B, csr=csr)
+            r["oracle_s"] = time.perf_counter() - t1
+            sg, sr = sv(b), sv(ref.B)
+            r["parity"] = {"rank": [info["rank"], ref.rank], "E": [info["error_indicator"], ref.E],
+                           "E_rel": abs(info["error_indicator"] - ref.E) / abs(ref.E),
+                           "sigma_max_rel": float(np.max(np.abs(sg - sr) / sr)) if len(sr) == len(sg) else None,
+                           "err": [err_g, err_r], "err_rel": abs(err_g - err_r) / err_r,
+                           "passes": [info["passes"], ref.passes]}
+        out.free()
+        h.free()
+        r["wall_s"] = time.perf_counter() - t0
+        res[c] = r
+        print(json.dumps(r), flush=True)
+        torch.cuda.empty_cache()
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    json.dump(res, open(os.path.join(ROOT, "gpurun_out", "configs.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
