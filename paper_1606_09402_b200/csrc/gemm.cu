@@ -332,7 +332,7 @@ void launch_family(cudaStream_t st, const MatView& a, const MatView& b, double* 
         launch_cfg<128, 64, 16, 4, 2, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
                                                       alpha, beta, partial, flags);
     else if constexpr (F == Family::kSkinny56)  // b = 50-56: 7 n8 tiles per warp, no 64-column padding
-        launch_cfg<128, 56, 16, 8, 1, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
+        launch_cfg<128, 56, 32, 8, 1, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
                                                       alpha, beta, partial, flags);
     else
         launch_cfg<64, 32, 32, 2, 2, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
@@ -388,7 +388,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     Family fam;
     int bm, bn, bk;
     if (N >= 96) { fam = Family::kWide; bm = 128; bn = 128; bk = QB_WIDE_BK; }
-    else if (N > 48 && N <= 56) { fam = Family::kSkinny56; bm = 128; bn = 56; bk = 16; }
+    else if (N > 48 && N <= 56) { fam = Family::kSkinny56; bm = 128; bn = 56; bk = 32; }
     else if (N > 32) { fam = Family::kSkinny; bm = 128; bn = 64; bk = 16; }
     else { fam = Family::kNarrow; bm = 64; bn = 32; bk = 32; }
     const bool vec2 = aligned16(a) && aligned16(b);
@@ -409,7 +409,10 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     if (tiles < want) {
         const std::int64_t max_by_k = std::max<std::int64_t>(1, K / (4 * bk));  // >= 4 k-tiles/split
         const std::int64_t cap = (M * N <= 65536) ? 512 : 64;  // small outputs (Grams): deep split-K
-        splits = static_cast<int>(std::min<std::int64_t>(std::min<std::int64_t>(ceil_div(want, tiles), max_by_k), cap));
+        // floor: tiles * splits must not exceed one wave of resident CTAs (a 2nd partial wave
+        // doubles the time; measured on Q^T Y 1000x50x1e5)
+        const std::int64_t fit = std::max<std::int64_t>(1, want / tiles);
+        splits = static_cast<int>(std::min<std::int64_t>(std::min<std::int64_t>(fit, max_by_k), cap));
     }
     int klen = static_cast<int>(round_up(ceil_div(K, splits), bk));
     splits = static_cast<int>(ceil_div(K, klen));

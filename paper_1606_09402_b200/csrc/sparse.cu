@@ -22,11 +22,17 @@ namespace qbgpu {
 
 namespace {
 
-// acc += sum_{e in [e0, e1)} v[e] * X[ci[e], :] for this lane's columns.
+// acc += sum_{e in [e0, e1)} v[e] * X[ci[e], :] for this lane's columns. Lanes load 32
+// (col, val) pairs at once and broadcast them; four nonzeros are gathered per step
+// into four independent accumulator sets (more loads in flight, no serial FMA chain),
+// combined in a fixed order at the end (deterministic).
 template <int NQ>
 __device__ __forceinline__ void row_dot(const std::int32_t* __restrict__ ci, const double* __restrict__ v,
                                         const double* __restrict__ x, std::int64_t ldx, int w, std::int64_t e0,
                                         std::int64_t e1, int lane, double (&acc)[NQ]) {
+    double a1[NQ], a2[NQ], a3[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) a1[q] = a2[q] = a3[q] = 0.0;
     for (std::int64_t eb = e0; eb < e1; eb += 32) {
         const int cnt = static_cast<int>(e1 - eb < 32 ? e1 - eb : 32);
         std::int32_t my_c = 0;
@@ -35,10 +41,35 @@ __device__ __forceinline__ void row_dot(const std::int32_t* __restrict__ ci, con
             my_c = __ldg(ci + eb + lane);
             my_v = __ldg(v + eb + lane);
         }
-        for (int j = 0; j < cnt; ++j) {
-            const std::int32_t c = __shfl_sync(0xffffffffu, my_c, j);
+        int j = 0;
+        for (; j + 4 <= cnt; j += 4) {
+            const double* x0 = x + static_cast<std::int64_t>(__shfl_sync(0xffffffffu, my_c, j)) * ldx;
+            const double* x1 = x + static_cast<std::int64_t>(__shfl_sync(0xffffffffu, my_c, j + 1)) * ldx;
+            const double* x2 = x + static_cast<std::int64_t>(__shfl_sync(0xffffffffu, my_c, j + 2)) * ldx;
+            const double* x3 = x + static_cast<std::int64_t>(__shfl_sync(0xffffffffu, my_c, j + 3)) * ldx;
+            const double v0 = __shfl_sync(0xffffffffu, my_v, j), v1 = __shfl_sync(0xffffffffu, my_v, j + 1);
+            const double v2 = __shfl_sync(0xffffffffu, my_v, j + 2), v3 = __shfl_sync(0xffffffffu, my_v, j + 3);
+            double g0[NQ], g1[NQ], g2[NQ], g3[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int col = lane + 32 * q;
+                const bool ok = col < w;
+                g0[q] = ok ? __ldg(x0 + col) : 0.0;
+                g1[q] = ok ? __ldg(x1 + col) : 0.0;
+                g2[q] = ok ? __ldg(x2 + col) : 0.0;
+                g3[q] = ok ? __ldg(x3 + col) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                acc[q] = fma(v0, g0[q], acc[q]);
+                a1[q] = fma(v1, g1[q], a1[q]);
+                a2[q] = fma(v2, g2[q], a2[q]);
+                a3[q] = fma(v3, g3[q], a3[q]);
+            }
+        }
+        for (; j < cnt; ++j) {
+            const double* xr = x + static_cast<std::int64_t>(__shfl_sync(0xffffffffu, my_c, j)) * ldx;
             const double a = __shfl_sync(0xffffffffu, my_v, j);
-            const double* xr = x + static_cast<std::int64_t>(c) * ldx;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const int col = lane + 32 * q;
@@ -46,6 +77,8 @@ __device__ __forceinline__ void row_dot(const std::int32_t* __restrict__ ci, con
             }
         }
     }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = (acc[q] + a1[q]) + (a2[q] + a3[q]);
 }
 
 // Heavy-row segments: warp per segment, partial row into partial[seg * w + col].
@@ -100,25 +133,7 @@ csr_spmm_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const st
         for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
         const std::int64_t e0 = rp[i], e1 = rp[i + 1];
         if (e1 - e0 > kHeavyRow) continue;  // heavy rows: segment kernels
-        for (std::int64_t eb = e0; eb < e1; eb += 32) {
-            const int cnt = static_cast<int>(e1 - eb < 32 ? e1 - eb : 32);
-            std::int32_t my_c = 0;
-            double my_v = 0.0;
-            if (lane < cnt) {
-                my_c = __ldg(ci + eb + lane);
-                my_v = __ldg(v + eb + lane);
-            }
-            for (int j = 0; j < cnt; ++j) {
-                const std::int32_t c = __shfl_sync(0xffffffffu, my_c, j);
-                const double a = __shfl_sync(0xffffffffu, my_v, j);
-                const double* xr = x + static_cast<std::int64_t>(c) * ldx;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const int col = lane + 32 * q;
-                    if (col < w) acc[q] = fma(a, __ldg(xr + col), acc[q]);
-                }
-            }
-        }
+        row_dot<NQ>(ci, v, x, ldx, w, e0, e1, lane, acc);
         double* yr = y + i * ldy;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
