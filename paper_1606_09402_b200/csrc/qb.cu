@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <tuple>
 
 namespace qbgpu {
 
@@ -52,6 +53,8 @@ Context::Context(int dev, int rank_, int world_, const void* nccl_id) : device(d
     QB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     QB_CUDA(cudaMalloc(&d_small, sizeof(double) * kSlot * kNumSlots + 64 * sizeof(double)));
     QB_CUDA(cudaMalloc(&d_status, sizeof(SmallStatus) * 4));
+    QB_CUDA(cudaMalloc(&d_lazy, sizeof(SmallStatus) * kLazyCap));
+    QB_CUDA(cudaMallocHost(&h_lazy, sizeof(SmallStatus) * kLazyCap));
     QB_CUDA(cudaMalloc(&d_ind, sizeof(IndicatorOut)));
     QB_CUDA(cudaMallocHost(&h_status, sizeof(SmallStatus) * 4));
     QB_CUDA(cudaMallocHost(&h_ind, sizeof(IndicatorOut)));
@@ -76,6 +79,8 @@ Context::~Context() {
     ws_sp.release();
     if (d_small) cudaFree(d_small);
     if (d_status) cudaFree(d_status);
+    if (d_lazy) cudaFree(d_lazy);
+    if (h_lazy) cudaFreeHost(h_lazy);
     if (d_ind) cudaFree(d_ind);
     if (h_status) cudaFreeHost(h_status);
     if (h_ind) cudaFreeHost(h_ind);
@@ -227,32 +232,63 @@ public:
     // (slot rinv_slot), such that Y = Q R, diag(R) > 0. `sharded`: rows are split over
     // ranks (Grams are allreduced). Returns the leading rank d (first index with
     // R_jj <= 1e-12 max R_jj, qr.hpp:20-21), b when full rank.
+    // Optimistic CholQR (per block): Cholesky statuses are written to a device array and
+    // checked once, together with the indicator read, at the end of the block. If any
+    // pass needed the fallback the caller re-runs the whole block with force_hh.
+    bool optimistic = false, force_hh = false;
+    int lazy_n = 0;
+    void begin_block(bool opt, bool force) {
+        optimistic = opt;
+        force_hh = force;
+        lazy_n = 0;
+    }
+    void fetch_lazy() {
+        if (lazy_n)
+            QB_CUDA(cudaMemcpyAsync(c_.h_lazy, c_.d_lazy, sizeof(SmallStatus) * 2 * lazy_n, cudaMemcpyDeviceToHost, st_));
+    }
+    bool lazy_ok() const {  // after the stream sync that follows fetch_lazy()
+        for (int i = 0; i < lazy_n; ++i)
+            if (!cholqr_ok(c_.h_lazy[2 * i], c_.h_lazy[2 * i + 1])) return false;
+        return true;
+    }
+    static bool cholqr_ok(const SmallStatus& s0, const SmallStatus& s1) {
+        return !s0.breakdown && !s1.breakdown && s0.diag_max > 0.0 && s0.diag_min >= kCholRatioMin * s0.diag_max &&
+               s1.gram_dev <= kCholGramDevMax && std::isfinite(s0.diag_max) && std::isfinite(s1.diag_max);
+    }
+
     int orth_block(const MatView& y, const MatView& qout, int r_slot, int rinv_slot, bool sharded, DBuf& tmp) {
         const int b = static_cast<int>(y.cols);
         const std::int64_t rows = y.rows;
         if (b == 0) return 0;
         if (b > kSmallMax) throw QbError(kDimensionError, "block size exceeds the device panel limit (112)");
         MatView t1{tmp.p, rows, b, b, true};
-        // pass 1
-        gemm(1.0, y.t(), y, 0.0, small(kG, b, b));
-        if (sharded) c_.allreduce(slot(kG), kSlot);
-        chol_small(st_, slot(kG), kSmallMax, b, slot(kRa), slot(kRainv), kSmallMax, c_.d_status + 0);
-        gemm(1.0, y, small(kRainv, b, b), 0.0, t1);
-        // pass 2
-        gemm(1.0, t1.t(), t1, 0.0, small(kG, b, b));
-        if (sharded) c_.allreduce(slot(kG), kSlot);
-        chol_small(st_, slot(kG), kSmallMax, b, slot(kRb), slot(kRbinv), kSmallMax, c_.d_status + 1);
-        QB_CUDA(cudaMemcpyAsync(c_.h_status, c_.d_status, sizeof(SmallStatus) * 2, cudaMemcpyDeviceToHost, st_));
-        QB_CUDA(cudaStreamSynchronize(st_));
-        const SmallStatus s0 = c_.h_status[0], s1 = c_.h_status[1];
-        const bool ok = !s0.breakdown && !s1.breakdown && s0.diag_max > 0.0 &&
-                        s0.diag_min >= kCholRatioMin * s0.diag_max && s1.gram_dev <= kCholGramDevMax &&
-                        std::isfinite(s0.diag_max) && std::isfinite(s1.diag_max);
-        if (ok) {
-            gemm(1.0, t1, small(kRbinv, b, b), 0.0, qout);
-            trmm_upper_pair(st_, slot(kRb), slot(kRa), slot(r_slot), slot(kRainv), slot(kRbinv), slot(rinv_slot), b,
-                            kSmallMax);
-            return b;
+        if (!force_hh) {
+            const bool lazy = optimistic && lazy_n < Context::kLazyCap / 2;
+            SmallStatus* st0 = lazy ? c_.d_lazy + 2 * lazy_n : c_.d_status + 0;
+            SmallStatus* st1 = st0 + 1;
+            // pass 1
+            gemm(1.0, y.t(), y, 0.0, small(kG, b, b));
+            if (sharded) c_.allreduce(slot(kG), kSlot);
+            chol_small(st_, slot(kG), kSmallMax, b, slot(kRa), slot(kRainv), kSmallMax, st0);
+            gemm(1.0, y, small(kRainv, b, b), 0.0, t1);
+            // pass 2
+            gemm(1.0, t1.t(), t1, 0.0, small(kG, b, b));
+            if (sharded) c_.allreduce(slot(kG), kSlot);
+            chol_small(st_, slot(kG), kSmallMax, b, slot(kRb), slot(kRbinv), kSmallMax, st1);
+            bool ok = true;
+            if (lazy) {
+                ++lazy_n;
+            } else {
+                QB_CUDA(cudaMemcpyAsync(c_.h_status, st0, sizeof(SmallStatus) * 2, cudaMemcpyDeviceToHost, st_));
+                QB_CUDA(cudaStreamSynchronize(st_));
+                ok = cholqr_ok(c_.h_status[0], c_.h_status[1]);
+            }
+            if (ok) {
+                gemm(1.0, t1, small(kRbinv, b, b), 0.0, qout);
+                trmm_upper_pair(st_, slot(kRb), slot(kRa), slot(r_slot), slot(kRainv), slot(kRbinv), slot(rinv_slot),
+                                b, kSmallMax);
+                return b;
+            }
         }
         // Householder fallback: exact deficiency decisions (qr.hpp:15-21).
         if (sharded && c_.world > 1)
@@ -458,15 +494,23 @@ struct State {
     MatView qslot(std::int64_t w) const { return MatView{q.p + k, m, w, ld, true}; }
     MatView btslot(std::int64_t w) const { return MatView{bt.p + k, n, w, ld, true}; }
 
-    // Rows of B_i enter E one by one. Returns (keep, met).
-    std::pair<int, bool> indicator(int d, bool check) {
+    // Rows of B_i enter E one by one: enqueue the device step and the
+    // read-back of its result (and of the block's lazy CholQR statuses), then one sync.
+    void indicator_enqueue(int d, bool check) {
         double* norms = c.d_small + static_cast<std::size_t>(kNorms) * kSlot;
         column_sumsq(c.st, c.ws_red, btslot(d), norms);
         indicator_step(c.st, d_e, norms, d, eps2, check ? 1 : 0, c.d_ind);
         QB_CUDA(cudaMemcpyAsync(c.h_ind, c.d_ind, sizeof(IndicatorOut), cudaMemcpyDeviceToHost, c.st));
+    }
+    std::pair<int, bool> indicator_finish() {
         QB_CUDA(cudaStreamSynchronize(c.st));
-        trace.push_back(c.h_ind->e);
         return {c.h_ind->keep, c.h_ind->met != 0};
+    }
+    std::pair<int, bool> indicator(int d, bool check) {
+        indicator_enqueue(d, check);
+        auto r = indicator_finish();
+        trace.push_back(c.h_ind->e);
+        return r;
     }
     void set_e(double e) {
         c.h_scalar[1] = e;
@@ -536,56 +580,81 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
     DBuf tmp(static_cast<std::size_t>(std::max<std::int64_t>(std::max<std::int64_t>(m, n), 1)) * bpad, c.st);
     DBuf z(p.power > 0 ? static_cast<std::size_t>(n) * bpad : 0, c.st);
     DBuf mbuf(static_cast<std::size_t>(std::max<std::int64_t>(cap, 1)) * bpad, c.st);
+    double e_host = norm_a_sq;
     while (true) {
         if (s.k >= cap) { term = 0; break; }
         const std::int64_t bi = std::min(p.b, cap - s.k);
         ++blocks;
+        const std::int64_t passes_before = a.passes;
         MatView omv{om.p, n, bi, bi, true};
-        gaussian_fill(c.st, c.rng, p.seed, p.stream, static_cast<std::uint64_t>(g_used), omv);  // step 4
-        g_used += n * bi;
         MatView yv{y.p, m, bi, bi, true};
         MatView mv{mbuf.p, s.k, bi, bi, true};
-        // step 5: Y = A Omega_i - Q (B Omega_i)
-        eng.apply(omv, yv); a.passes += 1;
-        if (s.k > 0) {
-            eng.gemm(1.0, s.btk().t(), omv, 0.0, mv);
-            eng.gemm(-1.0, s.qk(), mv, 1.0, yv);
-        }
-        // per-block power iteration with deflation at every application
-        for (std::int64_t it = 0; it < p.power; ++it) {
-            eng.orth_block(yv, yv, kR1, kR1inv, sharded, tmp);
-            MatView zv{z.p, n, bi, bi, true};
-            eng.apply_t(yv, zv); a.passes += 1;
+        int d = 0, keep = 0;
+        bool met = false;
+        // attempt 0: optimistic CholQR, statuses checked once with the indicator read;
+        // attempt 1 (rare): the same block with Householder panels (exact deficiency rules).
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            a.passes = passes_before;
+            eng.begin_block(/*optimistic=*/true, /*force_hh=*/attempt > 0);
+            gaussian_fill(c.st, c.rng, p.seed, p.stream, static_cast<std::uint64_t>(g_used), omv);  // step 4
+            // step 5: Y = A Omega_i - Q (B Omega_i)
+            eng.apply(omv, yv); a.passes += 1;
             if (s.k > 0) {
-                eng.gemm(1.0, s.qk().t(), yv, 0.0, mv);
-                eng.allreduce_view(mv);
-                eng.gemm(-1.0, s.btk(), mv, 1.0, zv);
-            }
-            eng.orth_block(zv, zv, kR1, kR1inv, false, tmp);
-            eng.apply(zv, yv); a.passes += 1;
-            if (s.k > 0) {
-                eng.gemm(1.0, s.btk().t(), zv, 0.0, mv);
+                eng.gemm(1.0, s.btk().t(), omv, 0.0, mv);
                 eng.gemm(-1.0, s.qk(), mv, 1.0, yv);
             }
+            // per-block power iteration with deflation at every application
+            for (std::int64_t it = 0; it < p.power; ++it) {
+                eng.orth_block(yv, yv, kR1, kR1inv, sharded, tmp);
+                MatView zv{z.p, n, bi, bi, true};
+                eng.apply_t(yv, zv); a.passes += 1;
+                if (s.k > 0) {
+                    eng.gemm(1.0, s.qk().t(), yv, 0.0, mv);
+                    eng.allreduce_view(mv);
+                    eng.gemm(-1.0, s.btk(), mv, 1.0, zv);
+                }
+                eng.orth_block(zv, zv, kR1, kR1inv, false, tmp);
+                eng.apply(zv, yv); a.passes += 1;
+                if (s.k > 0) {
+                    eng.gemm(1.0, s.btk().t(), zv, 0.0, mv);
+                    eng.gemm(-1.0, s.qk(), mv, 1.0, yv);
+                }
+            }
+            // orth, then re-orthogonalisation against Q (step 6)
+            MatView qs = s.qslot(bi);
+            d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp);
+            if (d > 0 && s.k > 0) {
+                MatView qd = s.qslot(d);
+                MatView md{mbuf.p, s.k, d, d, true};
+                eng.gemm(1.0, s.qk().t(), qd, 0.0, md);
+                eng.allreduce_view(md);
+                eng.gemm(-1.0, s.qk(), md, 1.0, qd);
+                const int d2 = eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp);
+                d = std::min(d, d2);
+            }
+            if (d == 0) {
+                if (attempt == 0) { eng.fetch_lazy(); QB_CUDA(cudaStreamSynchronize(c.st)); }
+                if (attempt == 0 && !eng.lazy_ok()) continue;
+                break;
+            }
+            // step 7: B_i^T = A^T Q_i (+1 pass)
+            eng.apply_t(s.qslot(d), s.btslot(d));
+            a.passes += 1;
+            s.indicator_enqueue(d, fixed_prec);
+            eng.fetch_lazy();
+            std::tie(keep, met) = s.indicator_finish();
+            if (attempt == 0 && !eng.lazy_ok()) {
+                if (sharded) throw QbError(kError, "numerically rank-deficient sketch under row sharding (Householder "
+                                                   "panel fallback is single-GPU)");
+                s.set_e(e_host);  // undo this block's indicator update
+                continue;
+            }
+            break;
         }
-        // orth, then re-orthogonalisation against Q (step 6)
-        MatView qs = s.qslot(bi);
-        int d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp);
+        g_used += n * bi;
         if (d == 0) { term = 3; break; }
-        if (s.k > 0) {
-            MatView qd = s.qslot(d);
-            MatView md{mbuf.p, s.k, d, d, true};
-            eng.gemm(1.0, s.qk().t(), qd, 0.0, md);
-            eng.allreduce_view(md);
-            eng.gemm(-1.0, s.qk(), md, 1.0, qd);
-            const int d2 = eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp);
-            if (d2 == 0) { term = 3; break; }
-            d = std::min(d, d2);
-        }
-        // step 7: B_i^T = A^T Q_i (+1 pass)
-        eng.apply_t(s.qslot(d), s.btslot(d));
-        a.passes += 1;
-        auto [keep, met] = s.indicator(d, fixed_prec);
+        e_host = c.h_ind->e;
+        s.trace.push_back(e_host);
         s.k += keep;
         if (met) { term = 1; break; }
         if (d < bi) { term = 3; break; }
@@ -638,6 +707,7 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
     DBuf m1(static_cast<std::size_t>(std::max<std::int64_t>(cap, 1)) * bpad, c.st);
     DBuf m2(static_cast<std::size_t>(std::max<std::int64_t>(cap, std::max<std::int64_t>(lpad, 64))) * std::max<std::int64_t>(bpad, 64), c.st);
     DBuf wtmp(p.power > 0 ? static_cast<std::size_t>(std::max<std::int64_t>(std::max<std::int64_t>(m, n), 1)) * 64 : 0, c.st);
+    double e_host = 0.0;
     for (int restart = 0;; ++restart) {
         if (s.k >= cap) { term = 0; break; }
         if (fixed && restart > 0) { term = 0; break; }
@@ -659,6 +729,7 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
         eng.apply(omv, gv); a.passes += 1;                                         // step 7
         if (restart == 0) {                                                        // step 9
             norm_a_sq = eng.frob_device(s.d_e);  // same logical pass (multiply_with_norm)
+            e_host = norm_a_sq;
             if (!fixed) {
                 check_eps(p.eps_abs, norm_a_sq);
                 if (norm_a_sq < s.eps2) { term = 1; break; }
@@ -674,47 +745,68 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
             MatView hi = hv.cols_range(off, bi);
             MatView yv{y.p, m, bi, bi, true};
             MatView m1v{m1.p, s.k, bi, bi, true};
-            copy_matrix(c.st, gi, yv);
-            if (s.k > 0) {                                                         // step 12
-                eng.gemm(1.0, s.btk().t(), omi, 0.0, m1v);
-                eng.gemm(-1.0, s.qk(), m1v, 1.0, yv);
-            }
-            MatView qs = s.qslot(bi);
-            int d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp);            // step 13
-            if (d == 0) { term = 3; stop = true; break; }
-            int r_slot = kR1, rinv_slot = kR1inv;
-            if (reorth && s.k > 0) {                                               // steps 14-15 (9a-9b)
-                MatView qd = s.qslot(d);
-                MatView md{m2.p, s.k, d, d, true};
-                eng.gemm(1.0, s.qk().t(), qd, 0.0, md);
-                eng.allreduce_view(md);
-                eng.gemm(-1.0, s.qk(), md, 1.0, qd);
-                const int d2 = eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp);
-                if (d2 == 0) { term = 3; stop = true; break; }
-                d = std::min(d, d2);
-                trmm_upper_pair(c.st, eng.slot(kR2), eng.slot(kR1), eng.slot(kR), eng.slot(kR1inv), eng.slot(kR2inv),
-                                eng.slot(kRinv), d, kSmallMax);
-                r_slot = kR;
-                rinv_slot = kRinv;
-            }
-            (void)r_slot;
-            // step 16 (9c): B_i^T = (H_i - B^T (Q^T Y_i + B Omega_i)) R_i^{-1}
-            //   (Alg. 3 without re-orth: B_i^T = (H_i - B^T (B Omega_i)) R_i^{-1})
-            MatView ctv{ct.p, n, d, d, true};
-            copy_matrix(c.st, hi.cols_range(0, d), ctv);
-            if (s.k > 0) {
-                MatView mm{m2.p, s.k, d, d, true};
-                if (reorth) {
-                    eng.gemm(1.0, s.qk().t(), yv.cols_range(0, d), 0.0, mm);
-                    eng.allreduce_view(mm);
-                    add_matrix(c.st, m1v.cols_range(0, d), mm, 1.0);
-                } else {
-                    copy_matrix(c.st, m1v.cols_range(0, d), mm);
+            int d = 0, keep = 0;
+            bool met = false;
+            for (int attempt = 0; attempt < 2; ++attempt) {  // optimistic CholQR, Householder redo
+                eng.begin_block(true, attempt > 0);
+                copy_matrix(c.st, gi, yv);
+                if (s.k > 0) {                                                     // step 12
+                    eng.gemm(1.0, s.btk().t(), omi, 0.0, m1v);
+                    eng.gemm(-1.0, s.qk(), m1v, 1.0, yv);
                 }
-                eng.gemm(-1.0, s.btk(), mm, 1.0, ctv);
+                MatView qs = s.qslot(bi);
+                d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp);            // step 13
+                int rinv_slot = kR1inv;
+                if (d > 0 && reorth && s.k > 0) {                                  // steps 14-15 (9a-9b)
+                    MatView qd = s.qslot(d);
+                    MatView md{m2.p, s.k, d, d, true};
+                    eng.gemm(1.0, s.qk().t(), qd, 0.0, md);
+                    eng.allreduce_view(md);
+                    eng.gemm(-1.0, s.qk(), md, 1.0, qd);
+                    const int d2 = eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp);
+                    d = std::min(d, d2);
+                    if (d > 0) {
+                        trmm_upper_pair(c.st, eng.slot(kR2), eng.slot(kR1), eng.slot(kR), eng.slot(kR1inv),
+                                        eng.slot(kR2inv), eng.slot(kRinv), d, kSmallMax);
+                        rinv_slot = kRinv;
+                    }
+                }
+                if (d == 0) {
+                    if (attempt == 0) { eng.fetch_lazy(); QB_CUDA(cudaStreamSynchronize(c.st)); }
+                    if (attempt == 0 && !eng.lazy_ok()) continue;
+                    break;
+                }
+                // step 16 (9c): B_i^T = (H_i - B^T (Q^T Y_i + B Omega_i)) R_i^{-1}
+                //   (Alg. 3 without re-orth: B_i^T = (H_i - B^T (B Omega_i)) R_i^{-1})
+                MatView ctv{ct.p, n, d, d, true};
+                copy_matrix(c.st, hi.cols_range(0, d), ctv);
+                if (s.k > 0) {
+                    MatView mm{m2.p, s.k, d, d, true};
+                    if (reorth) {
+                        eng.gemm(1.0, s.qk().t(), yv.cols_range(0, d), 0.0, mm);
+                        eng.allreduce_view(mm);
+                        add_matrix(c.st, m1v.cols_range(0, d), mm, 1.0);
+                    } else {
+                        copy_matrix(c.st, m1v.cols_range(0, d), mm);
+                    }
+                    eng.gemm(-1.0, s.btk(), mm, 1.0, ctv);
+                }
+                eng.gemm(1.0, ctv, eng.small(rinv_slot, d, d), 0.0, s.btslot(d));
+                s.indicator_enqueue(d, !fixed);                                    // steps 19-20
+                eng.fetch_lazy();
+                std::tie(keep, met) = s.indicator_finish();
+                if (attempt == 0 && !eng.lazy_ok()) {
+                    if (sharded) throw QbError(kError, "numerically rank-deficient sketch under row sharding "
+                                                       "(Householder panel fallback is single-GPU)");
+                    s.set_e(e_host);
+                    continue;
+                }
+                break;
             }
-            eng.gemm(1.0, ctv, eng.small(rinv_slot, d, d), 0.0, s.btslot(d));
-            auto [keep, met] = s.indicator(d, !fixed);                              // steps 19-20
+            eng.begin_block(false, false);
+            if (d == 0) { term = 3; stop = true; break; }
+            e_host = c.h_ind->e;
+            s.trace.push_back(e_host);
             s.k += keep;
             if (met) { term = 1; stop = true; break; }
             if (d < bi) { term = 3; stop = true; break; }

@@ -55,6 +55,9 @@ struct Context {
     double* d_small = nullptr;
     SmallStatus* d_status = nullptr;
     IndicatorOut* d_ind = nullptr;
+    static constexpr int kLazyCap = 256;    // optimistic CholQR statuses per block
+    SmallStatus* d_lazy = nullptr;
+    SmallStatus* h_lazy = nullptr;
     // pinned host mirrors
     SmallStatus* h_status = nullptr;
     IndicatorOut* h_ind = nullptr;
