@@ -8,12 +8,12 @@
 // the u64 pair (2*floor(g/2), 2*floor(g/2)+1) and the parity of g.
 //
 // B200 design: xoshiro256's state transition T is linear over GF(2), so the state
-// at u64 index u is T^u * s0. Host code precomputes T^(2^k) (k < 64) once; each CTA
-// jumps its anchor with a warp-cooperative GF(2) mat-vec (lanes split the 256
-// input bits, XOR-butterfly combine), then the CTA's 256 threads derive their own
-// starting states with an 8-level doubling scan. Each thread then runs the
-// generator sequentially over kPairsPerThread pairs. The integer stream is
-// bit-identical to the reference; log/sin/cos come from CUDA's libdevice.
+// at u64 index u is T^u * s0. The host precomputes T^(2^k) (k < 64) once, jumps the
+// call's base state, and keeps on the device nibble lookup tables of T^(d*16^(pos+1))
+// (6 hex positions x 15 digits, 2.9 MB); every thread derives its own start state with
+// one 64-lookup mat-vec per non-zero hex digit of its global index (<= 6, no barriers)
+// and runs the generator over 8 pairs. The integer stream is bit-identical to the
+// reference; log/sin/cos come from CUDA's libdevice.
 
 #include <array>
 #include <cstring>
@@ -98,117 +98,55 @@ const std::vector<std::uint64_t>& jump_tables_host() {
 
 // ---------------------------------------------------------------------------------
 constexpr int kGenThreads = 256;
-constexpr int kPairsPerThread = 32;            // 64 u64 per thread => per-thread jump = t * 2^6
-constexpr int kThreadJumpLevel0 = 6;           // log2(2 * kPairsPerThread)
+constexpr int kMinPairsPerThread = 8; // thread g starts at u64 offset 2 * ppt * g = 16 * (g * ppt / 8)
+constexpr int kDigitPositions = 6;    // hex digits of the global thread index (16^6 threads)
 
-// Warp-cooperative y = M * x for a table matrix M (global, 256 cols x 4 words).
-__device__ __forceinline__ void warp_matvec(const std::uint64_t* __restrict__ m, const std::uint64_t (&x)[4],
-                                            std::uint64_t (&y)[4]) {
-    const int lane = threadIdx.x & 31;
+// Nibble ("four Russians") table of a GF(2) 256x256 matrix M: entry [p][v] is the XOR of
+// the columns of M selected by nibble value v at nibble position p (64 x 16 x 4 words =
+// 32 KB). y = M x is 64 independent 32-byte lookups.
+__device__ __forceinline__ void nib_matvec(const std::uint64_t* __restrict__ tab, std::uint64_t& s0,
+                                           std::uint64_t& s1, std::uint64_t& s2, std::uint64_t& s3) {
     std::uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-    const int word = lane >> 3;              // bits [8*lane, 8*lane+8)
-    const std::uint64_t bits = (x[word] >> ((lane & 7) * 8)) & 0xFFULL;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if ((bits >> k) & 1ULL) {
-            const std::uint64_t* col = m + (lane * 8 + k) * 4;
-            r0 ^= __ldg(col); r1 ^= __ldg(col + 1); r2 ^= __ldg(col + 2); r3 ^= __ldg(col + 3);
-        }
+    for (int p = 0; p < 64; ++p) {
+        const std::uint64_t w = p < 16 ? s0 : (p < 32 ? s1 : (p < 48 ? s2 : s3));
+        const unsigned v = static_cast<unsigned>(w >> ((p & 15) * 4)) & 15u;
+        const ulonglong2* e = reinterpret_cast<const ulonglong2*>(tab + (p * 16 + v) * 4);
+        const ulonglong2 lo = __ldg(e), hi = __ldg(e + 1);
+        r0 ^= lo.x; r1 ^= lo.y; r2 ^= hi.x; r3 ^= hi.y;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        r0 ^= __shfl_xor_sync(0xffffffffu, r0, o);
-        r1 ^= __shfl_xor_sync(0xffffffffu, r1, o);
-        r2 ^= __shfl_xor_sync(0xffffffffu, r2, o);
-        r3 ^= __shfl_xor_sync(0xffffffffu, r3, o);
-    }
-    y[0] = r0; y[1] = r1; y[2] = r2; y[3] = r3;
-}
-
-__device__ __forceinline__ void thread_matvec(const std::uint64_t* __restrict__ m, const std::uint64_t* x,
-                                              std::uint64_t* y) {
-    std::uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-#pragma unroll 1
-    for (int w = 0; w < 4; ++w) {
-        std::uint64_t bits = x[w];
-        while (bits) {
-            const int b = __ffsll(static_cast<long long>(bits)) - 1;
-            bits &= bits - 1;
-            const std::uint64_t* col = m + (w * 64 + b) * 4;
-            r0 ^= __ldg(col); r1 ^= __ldg(col + 1); r2 ^= __ldg(col + 2); r3 ^= __ldg(col + 3);
-        }
-    }
-    y[0] = r0; y[1] = r1; y[2] = r2; y[3] = r3;
+    s0 = r0; s1 = r1; s2 = r2; s3 = r3;
 }
 
 struct GenArgs {
-    std::uint64_t s0[4];       // stream state at u64 index 0
+    std::uint64_t s0[4];       // state at u64 index 2 * floor(g0 / 2) (jumped on the host)
     std::uint64_t g0;          // first gaussian index written
     std::int64_t count;        // gaussians written
     std::int64_t rows;         // output matrix rows (column-major fill order)
+    int ppt;                   // pairs per thread (power of two >= 8)
     MatView out;
 };
 
-// The jump matrices T^(64 * 2^j), j < 8, used by the in-CTA doubling scan are staged
-// in shared memory (64 KB); the CTA anchor jumps from the call's base state (computed
-// on the host) by blockIdx * 2^14 u64 steps, i.e. only the bits of blockIdx.
-constexpr int kScanLevels = 8;  // 2^8 = kGenThreads
-constexpr int kGenSmem = kScanLevels * 1024 * 8 + kGenThreads * 4 * 8;
-
-__device__ __forceinline__ void smem_matvec(const std::uint64_t* m, const std::uint64_t* x, std::uint64_t* y) {
-    std::uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-        std::uint64_t bits = x[w];
-        while (bits) {
-            const int b = __ffsll(static_cast<long long>(bits)) - 1;
-            bits &= bits - 1;
-            const std::uint64_t* col = m + (w * 64 + b) * 4;
-            r0 ^= col[0]; r1 ^= col[1]; r2 ^= col[2]; r3 ^= col[3];
-        }
-    }
-    y[0] = r0; y[1] = r1; y[2] = r2; y[3] = r3;
-}
-
+// Thread g (global index) starts at u64 offset 16 g from the call's base state: one
+// table mat-vec T^(d * 16^(pos+1)) per non-zero hex digit d of g (<= 6, independent of
+// any other thread: no shared memory, no barrier), then 8 sequential Box-Muller pairs.
 __global__ void __launch_bounds__(kGenThreads)
-gaussian_kernel(GenArgs a, const std::uint64_t* __restrict__ tables) {
-    extern __shared__ std::uint64_t gsm[];
-    std::uint64_t* stab = gsm;                              // kScanLevels x 1024 words
-    std::uint64_t (*st)[4] = reinterpret_cast<std::uint64_t (*)[4]>(gsm + kScanLevels * 1024);
+gaussian_kernel(GenArgs a, const std::uint64_t* __restrict__ dig) {
+    const std::uint64_t gt = static_cast<std::uint64_t>(blockIdx.x) * kGenThreads + threadIdx.x;
+    const std::uint64_t unit = gt * static_cast<std::uint64_t>(a.ppt / kMinPairsPerThread);  // in 16-u64 units
+    std::uint64_t s0 = a.s0[0], s1 = a.s0[1], s2 = a.s0[2], s3 = a.s0[3];
+#pragma unroll 1
+    for (int pos = 0; pos < kDigitPositions; ++pos) {
+        const unsigned d = static_cast<unsigned>(unit >> (4 * pos)) & 15u;
+        if (d) nib_matvec(dig + static_cast<std::size_t>(pos * 15 + d - 1) * 4096, s0, s1, s2, s3);
+    }
+    std::uint64_t s[4] = {s0, s1, s2, s3};
     const std::uint64_t p_first = a.g0 >> 1;
     const std::uint64_t g_end = a.g0 + static_cast<std::uint64_t>(a.count);  // exclusive
-    const std::uint64_t cta_pair0 = p_first + static_cast<std::uint64_t>(blockIdx.x) * kGenThreads * kPairsPerThread;
-    for (int i = threadIdx.x; i < kScanLevels * 1024; i += kGenThreads)
-        stab[i] = __ldg(tables + static_cast<std::size_t>(kThreadJumpLevel0) * 1024 + i);
-    // CTA anchor: T^(2 * 8192 * blockIdx) * base, by warp 0 (levels 14 + bit of blockIdx).
-    if (threadIdx.x < 32) {
-        std::uint64_t x[4] = {a.s0[0], a.s0[1], a.s0[2], a.s0[3]};
-        unsigned e = blockIdx.x;
-        int k = kThreadJumpLevel0 + kScanLevels;
-        while (e) {
-            if (e & 1u) {
-                std::uint64_t y[4];
-                warp_matvec(tables + static_cast<std::size_t>(k) * 1024, x, y);
-                x[0] = y[0]; x[1] = y[1]; x[2] = y[2]; x[3] = y[3];
-            }
-            e >>= 1;
-            ++k;
-        }
-        if (threadIdx.x == 0) { st[0][0] = x[0]; st[0][1] = x[1]; st[0][2] = x[2]; st[0][3] = x[3]; }
-    }
-    __syncthreads();
-    // Doubling scan: st[t] = T^(64 t) st[0].
-#pragma unroll 1
-    for (int j = 0; j < kScanLevels; ++j) {
-        const int t = threadIdx.x;
-        if (t >= (1 << j) && t < (2 << j)) smem_matvec(stab + j * 1024, st[t - (1 << j)], st[t]);
-        __syncthreads();
-    }
-    std::uint64_t s[4] = {st[threadIdx.x][0], st[threadIdx.x][1], st[threadIdx.x][2], st[threadIdx.x][3]};
-    const std::uint64_t pair0 = cta_pair0 + static_cast<std::uint64_t>(threadIdx.x) * kPairsPerThread;
+    const std::uint64_t pair0 = p_first + gt * static_cast<std::uint64_t>(a.ppt);
     constexpr double kTwoPi = 2.0 * 3.141592653589793;  // (2.0 * pi) as in rng.cpp:63
 #pragma unroll 1
-    for (int q = 0; q < kPairsPerThread; ++q) {
+    for (int q = 0; q < a.ppt; ++q) {
         const std::uint64_t p = pair0 + q;
         const std::uint64_t g = 2 * p;
         if (g >= g_end) break;
@@ -244,9 +182,32 @@ std::uint64_t host_next_u64(std::uint64_t (&s)[4]) { return xoshiro_next(s); }
 
 const std::uint64_t* RngTables::device() {
     if (!dev_) {
+        // digit tables: for hex position pos (thread-index digit) and value d = 1..15, the
+        // nibble table of T^(d * 16^(pos+1)) (a thread covers 16 u64).
         const auto& h = jump_tables_host();
-        QB_CUDA(cudaMalloc(&dev_, h.size() * sizeof(std::uint64_t)));
-        QB_CUDA(cudaMemcpy(dev_, h.data(), h.size() * sizeof(std::uint64_t), cudaMemcpyHostToDevice));
+        auto level = [&](int k) { return Mat256(h.begin() + static_cast<std::size_t>(k) * 1024,
+                                                h.begin() + static_cast<std::size_t>(k + 1) * 1024); };
+        std::vector<std::uint64_t> tabs(static_cast<std::size_t>(kDigitPositions) * 15 * 4096);
+        for (int pos = 0; pos < kDigitPositions; ++pos) {
+            Mat256 m;
+            for (int d = 1; d <= 15; ++d) {
+                // T^(d * 2^(4 + 4 pos)) = T^(2^(4+4pos)) * T^((d-1) * 2^(4+4pos))
+                m = d == 1 ? level(4 + 4 * pos) : matmul_host(level(4 + 4 * pos), m);
+                std::uint64_t* t = &tabs[static_cast<std::size_t>(pos * 15 + d - 1) * 4096];
+                for (int p = 0; p < 64; ++p)
+                    for (int v = 0; v < 16; ++v) {
+                        std::uint64_t r[4] = {0, 0, 0, 0};
+                        for (int bit = 0; bit < 4; ++bit)
+                            if ((v >> bit) & 1) {
+                                const std::uint64_t* col = &m[(p * 4 + bit) * 4];
+                                for (int w = 0; w < 4; ++w) r[w] ^= col[w];
+                            }
+                        std::memcpy(t + (p * 16 + v) * 4, r, sizeof(r));
+                    }
+            }
+        }
+        QB_CUDA(cudaMalloc(&dev_, tabs.size() * sizeof(std::uint64_t)));
+        QB_CUDA(cudaMemcpy(dev_, tabs.data(), tabs.size() * sizeof(std::uint64_t), cudaMemcpyHostToDevice));
     }
     return dev_;
 }
@@ -284,14 +245,15 @@ void gaussian_fill(cudaStream_t st, RngTables& tables, std::uint64_t seed, std::
     const std::uint64_t p_first = g0 >> 1;
     const std::uint64_t p_last = (g0 + count - 1) >> 1;
     const std::uint64_t pairs = p_last - p_first + 1;
-    const std::uint64_t per_cta = static_cast<std::uint64_t>(kGenThreads) * kPairsPerThread;
+    // enough threads to fill the GPU (~2 waves of 148 x 2048), then longer runs per thread
+    int ppt = kMinPairsPerThread;
+    while (ppt < 64 && pairs / static_cast<std::uint64_t>(ppt) > 40000) ppt *= 2;
+    a.ppt = ppt;
+    const std::uint64_t per_cta = static_cast<std::uint64_t>(kGenThreads) * ppt;
+    if ((pairs + static_cast<std::uint64_t>(ppt) - 1) / ppt / kMinPairsPerThread * ppt >= (1ULL << (4 * kDigitPositions)))
+        throw QbError(kDimensionError, "gaussian: request too large for one call");
     const unsigned grid = static_cast<unsigned>((pairs + per_cta - 1) / per_cta);
-    static bool configured = false;
-    if (!configured) {
-        QB_CUDA(cudaFuncSetAttribute(gaussian_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGenSmem));
-        configured = true;
-    }
-    gaussian_kernel<<<grid, kGenThreads, kGenSmem, st>>>(a, tables.device());
+    gaussian_kernel<<<grid, kGenThreads, 0, st>>>(a, tables.device());
     QB_LAUNCH_CHECK();
 }
 
