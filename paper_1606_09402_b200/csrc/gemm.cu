@@ -284,6 +284,7 @@ bool dispatch_ws(int fam, cudaStream_t st, const MatView& a, const MatView& b, d
     if (fam == 0) launch_ws<128, 128, 32, 2, 4, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
     else if (fam == 1) launch_ws<128, 64, 32, 4, 2, 4, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
     else if (fam == 3) launch_ws<128, 56, 32, 8, 1, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
+    else if (fam == 4) launch_ws<128, 80, 32, 4, 2, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
     else launch_ws<64, 32, 32, 2, 2, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
     return true;
 }
@@ -315,7 +316,7 @@ void launch_cfg(cudaStream_t st, const MatView& a, const MatView& b, double* c, 
 // Tile families. "wide": 128x128 CTA tiles (warp 64x32) for the passes over A at
 // large widths; "skinny": 128x64 (warp 32x32) for widths ~50-100; "narrow":
 // 64x32 for the thinnest products (b = 20, Gram-like outputs).
-enum class Family { kWide, kSkinny, kNarrow, kSkinny56 };
+enum class Family { kWide, kSkinny, kNarrow, kSkinny56, kWide80 };
 
 template <Family F, bool AR, bool BR, int VEC>
 void launch_family(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc,
@@ -330,6 +331,9 @@ void launch_family(cudaStream_t st, const MatView& a, const MatView& b, double* 
                                                        alpha, beta, partial, flags);
     else if constexpr (F == Family::kSkinny)
         launch_cfg<128, 64, 16, 4, 2, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
+                                                      alpha, beta, partial, flags);
+    else if constexpr (F == Family::kWide80)  // widths that are multiples of 80 (l = 400): no 128-column padding
+        launch_cfg<128, 80, 32, 4, 2, 3, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
                                                       alpha, beta, partial, flags);
     else if constexpr (F == Family::kSkinny56)  // b = 50-56: 7 n8 tiles per warp, no 64-column padding
         launch_cfg<128, 56, 32, 8, 1, 4, AR, BR, VEC>(st, a, b, c, ldc, c_row, M, N, K, splits, klen,
@@ -387,7 +391,12 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     }
     Family fam;
     int bm, bn, bk;
-    if (N >= 96) { fam = Family::kWide; bm = 128; bn = 128; bk = QB_WIDE_BK; }
+    // wide widths: 128-column tiles unless 80-column tiles pad less (e.g. l = 400: 4 x 128 = 512
+    // vs 5 x 80 = 400)
+    // (A column-major only: the A^T passes measured faster on 128-wide tiles)
+    const bool use80 = N >= 96 && !a.rowmajor && 10 * round_up(N, 80) < 9 * round_up(N, 128);
+    if (use80) { fam = Family::kWide80; bm = 128; bn = 80; bk = 32; }
+    else if (N >= 96) { fam = Family::kWide; bm = 128; bn = 128; bk = QB_WIDE_BK; }
     else if (N > 48 && N <= 56) { fam = Family::kSkinny56; bm = 128; bn = 56; bk = 32; }
     else if (N > 32) { fam = Family::kSkinny; bm = 128; bn = 64; bk = 16; }
     else { fam = Family::kNarrow; bm = 64; bn = 32; bk = 32; }
@@ -398,7 +407,8 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     }();
     // Warp-specialised TMA path where it measured faster (tools/gemm_bench.py): A column-major
     // (long bulk segments), or both operands row-major with wide tiles (A^T G passes).
-    const bool ws_path = use_ws && vec2 && (!a.rowmajor || (b.rowmajor && N >= 96));
+    const bool tiny = false;  // (a no-split plain path for tiny products measured slower: split-K keeps SMs busy)
+    const bool ws_path = use_ws && vec2 && !tiny && (!a.rowmajor || (b.rowmajor && N >= 96));
     if (ws_path) bk = 32;  // the warp-specialised kernels use BK = 32 in every family
     if (ws_path && fam == Family::kSkinny56) bn = 64;
     const std::int64_t tiles = ceil_div(M, bm) * ceil_div(N, bn);
@@ -406,7 +416,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     // Resident CTAs per SM ~1 for the wide/skinny tiles, ~3 for narrow.
     const std::int64_t want = (fam == Family::kNarrow ? 3 : 1) * static_cast<std::int64_t>(sms);
     int splits = 1;
-    if (tiles < want) {
+    if (tiles < want && !tiny) {
         const std::int64_t max_by_k = std::max<std::int64_t>(1, K / (4 * bk));  // >= 4 k-tiles/split
         const std::int64_t cap = (M * N <= 65536) ? 512 : 64;  // small outputs (Grams): deep split-K
         // floor: tiles * splits must not exceed one wave of resident CTAs (a 2nd partial wave
@@ -421,7 +431,8 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     if (ws_path) {
         // warp-specialised TMA/mbarrier pipeline (gemm_ws.cuh)
         // the 56-wide tile measured slower than 64 on the TMA path (tools/gemm_bench.py): use 64 there
-        const int famid = fam == Family::kWide ? 0 : (fam == Family::kSkinny || fam == Family::kSkinny56) ? 1 : 2;
+        const int famid = fam == Family::kWide ? 0 : fam == Family::kWide80 ? 4
+                          : (fam == Family::kSkinny || fam == Family::kSkinny56) ? 1 : 2;
         {
             if (a.rowmajor) {
                 if (b.rowmajor) dispatch_ws<true, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);
@@ -439,6 +450,10 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
             break;
         case Family::kSkinny:
             dispatch_layout<Family::kSkinny>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K,
+                                             splits, klen, alpha, beta, partial, vec2, flags);
+            break;
+        case Family::kWide80:
+            dispatch_layout<Family::kWide80>(st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K,
                                              splits, klen, alpha, beta, partial, vec2, flags);
             break;
         case Family::kSkinny56:

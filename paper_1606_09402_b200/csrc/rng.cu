@@ -15,6 +15,7 @@
 // and runs the generator over 8 pairs. The integer stream is bit-identical to the
 // reference; log/sin/cos come from CUDA's libdevice.
 
+#include <algorithm>
 #include <array>
 #include <cstring>
 #include <mutex>
@@ -124,6 +125,7 @@ struct GenArgs {
     std::int64_t count;        // gaussians written
     std::int64_t rows;         // output matrix rows (column-major fill order)
     int ppt;                   // pairs per thread (power of two >= 8)
+    std::int64_t e_off;        // output element index of gaussian g0
     MatView out;
 };
 
@@ -159,11 +161,11 @@ gaussian_kernel(GenArgs a, const std::uint64_t* __restrict__ dig) {
         double sn, cs;
         sincos(theta, &sn, &cs);
         if (g >= a.g0) {
-            const std::int64_t e = static_cast<std::int64_t>(g - a.g0);
+            const std::int64_t e = a.e_off + static_cast<std::int64_t>(g - a.g0);
             *a.out.at(e % a.rows, e / a.rows) = __dmul_rn(r, cs);
         }
         if (g + 1 >= a.g0 && g + 1 < g_end) {
-            const std::int64_t e = static_cast<std::int64_t>(g + 1 - a.g0);
+            const std::int64_t e = a.e_off + static_cast<std::int64_t>(g + 1 - a.g0);
             *a.out.at(e % a.rows, e / a.rows) = __dmul_rn(r, sn);
         }
     }
@@ -216,14 +218,13 @@ RngTables::~RngTables() {
     if (dev_) cudaFree(dev_);
 }
 
-void gaussian_fill(cudaStream_t st, RngTables& tables, std::uint64_t seed, std::uint64_t stream,
-                   std::uint64_t g0, const MatView& out) {
-    const std::int64_t count = out.rows * out.cols;
-    if (count == 0) return;
+namespace {
+void gaussian_chunk(cudaStream_t st, RngTables& tables, std::uint64_t seed, std::uint64_t stream, std::uint64_t g0,
+                    std::int64_t count, std::int64_t e_off, const MatView& out) {
     GenArgs a{};
     stream_origin(seed, stream, a.s0);
     {
-        // base state of this call: T^(2 * p_first) s0, jumped on the host
+        // base state of this call: T^(2 * floor(g0 / 2)) s0, jumped on the host
         const auto& tab = jump_tables_host();
         std::uint64_t e = 2 * (g0 >> 1);
         int k = 0;
@@ -241,20 +242,29 @@ void gaussian_fill(cudaStream_t st, RngTables& tables, std::uint64_t seed, std::
     a.g0 = g0;
     a.count = count;
     a.rows = out.rows;
+    a.e_off = e_off;
     a.out = out;
-    const std::uint64_t p_first = g0 >> 1;
-    const std::uint64_t p_last = (g0 + count - 1) >> 1;
-    const std::uint64_t pairs = p_last - p_first + 1;
-    // enough threads to fill the GPU (~2 waves of 148 x 2048), then longer runs per thread
+    const std::uint64_t pairs = ((g0 + count - 1) >> 1) - (g0 >> 1) + 1;
+    // enough threads to fill the GPU, then longer runs per thread
     int ppt = kMinPairsPerThread;
     while (ppt < 64 && pairs / static_cast<std::uint64_t>(ppt) > 40000) ppt *= 2;
     a.ppt = ppt;
     const std::uint64_t per_cta = static_cast<std::uint64_t>(kGenThreads) * ppt;
-    if ((pairs + static_cast<std::uint64_t>(ppt) - 1) / ppt / kMinPairsPerThread * ppt >= (1ULL << (4 * kDigitPositions)))
-        throw QbError(kDimensionError, "gaussian: request too large for one call");
     const unsigned grid = static_cast<unsigned>((pairs + per_cta - 1) / per_cta);
     gaussian_kernel<<<grid, kGenThreads, 0, st>>>(a, tables.device());
     QB_LAUNCH_CHECK();
+}
+}  // namespace
+
+void gaussian_fill(cudaStream_t st, RngTables& tables, std::uint64_t seed, std::uint64_t stream,
+                   std::uint64_t g0, const MatView& out) {
+    const std::int64_t count = out.rows * out.cols;
+    // one launch covers < 16^6 thread-units of 8 pairs; larger requests are chunked
+    const std::int64_t chunk = std::int64_t(1) << 26;  // gaussians per launch (even)
+    for (std::int64_t done = 0; done < count; done += chunk) {
+        const std::int64_t c = std::min(chunk, count - done);
+        gaussian_chunk(st, tables, seed, stream, g0 + static_cast<std::uint64_t>(done), c, done, out);
+    }
 }
 
 }  // namespace qbgpu
