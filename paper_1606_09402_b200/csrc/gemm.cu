@@ -15,9 +15,12 @@
 
 #include "gemm.cuh"
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #ifndef QB_WIDE_BK
 #define QB_WIDE_BK 32
@@ -256,6 +259,37 @@ splitk_reduce_kernel(const double* __restrict__ partial, int splits, int M, int 
 
 #include "gemm_ws.cuh"
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        QB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess) throw QbError(kError, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
+// 2-D FP64 tensor map over a strided matrix: dim0 (contiguous) of extent inner, dim1 of
+// extent outer with a row pitch of ld doubles; box {box0, box1}; zero fill out of range.
+void make_tmap(CUtensorMap* map, const double* base, std::int64_t inner, std::int64_t outer, std::int64_t ld,
+               int box0, int box1) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(std::max<std::int64_t>(inner, 1)),
+                                static_cast<cuuint64_t>(std::max<std::int64_t>(outer, 1))};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box0), static_cast<cuuint32_t>(box1)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_tiled()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw QbError(kError, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int NP>
 void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc, bool c_row, int M,
                int N, int K, int splits, int klen, double alpha, double beta, double* partial, int flags) {
@@ -268,8 +302,14 @@ void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, s
         QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (WM * WN + NP) * 32, smem));
         if (per_sm < 1) per_sm = 1;
     }
-    WsArgs p{a.p, a.ld, b.p, b.ld, c, ldc, c_row ? 1 : 0, M, N, K, klen, splits,
-             static_cast<int>(ceil_div(M, BM)), static_cast<int>(ceil_div(N, BN)), flags, alpha, beta, partial};
+    WsArgs p{};
+    p.A = a.p; p.lda = a.ld; p.B = b.p; p.ldb = b.ld; p.C = c; p.ldc = ldc; p.c_row = c_row ? 1 : 0;
+    p.M = M; p.N = N; p.K = K; p.k_split_len = klen; p.splits = splits;
+    p.tiles_m = static_cast<int>(ceil_div(M, BM)); p.tiles_n = static_cast<int>(ceil_div(N, BN));
+    p.flags = flags; p.alpha = alpha; p.beta = beta; p.partial = partial;
+    if (AR) make_tmap(&p.tmA, a.p, K, M, a.ld, T::LDA, BM);               // A(i,k) at A + i*lda + k
+    if (BR && BN < 64) make_tmap(&p.tmB, b.p, N, K, b.ld, T::LDB, BK);    // B(k,j) at B + k*ldb + j
+    if (!BR) make_tmap(&p.tmB, b.p, K, N, b.ld, T::LDB, BN);              // B(k,j) at B + k + j*ldb
     const std::int64_t items = static_cast<std::int64_t>(p.tiles_m) * p.tiles_n * splits;
     const int grid = static_cast<int>(std::min<std::int64_t>(items, static_cast<std::int64_t>(per_sm) * gemm_num_sms()));
     kern<<<grid, (WM * WN + NP) * 32, smem, st>>>(p);
@@ -394,7 +434,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     // wide widths: 128-column tiles unless 80-column tiles pad less (e.g. l = 400: 4 x 128 = 512
     // vs 5 x 80 = 400)
     // (A column-major only: the A^T passes measured faster on 128-wide tiles)
-    const bool use80 = N >= 96 && !a.rowmajor && 10 * round_up(N, 80) < 9 * round_up(N, 128);
+    const bool use80 = N >= 96 && 10 * round_up(N, 80) < 9 * round_up(N, 128);
     if (use80) { fam = Family::kWide80; bm = 128; bn = 80; bk = 32; }
     else if (N >= 96) { fam = Family::kWide; bm = 128; bn = 128; bk = QB_WIDE_BK; }
     else if (N > 48 && N <= 56) { fam = Family::kSkinny56; bm = 128; bn = 56; bk = 32; }
@@ -408,9 +448,9 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     // Warp-specialised TMA path where it measured faster (tools/gemm_bench.py): A column-major
     // (long bulk segments), or both operands row-major with wide tiles (A^T G passes).
     const bool tiny = false;  // (a no-split plain path for tiny products measured slower: split-K keeps SMs busy)
-    const bool ws_path = use_ws && vec2 && !tiny && (!a.rowmajor || (b.rowmajor && N >= 96));
+    const bool ws_path = use_ws && vec2 && !tiny;
     if (ws_path) bk = 32;  // the warp-specialised kernels use BK = 32 in every family
-    if (ws_path && fam == Family::kSkinny56) bn = 64;
+    if (ws_path && fam == Family::kSkinny56 && !a.rowmajor) bn = 64;
     const std::int64_t tiles = ceil_div(M, bm) * ceil_div(N, bn);
     const int sms = gemm_num_sms();
     // Resident CTAs per SM ~1 for the wide/skinny tiles, ~3 for narrow.
@@ -432,7 +472,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
         // warp-specialised TMA/mbarrier pipeline (gemm_ws.cuh)
         // the 56-wide tile measured slower than 64 on the TMA path (tools/gemm_bench.py): use 64 there
         const int famid = fam == Family::kWide ? 0 : fam == Family::kWide80 ? 4
-                          : (fam == Family::kSkinny || fam == Family::kSkinny56) ? 1 : 2;
+                          : fam == Family::kSkinny56 ? (a.rowmajor ? 3 : 1) : fam == Family::kSkinny ? 1 : 2;
         {
             if (a.rowmajor) {
                 if (b.rowmajor) dispatch_ws<true, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);

@@ -133,7 +133,17 @@ __device__ __forceinline__ unsigned operand_bulk_bytes(const double* __restrict_
     return bytes;
 }
 
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
 struct WsArgs {
+    CUtensorMap tmA;  // used when A's contiguous segments are short (A row-major)
+    CUtensorMap tmB;  // used when B's contiguous segments are short (B column-major, or BN < 64)
     const double* A;
     std::int64_t lda;
     const double* B;
@@ -146,7 +156,7 @@ struct WsArgs {
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int NP>
-__global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(WsArgs p) {
+__global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const __grid_constant__ WsArgs p) {
     using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
     constexpr int NC = WM * WN;  // consumer warps
     extern __shared__ __align__(128) double smem[];
@@ -158,7 +168,7 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(WsArgs
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1 + 32 * NP);  // expect_tx arrive + one cp.async noinc arrive per producer lane
+            mbar_init(&full[s], 1);  // one arrive carrying expect_tx (bulk + tensor TMA bytes)
             mbar_init(&empty[s], NC);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -188,8 +198,12 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(WsArgs
                                          : p.A + m0 + static_cast<std::int64_t>(k0) * p.lda;
                 const double* b_src = BR ? p.B + static_cast<std::int64_t>(k0) * p.ldb + n0
                                          : p.B + k0 + static_cast<std::int64_t>(n0) * p.ldb;
-                // Long segments (A col-major: BM rows; B row-major: BN cols) go by TMA bulk
-                // copy; short ones (length BK along K) by cp.async.
+                // Long contiguous segments (A column-major: BM rows; B row-major: BN >= 64
+                // columns) go by per-row TMA bulk copies into the padded layout; short ones
+                // (BK along the reduction dimension, or BN < 64) by ONE 2-D tensor TMA per
+                // operand whose box is the padded row length (the extra 4 doubles per row are
+                // an over-read that keeps the layout bank-conflict free); out-of-range
+                // elements are zero-filled by the TMA unit.
                 constexpr bool A_BULK = !AR;
                 constexpr bool B_BULK = BR && BN >= 64;
                 // 1) generic pass for bulk operands: K-tail zero segments and unaligned/odd segments
@@ -197,7 +211,7 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(WsArgs
                     produce_operand<BK, BM, T::LDA>(a_dst, a_src, p.lda, m0, p.M, k0, k_end, false, pt, false, nullptr, PT);
                 if constexpr (B_BULK)
                     produce_operand<BK, BN, T::LDB>(b_dst, b_src, p.ldb, n0, p.N, k0, k_end, false, pt, false, nullptr, PT);
-                // 2) expected bulk bytes, then one arrive carrying expect_tx
+                // 2) expected bytes, then one arrive carrying expect_tx
                 unsigned bytes = 0;
                 if constexpr (A_BULK) bytes += operand_bulk_bytes<BK, BM>(a_src, p.lda, m0, p.M, k0, k_end, pt, PT);
                 if constexpr (B_BULK) bytes += operand_bulk_bytes<BK, BN>(b_src, p.ldb, n0, p.N, k0, k_end, pt, PT);
@@ -212,6 +226,8 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(WsArgs
                     for (int q = 0; q < NP; ++q) bytes += s_bytes[q];
                     asm volatile("bar.sync 1, %0;\n" ::"n"(NP * 32) : "memory");
                 }
+                if constexpr (!A_BULK) bytes += T::A_STAGE * 8;   // full box, zero-filled where out of range
+                if constexpr (!B_BULK) bytes += T::B_STAGE * 8;
                 fence_proxy_async();
                 __syncwarp();
                 if (pt == 0) mbar_arrive_tx(&full[stage], bytes);
@@ -220,15 +236,14 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(WsArgs
                 // 3) copies
                 if constexpr (A_BULK)
                     produce_operand<BK, BM, T::LDA>(a_dst, a_src, p.lda, m0, p.M, k0, k_end, false, pt, true, &full[stage], PT);
-                else
-                    produce_async<BM, BK, T::LDA, false>(a_dst, a_src, p.lda, k0, k_end, m0, p.M, pt, PT);
+                else if (pt == 0)
+                    tma_2d(a_dst, &p.tmA, k0, m0, &full[stage]);          // box {LDA, BM} at (k0, m0)
                 if constexpr (B_BULK)
                     produce_operand<BK, BN, T::LDB>(b_dst, b_src, p.ldb, n0, p.N, k0, k_end, false, pt, true, &full[stage], PT);
-                else if constexpr (BR)
-                    produce_async<BK, BN, T::LDB, true>(b_dst, b_src, p.ldb, n0, p.N, k0, k_end, pt, PT);
-                else
-                    produce_async<BN, BK, T::LDB, false>(b_dst, b_src, p.ldb, k0, k_end, n0, p.N, pt, PT);
-                cp_async_arrive_noinc(&full[stage]);  // this lane's cp.asyncs (possibly none)
+                else if (pt == 0) {
+                    if constexpr (BR) tma_2d(b_dst, &p.tmB, n0, k0, &full[stage]);   // box {LDB, BK} at (n0, k0)
+                    else tma_2d(b_dst, &p.tmB, k0, n0, &full[stage]);                // box {LDB, BN} at (k0, n0)
+                }
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }

@@ -240,3 +240,29 @@ def test_determinism(ctx):
     r1 = qbfac.rand_qb_fp(qbfac.MatrixHandle.dense(a, ctx), eps, 10, 1, 100, qbfac.RngStream(3))
     r2 = qbfac.rand_qb_fp(qbfac.MatrixHandle.dense(a, ctx), eps, 10, 1, 100, qbfac.RngStream(3))
     assert np.array_equal(r1.Q, r2.Q) and np.array_equal(r1.B, r2.B)
+
+
+def test_cfg3_full_size_vs_oracle_golden(ctx):
+    """BASELINE config 3 at full size (CSR 1e5 x 5e4, 5M nnz, b=50, P=1, eps=0.5 rel, cap 1000)
+    against the oracle's result (tests/golden/cfg3_full_oracle.json, tools/oracle_cfg3.py;
+    220 s on one CPU core)."""
+    import json
+    import os
+    import sys
+
+    from paper_1606_09402_b200 import matgen, qbfac
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "tools"))
+    from run_configs import csr_explicit_error
+    gold = json.load(open(os.path.join(root, "tests", "golden", "cfg3_full_oracle.json")))
+    csr = matgen.csr_uniform(100000, 50000, 50, seed=3)
+    eps = 0.5 * float(np.sqrt((csr[4] ** 2).sum()))
+    got = qbfac.rand_qb_ei(qbfac.MatrixHandle.csr(*csr, ctx=ctx), qbfac.StopRule.fixed_precision(eps), 50, 1,
+                           qbfac.RngStream(42), max_rank=1000)
+    assert got.rank == gold["rank"] and got.passes == gold["passes"] and got.terminated_by == gold["terminated_by"]
+    assert abs(got.error_indicator - gold["E"]) <= 1e-10 * gold["E"] + 2e-13 * gold["norm_a_sq"]
+    s = np.linalg.svd(got.B, compute_uv=False)
+    sr = np.asarray(gold["sigma"])
+    assert np.max(np.abs(s - sr) / sr) <= 1e-10
+    err = csr_explicit_error(csr, got.Q, got.B)
+    assert abs(err - gold["explicit_error"]) <= 1e-10 * gold["explicit_error"]
