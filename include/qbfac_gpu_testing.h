@@ -6,6 +6,7 @@
  *   qbfac_gpu_test_gemm      the DMMA GEMM behind every dense product
  *                            (replaces kernels::gemm_nn / gemm_tn, kernels_drivers.cpp:21-65)
  *   qbfac_gpu_test_chol      the in-CTA Cholesky + inverse used by CholQR
+ *   qbfac_gpu_test_chol_wide the blocked (cooperative) Cholesky + inverse of the wide CholQR
  *   qbfac_gpu_test_householder  the Householder panel QR (orth_qr, qr.hpp:15-18)
  *   qbfac_gpu_test_orth_wide the power step's orth() of a wide sketch (CholQR2 or BCGS2)
  *   qbfac_gpu_test_colsumsq  per-column sums of squares (the indicator's row norms)
@@ -29,6 +30,8 @@ int qbfac_gpu_test_gemm(qbfac_gpu_ctx* ctx, double alpha, const double* a, int64
                         int64_t ldc, int c_row);
 /* b x b Gram (col-major, ld b) -> R, R^{-1} (col-major, ld b); returns breakdown flag in *status. */
 int qbfac_gpu_test_chol(qbfac_gpu_ctx* ctx, const double* g, int b, double* r, double* rinv, int* status);
+/* blocked Cholesky + inverse of an l x l Gram (col-major, upper triangle read and overwritten), one cooperative launch */
+int qbfac_gpu_test_chol_wide(qbfac_gpu_ctx* ctx, double* g, int l, double* r, double* rinv, int* breakdown);
 /* Householder QR of a column-major m x b panel in place (Q overwrites y); R col-major ld b. */
 int qbfac_gpu_test_householder(qbfac_gpu_ctx* ctx, double* y, int64_t m, int b, int64_t ld, double* r);
 /* Orthonormalise a wide row-major rows x l panel in place (CholQR2 / BCGS2, the power step's orth). */

@@ -334,6 +334,23 @@ int qbfac_gpu_test_chol(qbfac_gpu_ctx* ctx, const double* g, int b, double* r, d
     });
 }
 
+int qbfac_gpu_test_chol_wide(qbfac_gpu_ctx* ctx, double* g, int l, double* r, double* rinv, int* breakdown) {
+    return guard(ctx, [&] {
+        auto& cx = *ctx->c;
+        const int nt = (l + 63) / 64;
+        qbgpu::DBuf st(static_cast<std::size_t>(nt) * 4, cx.st);
+        QB_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * l * l, cx.st));
+        QB_CUDA(cudaMemsetAsync(rinv, 0, sizeof(double) * l * l, cx.st));
+        auto* stats = reinterpret_cast<qbgpu::SmallStatus*>(st.p);
+        qbgpu::chol_wide(cx.st, g, l, l, r, rinv, l, stats);
+        std::vector<qbgpu::SmallStatus> hs(static_cast<std::size_t>(nt));
+        QB_CUDA(cudaMemcpyAsync(hs.data(), stats, sizeof(qbgpu::SmallStatus) * nt, cudaMemcpyDeviceToHost, cx.st));
+        QB_CUDA(cudaStreamSynchronize(cx.st));
+        *breakdown = 0;
+        for (const auto& s : hs) *breakdown |= s.breakdown;
+    });
+}
+
 int qbfac_gpu_test_householder(qbfac_gpu_ctx* ctx, double* y, int64_t m, int b, int64_t ld, double* r) {
     return guard(ctx, [&] {
         auto& cx = *ctx->c;

@@ -31,6 +31,16 @@ namespace qbgpu {
 
 namespace {
 
+// Output tiles of an M x N product; with kGemmUpperC only those reaching the diagonal
+// or above (tile row mt starts at tile column mt*bm/bn).
+std::int64_t output_tiles(std::int64_t M, std::int64_t N, int bm, int bn, int flags) {
+    const std::int64_t tm = ceil_div(M, bm), tn = ceil_div(N, bn);
+    if (!(flags & kGemmUpperC)) return tm * tn;
+    std::int64_t t = 0;
+    for (std::int64_t mt = 0; mt < tm; ++mt) t += std::max<std::int64_t>(0, tn - (mt * bm) / bn);
+    return t;
+}
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -307,10 +317,11 @@ void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, s
     p.M = M; p.N = N; p.K = K; p.k_split_len = klen; p.splits = splits;
     p.tiles_m = static_cast<int>(ceil_div(M, BM)); p.tiles_n = static_cast<int>(ceil_div(N, BN));
     p.flags = flags; p.alpha = alpha; p.beta = beta; p.partial = partial;
+    p.tiles = static_cast<int>(output_tiles(M, N, BM, BN, flags));
     if (AR) make_tmap(&p.tmA, a.p, K, M, a.ld, T::LDA, BM);               // A(i,k) at A + i*lda + k
     if (BR && BN < 64) make_tmap(&p.tmB, b.p, N, K, b.ld, T::LDB, BK);    // B(k,j) at B + k*ldb + j
     if (!BR) make_tmap(&p.tmB, b.p, K, N, b.ld, T::LDB, BN);              // B(k,j) at B + k + j*ldb
-    const std::int64_t items = static_cast<std::int64_t>(p.tiles_m) * p.tiles_n * splits;
+    const std::int64_t items = static_cast<std::int64_t>(p.tiles) * splits;
     const int grid = static_cast<int>(std::min<std::int64_t>(items, static_cast<std::int64_t>(per_sm) * gemm_num_sms()));
     kern<<<grid, (WM * WN + NP) * 32, smem, st>>>(p);
     QB_LAUNCH_CHECK();
@@ -451,7 +462,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     const bool ws_path = use_ws && vec2 && !tiny;
     if (ws_path) bk = 32;  // the warp-specialised kernels use BK = 32 in every family
     if (ws_path && fam == Family::kSkinny56 && !a.rowmajor) bn = 64;
-    const std::int64_t tiles = ceil_div(M, bm) * ceil_div(N, bn);
+    const std::int64_t tiles = output_tiles(M, N, bm, bn, flags);
     const int sms = gemm_num_sms();
     // Resident CTAs per SM ~1 for the wide/skinny tiles, ~3 for narrow.
     const std::int64_t want = (fam == Family::kNarrow ? 3 : 1) * static_cast<std::int64_t>(sms);

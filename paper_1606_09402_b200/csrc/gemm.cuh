@@ -72,6 +72,11 @@ struct SmallStatus {
 constexpr int kSmallMax = 112;  // chol_small keeps [G | I] (b x 2b) in shared memory
 void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, double* r,
                 double* rinv, std::int64_t ldr, SmallStatus* status);
+// Blocked Cholesky W = R^T R (upper triangle of the l x l col-major W, overwritten) and
+// R^{-1}, one cooperative launch; r and rinv (ld ldr) must be zero on entry; one status
+// per 64-column diagonal block.
+void chol_wide(cudaStream_t st, double* w, std::int64_t ldw, int l, double* r, double* rinv, std::int64_t ldr,
+               SmallStatus* stats);
 // C = A * B for upper-triangular b x b (col-major, ld); C must not alias.
 void trmm_upper_small(cudaStream_t st, const double* a, const double* b, double* c, int n,
                       std::int64_t ld);

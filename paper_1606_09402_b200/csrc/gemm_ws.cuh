@@ -151,9 +151,30 @@ struct WsArgs {
     double* C;
     std::int64_t ldc;
     int c_row, M, N, K, k_split_len, splits, tiles_m, tiles_n, flags;
+    int tiles;  // output tiles per k-split (kGemmUpperC: only those on/above the diagonal)
     double alpha, beta;
     double* partial;
 };
+
+// Work item -> (m tile, n tile, k split), n-fastest. For kGemmUpperC only the tiles
+// reaching the diagonal or above are enumerated (row mt starts at n tile mt*BM/BN),
+// so the static persistent schedule stays balanced on Gram/SYRK outputs.
+template <int BM, int BN>
+__device__ __forceinline__ void ws_decode_item(const WsArgs& p, int it, int& mt, int& nt, int& kz) {
+    kz = it / p.tiles;
+    int t = it - kz * p.tiles;
+    if (!(p.flags & kGemmUpperC)) {
+        nt = t % p.tiles_n;
+        mt = t / p.tiles_n;
+        return;
+    }
+    for (mt = 0; mt < p.tiles_m - 1; ++mt) {
+        const int cnt = max(0, p.tiles_n - (mt * BM) / BN);
+        if (t < cnt) break;
+        t -= cnt;
+    }
+    nt = (mt * BM) / BN + t;
+}
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int NP>
 __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const __grid_constant__ WsArgs p) {
@@ -174,7 +195,7 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    const int items = p.tiles_m * p.tiles_n * p.splits;
+    const int items = p.tiles * p.splits;
     if (warp >= NC) {
         // ===== producer warps =====
         const int pt = threadIdx.x - NC * 32;  // producer thread index
@@ -182,9 +203,9 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
         int stage = 0;
         unsigned phase = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
-            const int nt = it % p.tiles_n, mt = (it / p.tiles_n) % p.tiles_m, kz = it / (p.tiles_n * p.tiles_m);
+            int mt, nt, kz;
+            ws_decode_item<BM, BN>(p, it, mt, nt, kz);
             const int m0 = mt * BM, n0 = nt * BN;
-            if ((p.flags & kGemmUpperC) && m0 >= n0 + BN) continue;
             const int k_begin = kz * p.k_split_len;
             int k_end = min(p.K, k_begin + p.k_split_len);
             if (p.flags & kGemmTriB) k_end = min(k_end, n0 + BN);
@@ -255,9 +276,9 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
     int stage = 0;
     unsigned phase = 0;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        const int nt = it % p.tiles_n, mt = (it / p.tiles_n) % p.tiles_m, kz = it / (p.tiles_n * p.tiles_m);
+        int mt, nt, kz;
+        ws_decode_item<BM, BN>(p, it, mt, nt, kz);
         const int m0 = mt * BM, n0 = nt * BN;
-        if ((p.flags & kGemmUpperC) && m0 >= n0 + BN) continue;
         const int k_begin = kz * p.k_split_len;
         int k_end = min(p.K, k_begin + p.k_split_len);
         if (p.flags & kGemmTriB) k_end = min(k_end, n0 + BN);

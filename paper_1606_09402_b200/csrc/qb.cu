@@ -313,10 +313,10 @@ public:
 
     // Blocked right-looking Cholesky of the l x l SPD matrix W (column-major, upper
     // triangle read, overwritten) into R (upper) and R^{-1}, both column-major (ld l).
-    // Diagonal blocks use chol_small (which also returns their inverses); the row panel
-    // is R_kk^{-T} W_k,rest and the trailing update a DMMA SYRK on upper tiles only.
-    // Off-diagonal blocks of R^{-1} follow column by column:
-    //   Rinv[:j, j] = -(Rinv[:j,:j] R[:j, j]) Rinv_jj.
+    // One cooperative launch (chol_wide, small.cu): right-looking over 64-column tiles,
+    // diagonal blocks by chol_small's register-tiled elimination of [W_kk | I], row panels
+    // R_kk^{-T} W_kj and trailing updates as DMMA tile products; R^{-1} is accumulated
+    // alongside (the transposed right half of the elimination of [W | I]).
     // Returns false on breakdown or when min diag(R) < kCholRatioMin * max diag(R).
     bool chol_blocked(double* w, int l, double* r, double* rinv, double max_gram_dev, double* ratio = nullptr) {
         const int nb = 64;
@@ -326,31 +326,7 @@ public:
         if (stat_.n < static_cast<std::size_t>(nt) * 4) stat_ = DBuf(static_cast<std::size_t>(nt) * 4, st_);
         auto* stats = reinterpret_cast<SmallStatus*>(stat_.p);
         static_assert(sizeof(SmallStatus) <= 4 * sizeof(double), "status size");
-        for (int kb = 0; kb < nt; ++kb) {
-            const int k0 = kb * nb, w0 = std::min(nb, l - k0), rest = l - k0 - w0;
-            chol_small(st_, w + k0 + static_cast<std::int64_t>(k0) * l, l, w0, r + k0 + static_cast<std::int64_t>(k0) * l,
-                       rinv + k0 + static_cast<std::int64_t>(k0) * l, l,
-                       stats + kb);
-            if (rest > 0) {
-                MatView rkk_inv{rinv + k0 + static_cast<std::int64_t>(k0) * l, w0, w0, l, false};
-                MatView wp{w + k0 + static_cast<std::int64_t>(k0 + w0) * l, w0, rest, l, false};
-                MatView rp{r + k0 + static_cast<std::int64_t>(k0 + w0) * l, w0, rest, l, false};
-                gemm(1.0, rkk_inv.t(), wp, 0.0, rp);
-                MatView wt{w + (k0 + w0) + static_cast<std::int64_t>(k0 + w0) * l, rest, rest, l, false};
-                qbgpu::gemm(st_, c_.ws_gemm, -1.0, rp.t(), rp, 1.0, wt, kGemmUpperC);
-            }
-        }
-        for (int jb = 1; jb < nt; ++jb) {
-            const int j0 = jb * nb, wj = std::min(nb, l - j0);
-            if (tri_.n < static_cast<std::size_t>(l) * nb) tri_ = DBuf(static_cast<std::size_t>(l) * nb, st_);
-            MatView t{tri_.p, j0, wj, j0, false};
-            MatView rinv_tl{rinv, j0, j0, l, false};
-            MatView r_col{r + static_cast<std::int64_t>(j0) * l, j0, wj, l, false};
-            gemm(1.0, rinv_tl, r_col, 0.0, t);
-            MatView rinv_jj{rinv + j0 + static_cast<std::int64_t>(j0) * l, wj, wj, l, false};
-            MatView rinv_col{rinv + static_cast<std::int64_t>(j0) * l, j0, wj, l, false};
-            gemm(-1.0, t, rinv_jj, 0.0, rinv_col);
-        }
+        chol_wide(st_, w, l, l, r, rinv, l, stats);
         std::vector<SmallStatus> hs(static_cast<std::size_t>(nt));
         QB_CUDA(cudaMemcpyAsync(hs.data(), stats, sizeof(SmallStatus) * nt, cudaMemcpyDeviceToHost, st_));
         QB_CUDA(cudaStreamSynchronize(st_));

@@ -12,6 +12,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 
 #include "gemm.cuh"
@@ -156,9 +158,9 @@ __global__ void colsumsq_stage2(const double* __restrict__ partial, int nblk, st
 // 1/sqrt(piv_k) is R(k,:) on the left and R^{-T}(k,:) on the right. The upper
 // triangle of G and the lower triangle of the right part are cut into T x T tiles
 // on a 16 x 16 grid and every thread owns ONE tile in registers (136 + 136 tiles).
-// Per step the owners of row k publish it (double-buffered in shared memory) and
-// the pivot owner publishes 1/piv; each thread then updates its tile: one barrier
-// and <= 2T shared loads per thread per step.
+// Per step the owners of row k publish it (double-buffered in shared memory); each
+// thread forms 1/piv itself and updates its tile: one barrier and <= 2T + 1 shared
+// loads per thread per step, square roots deferred to the end.
 // A near-identity Gram (max|G - I| <= 1e-8: the second CholQR pass and every
 // re-orthogonalisation) takes the exact-to-rounding first-order path
 // R = I + F, R^{-1} = I - F, F = triu(G - I) - diag(G - I)/2 (error O(|G - I|^2)).
@@ -167,12 +169,22 @@ constexpr int kCholTiles = kCholGrid * (kCholGrid + 1);   // 136 left + 136 righ
 constexpr int kCholThreads = ((kCholTiles + 31) / 32) * 32;  // 288
 constexpr double kFirstOrderDev = 1e-8;
 
+// 1/x to full double precision: MUFU reciprocal seed + two Newton steps (no IEEE
+// division slow path on the Cholesky's critical path).
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
 template <int T>
-__global__ void __launch_bounds__(kCholThreads)
-chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double* __restrict__ r,
-                  double* __restrict__ rinv, std::int64_t ldr, SmallStatus* status) {
+__device__ __noinline__ void chol_small_block(const double* __restrict__ g, std::int64_t ldg, int b, double* __restrict__ r,
+                                 double* __restrict__ rinv, std::int64_t ldr, SmallStatus* status) {
     __shared__ double bufL[2][kSmallMax], bufR[2][kSmallMax];
-    __shared__ double s_pinv[kSmallMax], s_rsq[kSmallMax], s_sq[kSmallMax];
+    __shared__ double s_rsq[kSmallMax], s_sq[kSmallMax];
     __shared__ double s_red[kCholThreads / 32];
     __shared__ double s_dev;
     __shared__ int s_bad;
@@ -235,72 +247,65 @@ chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double*
             }
         }
     } else {
-        // publish row 0 and pivot 0
+        // Publication buffers start at zero: entries nobody publishes must read as 0.
+        for (int idx = tid; idx < 2 * kSmallMax; idx += kCholThreads) {
+            (&bufL[0][0])[idx] = 0.0;
+            (&bufR[0][0])[idx] = 0.0;
+        }
+        // The owners of row k publish their T entries of it: left side with entries j <= k
+        // zeroed (the pivot goes to s_sq[k], sanitised: a breakdown is recorded and the
+        // step continues with pivot 1), right side as is (its entries j > k are 0). The
+        // row is selected from registers by compile-time indices (no local memory).
         auto publish = [&](int k, int buf) {
-            if (k < i0 || k >= i0 + T || k >= b) return;
+            const int a = k - i0;
+            if (side < 0 || a < 0 || a >= T) return;
 #pragma unroll
-            for (int a = 0; a < T; ++a) {
-                if (i0 + a != k) continue;  // compile-time row index keeps v[][] in registers
+            for (int c = 0; c < T; ++c) {
+                double x = v[0][c];
 #pragma unroll
-                for (int c = 0; c < T; ++c) {
-                    const int j = j0 + c;
-                    if (j >= b) continue;
-                    if (side == 0 && j >= k) bufL[buf][j] = v[a][c];
-                    if (side == 1 && j <= k) bufR[buf][j] = v[a][c];
-                    if (side == 0 && j == k) {
-                        const double piv = v[a][c];
-                        const bool bad = !(piv > 0.0) || !isfinite(piv);
+                for (int aa = 1; aa < T; ++aa) x = (a == aa) ? v[aa][c] : x;
+                const int j = j0 + c;
+                if (side == 0) {
+                    if (j == k) {
+                        const bool bad = !(x > 0.0) || !isfinite(x);
                         if (bad && s_bad < 0) s_bad = k;
-                        const double pp = bad ? 1.0 : piv;
-                        const double sq = sqrt(pp);
-                        s_pinv[k] = 1.0 / pp;
-                        s_sq[k] = sq;
-                        s_rsq[k] = 1.0 / sq;
+                        s_sq[k] = bad ? 1.0 : x;
                     }
+                    bufL[buf][j] = j > k ? x : 0.0;
+                } else {
+                    bufR[buf][j] = x;
                 }
             }
         };
-        if (side >= 0) publish(0, 0);
+        __syncthreads();
+        publish(0, 0);
         __syncthreads();
         for (int k = 0; k < b; ++k) {
             const int p = k & 1;
+            // one branch-free update per step for both sides: rows i > k of the tile take
+            // f_i = G(k, i) / piv_k times the published row k (left: G, right: the R^{-T} part)
             if (side >= 0 && i0 + T - 1 > k) {
-                const double pinv = s_pinv[k];
-                double f[T];
+                const double pinv = rcp_nr(s_sq[k]);
+                const double* rb = side == 0 ? bufL[p] : bufR[p];
+                double f[T], rowk[T];
 #pragma unroll
-                for (int a = 0; a < T; ++a) {
-                    const int i = i0 + a;
-                    f[a] = (i > k && i < b) ? bufL[p][i] * pinv : 0.0;
-                }
-                if (side == 0) {
-                    if (j0 + T - 1 > k) {
-                        double rowk[T];
+                for (int a = 0; a < T; ++a) f[a] = (i0 + a > k) ? bufL[p][i0 + a] * pinv : 0.0;
 #pragma unroll
-                        for (int c = 0; c < T; ++c) {
-                            const int j = j0 + c;
-                            rowk[c] = (j > k && j < b) ? bufL[p][j] : 0.0;
-                        }
+                for (int c = 0; c < T; ++c) rowk[c] = rb[j0 + c];
 #pragma unroll
-                        for (int a = 0; a < T; ++a)
+                for (int a = 0; a < T; ++a)
 #pragma unroll
-                            for (int c = 0; c < T; ++c) v[a][c] = fma(-f[a], rowk[c], v[a][c]);
-                    }
-                } else if (j0 <= k) {
-                    double rowk[T];
-#pragma unroll
-                    for (int c = 0; c < T; ++c) {
-                        const int j = j0 + c;
-                        rowk[c] = (j <= k && j < b) ? bufR[p][j] : 0.0;
-                    }
-#pragma unroll
-                    for (int a = 0; a < T; ++a)
-#pragma unroll
-                        for (int c = 0; c < T; ++c) v[a][c] = fma(-f[a], rowk[c], v[a][c]);
-                }
+                    for (int c = 0; c < T; ++c) v[a][c] = fma(-f[a], rowk[c], v[a][c]);
             }
-            if (side >= 0 && k + 1 < b) publish(k + 1, p ^ 1);
+            if (k + 1 < b) publish(k + 1, p ^ 1);
             __syncthreads();
         }
+        for (int k = tid; k < b; k += kCholThreads) {
+            const double sq = sqrt(s_sq[k]);
+            s_sq[k] = sq;
+            s_rsq[k] = 1.0 / sq;
+        }
+        __syncthreads();
         // row k of the result = row k / sqrt(piv_k); right part transposed into R^{-1}
 #pragma unroll
         for (int a = 0; a < T; ++a)
@@ -338,6 +343,188 @@ chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double*
             status->diag_max = dmax;
             status->gram_dev = s_dev;
         }
+    }
+}
+
+template <int T>
+__global__ void __launch_bounds__(kCholThreads)
+chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double* __restrict__ r,
+                  double* __restrict__ rinv, std::int64_t ldr, SmallStatus* status) {
+    chol_small_block<T>(g, ldg, b, r, rinv, ldr, status);
+}
+
+// ---- blocked Cholesky + inverse of an l x l Gram in ONE cooperative launch -----------
+// Right-looking over 64 x 64 tiles (nt = ceil(l/64)) of the upper triangle of W (col-major):
+//   step k:  [CTA 0]  R_kk, R_kk^{-1} = chol_small_block(W_kk)          (phase 1)
+//            grid.sync
+//            R_kj   = R_kk^{-T} W_kj            for j > k                (phase 2, left)
+//            F_pk   = F_pk R_kk^{-1}            for p < k                (phase 2, right)
+//            grid.sync
+//            W_ij  -= R_ki^T R_kj               for k < i <= j           (phase 3, left)
+//            F_pi  -= F_pk R_ki                 for p <= k < i           (phase 3, right)
+//            [CTA 0 takes only W_{k+1,k+1} and runs phase 1 of step k+1 right after it]
+//            grid.sync
+// F (in `rinv`, zero-initialised) ends as R^{-1}: the right half of the elimination of
+// [W | I] kept transposed (F_kk = R_kk^{-1} from phase 1). Two grid barriers per step
+// instead of ~5 dependent launches per 64-column panel.
+__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a0), "d"(a1), "d"(b0));
+}
+
+constexpr int kCwNb = 64;
+constexpr int kCwLd = 68;   // padded shared stride (= 4 mod 16 doubles: conflict-free fragments)
+constexpr int kCwSmemBytes = 2 * kCwNb * kCwLd * 8;
+
+// Stage a 64 x 64 operand X(u, v) = x[u*su + v*sv] (u < ur, v < vr; zero elsewhere) in
+// shared memory along its contiguous global dimension. Threads 0..255 each gather 16
+// elements into registers first (all loads in flight at once), then store.
+__device__ __forceinline__ void cw_stage(double* s, const double* __restrict__ x, std::int64_t su,
+                                         std::int64_t sv, int ur, int vr, int& ssu, int& ssv) {
+    const bool u_contig = su == 1;
+    ssu = u_contig ? 1 : kCwLd;
+    ssv = u_contig ? kCwLd : 1;
+    const int tid = threadIdx.x;
+    if (tid >= 256) return;
+    // thread -> fixed index `fast` along the contiguous dimension, `slow` = slow0 + 4q
+    const int fast = tid & (kCwNb - 1), slow0 = tid >> 6;
+    const std::int64_t s_fast = u_contig ? su : sv, s_slow = u_contig ? sv : su;
+    const int lim_fast = u_contig ? ur : vr, lim_slow = u_contig ? vr : ur;
+    const int ss_fast = u_contig ? ssu : ssv, ss_slow = u_contig ? ssv : ssu;
+    const double* src = x + fast * s_fast + slow0 * s_slow;
+    const bool fast_ok = fast < lim_fast;
+    double vals[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+        vals[q] = (fast_ok && slow0 + 4 * q < lim_slow) ? __ldcg(src + 4 * q * s_slow) : 0.0;
+    double* dst = s + fast * ss_fast + slow0 * ss_slow;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) dst[4 * q * ss_slow] = vals[q];
+}
+
+// C(m, n) = alpha * sum_q A(m, q) B(q, n) + beta * C(m, n) on one 64 x 64 tile (m < mr,
+// n < nc, q < kd): A(m, q) = a[m*a_sm + q*a_sq], B(q, n) = b[q*b_sq + n*b_sn], C col-major.
+// Both operands are staged before any store, so C may alias A. DMMA m16n8k4, 8 warps of
+// 16 x 32 outputs; the C tile is read into registers (beta != 0) before the MMAs.
+__device__ __noinline__ void cw_tile_gemm(double* smem, const double* a, std::int64_t a_sm, std::int64_t a_sq, const double* b,
+                             std::int64_t b_sq, std::int64_t b_sn, double* c, std::int64_t ldc, int mr, int nc,
+                             int kd, double alpha, double beta) {
+    double* sa = smem;
+    double* sb = smem + kCwNb * kCwLd;
+    int am, aq, bn, bq;
+    cw_stage(sa, a, a_sm, a_sq, mr, kd, am, aq);
+    cw_stage(sb, b, b_sn, b_sq, nc, kd, bn, bq);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp & 3, wn = warp >> 2;
+    const int g = lane >> 2, t = lane & 3;
+    double cv[4][4];
+    if (warp < 8 && beta != 0.0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int row = wm * 16 + g + (e >= 2 ? 8 : 0);
+                const int col = wn * 32 + j * 8 + 2 * t + (e & 1);
+                cv[j][e] = (row < mr && col < nc) ? __ldcg(c + row + static_cast<std::int64_t>(col) * ldc) : 0.0;
+            }
+    }
+    __syncthreads();
+    if (warp < 8) {
+        double acc[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
+        const int kq = (kd + 3) & ~3;
+        for (int kk = 0; kk < kq; kk += 4) {
+            const int r0 = wm * 16 + g;
+            const double a0 = sa[r0 * am + (kk + t) * aq];
+            const double a1 = sa[(r0 + 8) * am + (kk + t) * aq];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double bf = sb[(wn * 32 + j * 8 + g) * bn + (kk + t) * bq];
+                dmma_16x8x4(acc[j], a0, a1, bf);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int row = wm * 16 + g + (e >= 2 ? 8 : 0);
+                const int col = wn * 32 + j * 8 + 2 * t + (e & 1);
+                if (row < mr && col < nc) {
+                    const double v = alpha * acc[j][e];
+                    c[row + static_cast<std::int64_t>(col) * ldc] = beta == 0.0 ? v : v + beta * cv[j][e];
+                }
+            }
+    }
+    __syncthreads();
+}
+
+struct CholWideArgs {
+    double* w;
+    std::int64_t ldw;
+    double* r;
+    double* rinv;
+    std::int64_t ldr;
+    int l, nt;
+    SmallStatus* stats;
+};
+
+__global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs p) {
+    extern __shared__ __align__(16) double cw_smem[];
+    cg::grid_group grid = cg::this_grid();
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int nt = p.nt, l = p.l;
+    auto sz = [&](int t) { return min(kCwNb, l - t * kCwNb); };
+    auto W = [&](int i, int j) { return p.w + static_cast<std::int64_t>(i) * kCwNb + static_cast<std::int64_t>(j) * kCwNb * p.ldw; };
+    auto R = [&](int i, int j) { return p.r + static_cast<std::int64_t>(i) * kCwNb + static_cast<std::int64_t>(j) * kCwNb * p.ldr; };
+    auto F = [&](int i, int j) { return p.rinv + static_cast<std::int64_t>(i) * kCwNb + static_cast<std::int64_t>(j) * kCwNb * p.ldr; };
+    // item e >= 1 of a phase -> CTA 1 + (e-1) % (G-1); item 0 (phase 3: W_{k+1,k+1}) -> CTA 0
+    const int e_first = G == 1 ? 1 : cta, e_step = G == 1 ? 1 : G - 1;
+    if (cta == 0) chol_small_block<4>(W(0, 0), p.ldw, sz(0), R(0, 0), F(0, 0), p.ldr, p.stats);
+    grid.sync();
+    for (int k = 0; k < nt; ++k) {
+        const int bk = sz(k);
+        const int n = nt - k - 1;
+        // phase 2: items 1..n left (j = k + e), n+1..n+k right (p = e - n - 1)
+        for (int e = e_first; e >= 1 && e <= n + k; e += e_step) {
+            if (e <= n) {
+                const int j = k + e;
+                // R_kj(a, c) = sum_q Rinv_kk(q, a) W_kj(q, c)
+                cw_tile_gemm(cw_smem, F(k, k), p.ldr, 1, W(k, j), 1, p.ldw, R(k, j), p.ldr, bk, sz(j), bk, 1.0, 0.0);
+            } else {
+                const int pp = e - n - 1;
+                // F_pk(a, c) = sum_q F_pk(a, q) Rinv_kk(q, c)   (in place)
+                cw_tile_gemm(cw_smem, F(pp, k), 1, p.ldr, F(k, k), 1, p.ldr, F(pp, k), p.ldr, sz(pp), bk, bk, 1.0, 0.0);
+            }
+        }
+        grid.sync();
+        if (n == 0) break;
+        // phase 3: item 0 = (k+1, k+1); then the other left tiles, then the right tiles
+        const int n_left = n * (n + 1) / 2;
+        const int items = n_left + (k + 1) * n;
+        for (int e = (G == 1 || cta == 0) ? 0 : cta; e < items; e = (G == 1) ? e + 1 : (e == 0 ? items : e + e_step)) {
+            if (e < n_left) {
+                // e -> (i, j), k < i <= j, enumerated row by row starting at (k+1, k+1)
+                int t = e, i = k + 1;
+                while (t >= nt - i) { t -= nt - i; ++i; }
+                const int j = i + t;
+                // W_ij(a, c) -= sum_q R_ki(q, a) R_kj(q, c)
+                cw_tile_gemm(cw_smem, R(k, i), p.ldr, 1, R(k, j), 1, p.ldr, W(i, j), p.ldw, sz(i), sz(j), bk, -1.0, 1.0);
+            } else {
+                const int t = e - n_left;
+                const int pp = t / n, i = k + 1 + t % n;
+                // F_pi(a, c) -= sum_q F_pk(a, q) R_ki(q, c)
+                cw_tile_gemm(cw_smem, F(pp, k), 1, p.ldr, R(k, i), 1, p.ldr, F(pp, i), p.ldr, sz(pp), sz(i), bk, -1.0, 1.0);
+            }
+            if (e == 0)
+                chol_small_block<4>(W(k + 1, k + 1), p.ldw, sz(k + 1), R(k + 1, k + 1), F(k + 1, k + 1), p.ldr,
+                                    p.stats + k + 1);
+        }
+        grid.sync();
     }
 }
 
@@ -622,6 +809,23 @@ void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, doubl
     if (b <= 32) chol_small_kernel<2><<<1, kCholThreads, 0, st>>>(g, ldg, b, r, rinv, ldr, status);
     else if (b <= 64) chol_small_kernel<4><<<1, kCholThreads, 0, st>>>(g, ldg, b, r, rinv, ldr, status);
     else chol_small_kernel<7><<<1, kCholThreads, 0, st>>>(g, ldg, b, r, rinv, ldr, status);
+    QB_LAUNCH_CHECK();
+}
+
+void chol_wide(cudaStream_t st, double* w, std::int64_t ldw, int l, double* r, double* rinv, std::int64_t ldr,
+               SmallStatus* stats) {
+    if (l < 1) throw QbError(kDimensionError, "chol_wide: empty");
+    static int grid = 0;
+    if (!grid) {
+        QB_CUDA(cudaFuncSetAttribute(chol_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCwSmemBytes));
+        int per_sm = 0;
+        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_wide_kernel, kCholThreads, kCwSmemBytes));
+        grid = std::max(1, std::min(per_sm, 1) * gemm_num_sms());
+    }
+    CholWideArgs a{w, ldw, r, rinv, ldr, l, static_cast<int>(ceil_div(l, kCwNb)), stats};
+    void* args[] = {&a};
+    QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(chol_wide_kernel), grid, kCholThreads, args,
+                                        kCwSmemBytes, st));
     QB_LAUNCH_CHECK();
 }
 

@@ -186,6 +186,33 @@ def test_chol_small_breakdown(ctx):
     assert status.value == 1
 
 
+@pytest.mark.parametrize("l", [65, 130, 300, 1000, 2000])
+def test_chol_wide(ctx, l):
+    """Blocked Cholesky + R^{-1} in one cooperative launch (partial last tiles included);
+    the strict lower triangle of the input is garbage (only the upper one is read)."""
+    L = _lib()
+    L.qbfac_gpu_test_chol_wide.argtypes = [C.c_void_p] * 2 + [C.c_int] + [C.c_void_p] * 3
+    rs = np.random.default_rng(l)
+    y = rs.standard_normal((2 * l + 5, l)) * np.logspace(0, -3, l)
+    g = y.T @ y
+    gin = np.triu(g) + np.tril(np.full((l, l), np.nan), -1)
+    gd = _dev(gin.T)
+    import torch
+    rd = torch.zeros((l, l), dtype=torch.float64, device="cuda")
+    rid = torch.zeros((l, l), dtype=torch.float64, device="cuda")
+    bd = C.c_int(-1)
+    torch.cuda.synchronize()
+    assert L.qbfac_gpu_test_chol_wide(ctx.handle, _ptr(gd), l, _ptr(rd), _ptr(rid), C.byref(bd)) == 0
+    r = rd.cpu().numpy().T
+    ri = rid.cpu().numpy().T
+    assert bd.value == 0
+    assert np.array_equal(np.triu(r), r) and np.array_equal(np.triu(ri), ri) and np.all(np.diag(r) > 0)
+    assert np.linalg.norm(r.T @ r - g) / np.linalg.norm(g) < 1e-14
+    r_ref = np.linalg.cholesky(g).T
+    assert np.abs(r - r_ref).max() <= 1e-9 * np.abs(r_ref).max()
+    assert np.linalg.norm(r @ ri - np.eye(l)) < 1e-14 * np.linalg.cond(r) * l
+
+
 @pytest.mark.parametrize("m,b", [(10, 1), (50, 10), (1000, 20), (30000, 50), (5000, 100)])
 def test_householder_panel_matches_oracle(ctx, oracle, m, b):
     L = _lib()
