@@ -6,6 +6,7 @@
  *   qbfac_gpu_test_gemm      the DMMA GEMM behind every dense product
  *                            (replaces kernels::gemm_nn / gemm_tn, kernels_drivers.cpp:21-65)
  *   qbfac_gpu_test_chol      the in-CTA Cholesky + inverse used by CholQR
+ *   qbfac_gpu_test_cholqr2   the fused one-launch CholQR2 of a tall panel
  *   qbfac_gpu_test_chol_wide the blocked (cooperative) Cholesky + inverse of the wide CholQR
  *   qbfac_gpu_test_householder  the Householder panel QR (orth_qr, qr.hpp:15-18)
  *   qbfac_gpu_test_orth_wide the power step's orth() of a wide sketch (CholQR2 or BCGS2)
@@ -31,6 +32,9 @@ int qbfac_gpu_test_gemm(qbfac_gpu_ctx* ctx, double alpha, const double* a, int64
 /* b x b Gram (col-major, ld b) -> R, R^{-1} (col-major, ld b); returns breakdown flag in *status. */
 int qbfac_gpu_test_chol(qbfac_gpu_ctx* ctx, const double* g, int b, double* r, double* rinv, int* status);
 /* blocked Cholesky + inverse of an l x l Gram (col-major, upper triangle read and overwritten), one cooperative launch */
+/* fused CholQR2 of a row-major panel (rows x b, b <= 112): q (may alias y), R and R^{-1} (ld 112, column-major) */
+int qbfac_gpu_test_cholqr2(qbfac_gpu_ctx* ctx, const double* y, int64_t rows, int b, int64_t ldy, double* q,
+                           int64_t ldq, double* r, double* rinv, int* status);
 int qbfac_gpu_test_chol_wide(qbfac_gpu_ctx* ctx, double* g, int l, double* r, double* rinv, int* breakdown);
 /* Householder QR of a column-major m x b panel in place (Q overwrites y); R col-major ld b. */
 int qbfac_gpu_test_householder(qbfac_gpu_ctx* ctx, double* y, int64_t m, int b, int64_t ld, double* r);

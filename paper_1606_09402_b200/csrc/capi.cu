@@ -351,6 +351,26 @@ int qbfac_gpu_test_chol_wide(qbfac_gpu_ctx* ctx, double* g, int l, double* r, do
     });
 }
 
+int qbfac_gpu_test_cholqr2(qbfac_gpu_ctx* ctx, const double* y, int64_t rows, int b, int64_t ldy, double* q,
+                           int64_t ldq, double* r, double* rinv, int* status) {
+    return guard(ctx, [&] {
+        auto& cx = *ctx->c;
+        constexpr int S = qbgpu::kSmallMax * qbgpu::kSmallMax;
+        qbgpu::DBuf small(static_cast<std::size_t>(S) * 5, cx.st);
+        qbgpu::DBuf t1(static_cast<std::size_t>(std::max<int64_t>(rows, 1)) * b, cx.st);
+        qbgpu::DBuf st(8, cx.st);
+        auto* sts = reinterpret_cast<qbgpu::SmallStatus*>(st.p);
+        double* sl = small.p;
+        qbgpu::cholqr2_panel(cx.st, cx.ws_panel, y, rows, b, ldy, t1.p, q, ldq, sl, sl + S, sl + 2 * S, sl + 3 * S,
+                             sl + 4 * S, sts, sts + 1);
+        qbgpu::trmm_upper_pair(cx.st, sl + 3 * S, sl + S, r, sl + 2 * S, sl + 4 * S, rinv, b, qbgpu::kSmallMax);
+        qbgpu::SmallStatus h[2];
+        QB_CUDA(cudaMemcpyAsync(h, sts, sizeof(h), cudaMemcpyDeviceToHost, cx.st));
+        QB_CUDA(cudaStreamSynchronize(cx.st));
+        *status = h[0].breakdown | (h[1].breakdown << 1);
+    });
+}
+
 int qbfac_gpu_test_householder(qbfac_gpu_ctx* ctx, double* y, int64_t m, int b, int64_t ld, double* r) {
     return guard(ctx, [&] {
         auto& cx = *ctx->c;

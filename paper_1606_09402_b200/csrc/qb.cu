@@ -77,6 +77,7 @@ Context::~Context() {
     ws_red.release();
     ws_hh.release();
     ws_sp.release();
+    ws_panel.release();
     if (d_small) cudaFree(d_small);
     if (d_status) cudaFree(d_status);
     if (d_lazy) cudaFree(d_lazy);
@@ -256,7 +257,8 @@ public:
                s1.gram_dev <= kCholGramDevMax && std::isfinite(s0.diag_max) && std::isfinite(s1.diag_max);
     }
 
-    int orth_block(const MatView& y, const MatView& qout, int r_slot, int rinv_slot, bool sharded, DBuf& tmp) {
+    int orth_block(const MatView& y, const MatView& qout, int r_slot, int rinv_slot, bool sharded, DBuf& tmp,
+                   bool need_r = true) {
         const int b = static_cast<int>(y.cols);
         const std::int64_t rows = y.rows;
         if (b == 0) return 0;
@@ -266,6 +268,26 @@ public:
             const bool lazy = optimistic && lazy_n < Context::kLazyCap / 2;
             SmallStatus* st0 = lazy ? c_.d_lazy + 2 * lazy_n : c_.d_status + 0;
             SmallStatus* st1 = st0 + 1;
+            // Unsharded panels: the whole CholQR2 in one cooperative launch (q may alias y
+            // only when the statuses are checked lazily: the Householder redo restarts the block).
+            if (!sharded && rows > 0 && y.rowmajor && qout.rowmajor && (lazy || qout.p != y.p)) {
+                cholqr2_panel(st_, c_.ws_panel, y.p, rows, b, y.ld, t1.p, qout.p, qout.ld, slot(kG), slot(kRa),
+                              slot(kRainv), slot(kRb), slot(kRbinv), st0, st1);
+                bool ok = true;
+                if (lazy) {
+                    ++lazy_n;
+                } else {
+                    QB_CUDA(cudaMemcpyAsync(c_.h_status, st0, sizeof(SmallStatus) * 2, cudaMemcpyDeviceToHost, st_));
+                    QB_CUDA(cudaStreamSynchronize(st_));
+                    ok = cholqr_ok(c_.h_status[0], c_.h_status[1]);
+                }
+                if (ok) {
+                    if (need_r)
+                        trmm_upper_pair(st_, slot(kRb), slot(kRa), slot(r_slot), slot(kRainv), slot(kRbinv),
+                                        slot(rinv_slot), b, kSmallMax);
+                    return b;
+                }
+            } else {
             // pass 1
             gemm(1.0, y.t(), y, 0.0, small(kG, b, b));
             if (sharded) c_.allreduce(slot(kG), kSlot);
@@ -285,9 +307,11 @@ public:
             }
             if (ok) {
                 gemm(1.0, t1, small(kRbinv, b, b), 0.0, qout);
-                trmm_upper_pair(st_, slot(kRb), slot(kRa), slot(r_slot), slot(kRainv), slot(kRbinv), slot(rinv_slot),
-                                b, kSmallMax);
+                if (need_r)
+                    trmm_upper_pair(st_, slot(kRb), slot(kRa), slot(r_slot), slot(kRainv), slot(kRbinv),
+                                    slot(rinv_slot), b, kSmallMax);
                 return b;
+            }
             }
         }
         // Householder fallback: exact deficiency decisions (qr.hpp:15-21).
@@ -581,7 +605,7 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             }
             // per-block power iteration with deflation at every application
             for (std::int64_t it = 0; it < p.power; ++it) {
-                eng.orth_block(yv, yv, kR1, kR1inv, sharded, tmp);
+                eng.orth_block(yv, yv, kR1, kR1inv, sharded, tmp, false);
                 MatView zv{z.p, n, bi, bi, true};
                 eng.apply_t(yv, zv); a.passes += 1;
                 if (s.k > 0) {
@@ -589,7 +613,7 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
                     eng.allreduce_view(mv);
                     eng.gemm(-1.0, s.btk(), mv, 1.0, zv);
                 }
-                eng.orth_block(zv, zv, kR1, kR1inv, false, tmp);
+                eng.orth_block(zv, zv, kR1, kR1inv, false, tmp, false);
                 eng.apply(zv, yv); a.passes += 1;
                 if (s.k > 0) {
                     eng.gemm(1.0, s.btk().t(), zv, 0.0, mv);
@@ -598,14 +622,14 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             }
             // orth, then re-orthogonalisation against Q (step 6)
             MatView qs = s.qslot(bi);
-            d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp);
+            d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp, false);
             if (d > 0 && s.k > 0) {
                 MatView qd = s.qslot(d);
                 MatView md{mbuf.p, s.k, d, d, true};
                 eng.gemm(1.0, s.qk().t(), qd, 0.0, md);
                 eng.allreduce_view(md);
                 eng.gemm(-1.0, s.qk(), md, 1.0, qd);
-                const int d2 = eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp);
+                const int d2 = eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp, false);
                 d = std::min(d, d2);
             }
             if (d == 0) {

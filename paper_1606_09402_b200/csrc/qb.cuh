@@ -46,7 +46,7 @@ struct Context {
     int device = 0;
     cudaStream_t st = nullptr;
     int sms = 148;
-    Workspace ws_gemm, ws_red, ws_hh, ws_sp;
+    Workspace ws_gemm, ws_red, ws_hh, ws_sp, ws_panel;
     RngTables rng;
     std::unique_ptr<Comm> comm;
     int rank = 0, world = 1;

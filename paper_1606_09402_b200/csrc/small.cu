@@ -528,6 +528,238 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
     }
 }
 
+// ---- fused CholQR2 of a tall panel in ONE cooperative launch -----------------------
+// Y (rows x b, row-major) -> Q = Y Ra^{-1} Rb^{-1} with Ra = chol(Y^T Y), Rb = chol(T1^T T1),
+// T1 = Y Ra^{-1}: the same arithmetic as the launch sequence Gram / chol_small / Y R^{-1}
+// twice, without its 11 launches and split-K round trips. 64-row sub-tiles are staged in
+// shared memory (CTA c takes sub-tiles c, c+G, ...); Grams are accumulated with DMMA on
+// the upper fragments only, written per CTA and reduced over CTAs in a fixed order (so the
+// result is deterministic for a given device); the b x b Choleskies run on CTA 0 between
+// grid barriers. Phase B writes T1 and accumulates its Gram from the same registers.
+struct PanelArgs {
+    const double* y;
+    std::int64_t ldy;
+    double* t1;  // rows x b, ld b
+    double* q;
+    std::int64_t ldq;
+    std::int64_t rows;
+    int b, nsub;
+    double* part;  // gridDim.x x BP x BP partial Grams
+    double* g;     // b x b Gram (ld kSmallMax)
+    double *ra, *rainv, *rb, *rbinv;  // ld kSmallMax
+    SmallStatus *st0, *st1;
+};
+
+template <int BP>
+struct PanelCfg {
+    static constexpr int SUB = BP > 96 ? 32 : 64;  // rows per sub-tile (two buffers + R fit in 227 KB)
+    static constexpr int LD = BP + 4;              // = 4 mod 16 doubles (BP multiple of 16)
+    static constexpr int MI = SUB / 16;            // m16 blocks per sub-tile
+    static constexpr int NG = 8 / MI;              // warps sharing one m16 block
+    static constexpr int NFG = (BP / 16) * (BP / 8) - (BP / 16) * (BP / 16 - 1);  // upper Gram fragments
+    static constexpr int MAXG = (NFG + 7) / 8;
+    static constexpr int MAXT = (BP / 8 + NG - 1) / NG;  // product fragments per warp: mi = w % MI, ni = w / MI + NG j
+    static constexpr int SMEM = (2 * SUB + BP) * LD * 8;
+};
+
+// Asynchronous variant: 8-byte cp.async copies (zero-filled out of range) into ys;
+// the caller commits / waits (double-buffered sub-tiles).
+template <int BP>
+__device__ __forceinline__ void panel_stage_async(double* ys, const double* __restrict__ src, std::int64_t ld,
+                                                  std::int64_t r0, std::int64_t rows, int b) {
+    using C = PanelCfg<BP>;
+    for (int idx = threadIdx.x; idx < C::SUB * BP; idx += blockDim.x) {
+        const int r = idx / BP, c = idx - r * BP;
+        const std::int64_t gr = r0 + r;
+        const bool ok = gr < rows && c < b;
+        const double* s = ok ? src + gr * ld + c : src;
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(ys + r * C::LD + c));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(s), "r"(ok ? 8 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// acc += Ys^T Ys on this warp's upper fragments
+template <int BP>
+__device__ __forceinline__ void panel_gram(const double* ys, double (&acc)[PanelCfg<BP>::MAXG][4],
+                                           const int (&fm)[PanelCfg<BP>::MAXG], const int (&fn)[PanelCfg<BP>::MAXG]) {
+    using C = PanelCfg<BP>;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll 4
+    for (int kk = 0; kk < C::SUB; kk += 4) {
+        const double* row = ys + (kk + t) * C::LD;  // A = Ys^T: a(m, k) = Ys(k, m)
+#pragma unroll
+        for (int f = 0; f < C::MAXG; ++f) {
+            if (fm[f] < 0) continue;
+            dmma_16x8x4(acc[f], row[16 * fm[f] + g], row[16 * fm[f] + g + 8], row[8 * fn[f] + g]);
+        }
+    }
+}
+
+// out fragments = Ys (SUB x BP) * Rs (BP x BP, upper), mi = warp % MI, ni = warp / MI + NG j
+template <int BP>
+__device__ __forceinline__ void panel_trmm(const double* ys, const double* rs, double (&acc)[PanelCfg<BP>::MAXT][4],
+                                           int b) {
+    using C = PanelCfg<BP>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int mi = warp % C::MI, h = warp / C::MI;
+    const int nb8 = (b + 7) >> 3, kmax = (b + 3) & ~3;
+#pragma unroll
+    for (int j = 0; j < C::MAXT; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < kmax; kk += 4) {
+        const double a0 = ys[(16 * mi + g) * C::LD + kk + t];
+        const double a1 = ys[(16 * mi + g + 8) * C::LD + kk + t];
+#pragma unroll
+        for (int j = 0; j < C::MAXT; ++j) {
+            const int ni = h + C::NG * j;
+            // R^{-1} upper: column block ni needs k < 8 ni + 8; blocks past b are zero
+            if (ni >= nb8 || kk >= 8 * ni + 8) continue;
+            dmma_16x8x4(acc[j], a0, a1, rs[(kk + t) * C::LD + 8 * ni + g]);
+        }
+    }
+}
+
+template <int BP, int T>
+__global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArgs p) {
+    using C = PanelCfg<BP>;
+    extern __shared__ __align__(16) double psm[];
+    double* ys2 = psm;                        // two SUB x LD sub-tile buffers
+    double* rs = psm + 2 * C::SUB * C::LD;    // BP x LD triangular factor
+    cg::grid_group grid = cg::this_grid();
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const bool mma_warp = warp < 8;
+    // this warp's upper Gram fragments
+    int fm[C::MAXG], fn[C::MAXG];
+#pragma unroll
+    for (int f = 0; f < C::MAXG; ++f) {
+        int e = warp + 8 * f, mi = 0;
+        fm[f] = -1;
+        fn[f] = 0;
+        // upper fragments (mi, ni >= 2 mi) with column blocks inside b only
+        const int nb8 = (p.b + 7) >> 3;
+        int nf = 0;
+        for (int m2 = 0; m2 < BP / 16; ++m2) nf += max(0, nb8 - 2 * m2);
+        if (!mma_warp || e >= nf) continue;
+        while (e >= nb8 - 2 * mi) { e -= nb8 - 2 * mi; ++mi; }
+        fm[f] = mi;
+        fn[f] = 2 * mi + e;
+    }
+    double acc[C::MAXG][4];
+    auto zero_acc = [&]() {
+#pragma unroll
+        for (int f = 0; f < C::MAXG; ++f)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[f][e] = 0.0;
+    };
+    auto write_part = [&]() {
+        double* dst = p.part + static_cast<std::size_t>(cta) * BP * BP;
+#pragma unroll
+        for (int f = 0; f < C::MAXG; ++f) {
+            if (fm[f] < 0) continue;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int row = 16 * fm[f] + g + (e >= 2 ? 8 : 0), col = 8 * fn[f] + 2 * t + (e & 1);
+                dst[row + col * BP] = acc[f][e];
+            }
+        }
+    };
+    // fixed-order sum of the CTA partials into the b x b Gram slot (upper triangle)
+    auto reduce_parts = [&]() {
+        for (int e = cta * blockDim.x + tid; e < BP * BP; e += G * blockDim.x) {
+            const int i = e % BP, j = e / BP;
+            if (i > j || j >= p.b) continue;
+            double s = 0.0;
+            for (int c = 0; c < G; ++c) s += __ldcg(p.part + static_cast<std::size_t>(c) * BP * BP + e);
+            p.g[i + j * kSmallMax] = s;
+        }
+    };
+    auto stage_r = [&](const double* rinv) {
+        for (int idx = tid; idx < BP * BP; idx += blockDim.x) {
+            const int k = idx / BP, n = idx - k * BP;
+            rs[k * C::LD + n] = (k < p.b && n < p.b && k <= n) ? __ldcg(rinv + k + n * kSmallMax) : 0.0;
+        }
+    };
+    // sub-tile loop with the next sub-tile's copy in flight (two shared buffers)
+    auto sub_loop = [&](const double* src, std::int64_t ld, auto&& body) {
+        int i = 0;
+        if (cta < p.nsub) panel_stage_async<BP>(ys2, src, ld, static_cast<std::int64_t>(cta) * C::SUB, p.rows, p.b);
+        for (int sub = cta; sub < p.nsub; sub += G, ++i) {
+            double* cur = ys2 + (i & 1) * C::SUB * C::LD;
+            double* nxt = ys2 + ((i + 1) & 1) * C::SUB * C::LD;
+            if (sub + G < p.nsub) {
+                panel_stage_async<BP>(nxt, src, ld, static_cast<std::int64_t>(sub + G) * C::SUB, p.rows, p.b);
+                cp_async_wait_1();
+            } else {
+                cp_async_wait_0();
+            }
+            __syncthreads();
+            body(cur, static_cast<std::int64_t>(sub) * C::SUB);
+            __syncthreads();
+        }
+    };
+    // ---- phase A: Gram of Y
+    zero_acc();
+    sub_loop(p.y, p.ldy, [&](double* cur, std::int64_t) {
+        if (mma_warp) panel_gram<BP>(cur, acc, fm, fn);
+    });
+    if (mma_warp) write_part();
+    grid.sync();
+    reduce_parts();
+    grid.sync();
+    if (cta == 0) chol_small_block<T>(p.g, kSmallMax, p.b, p.ra, p.rainv, kSmallMax, p.st0);
+    grid.sync();
+    // ---- phase B: T1 = Y Ra^{-1} (written out) and the Gram of T1
+    stage_r(p.rainv);
+    zero_acc();
+    sub_loop(p.y, p.ldy, [&](double* cur, std::int64_t r0) {
+        double tacc[C::MAXT][4];
+        if (mma_warp) panel_trmm<BP>(cur, rs, tacc, p.b);
+        __syncthreads();
+        if (mma_warp) {
+            const int mi = warp % C::MI, h = warp / C::MI;
+#pragma unroll
+            for (int j = 0; j < C::MAXT; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int row = 16 * mi + g + (e >= 2 ? 8 : 0), col = 8 * (h + C::NG * j) + 2 * t + (e & 1);
+                    if (col >= BP) continue;
+                    cur[row * C::LD + col] = tacc[j][e];
+                    if (r0 + row < p.rows && col < p.b) p.t1[(r0 + row) * p.b + col] = tacc[j][e];
+                }
+        }
+        __syncthreads();
+        if (mma_warp) panel_gram<BP>(cur, acc, fm, fn);
+    });
+    if (mma_warp) write_part();
+    grid.sync();
+    reduce_parts();
+    grid.sync();
+    if (cta == 0) chol_small_block<T>(p.g, kSmallMax, p.b, p.rb, p.rbinv, kSmallMax, p.st1);
+    grid.sync();
+    // ---- phase D: Q = T1 Rb^{-1}
+    stage_r(p.rbinv);
+    sub_loop(p.t1, p.b, [&](double* cur, std::int64_t r0) {
+        if (mma_warp) {
+            double tacc[C::MAXT][4];
+            panel_trmm<BP>(cur, rs, tacc, p.b);
+            const int mi = warp % C::MI, h = warp / C::MI;
+#pragma unroll
+            for (int j = 0; j < C::MAXT; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int row = 16 * mi + g + (e >= 2 ? 8 : 0), col = 8 * (h + C::NG * j) + 2 * t + (e & 1);
+                    if (r0 + row < p.rows && col < p.b) p.q[(r0 + row) * p.ldq + col] = tacc[j][e];
+                }
+        }
+    });
+}
+
 // C = A * B for upper-triangular n x n operands staged in shared memory; blockIdx.x
 // selects one of two independent products so R = Rb*Ra and Rinv = Ra^{-1} Rb^{-1}
 // are formed in one launch.
@@ -827,6 +1059,44 @@ void chol_wide(cudaStream_t st, double* w, std::int64_t ldw, int l, double* r, d
     QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(chol_wide_kernel), grid, kCholThreads, args,
                                         kCwSmemBytes, st));
     QB_LAUNCH_CHECK();
+}
+
+template <int BP, int T>
+void launch_cholqr2_panel(cudaStream_t st, PanelArgs& a, int grid_cap) {
+    using C = PanelCfg<BP>;
+    auto kern = cholqr2_panel_kernel<BP, T>;
+    a.nsub = static_cast<int>(ceil_div(a.rows, C::SUB));
+    static int per_sm = 0;
+    if (!per_sm) {
+        QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCholThreads, C::SMEM));
+        if (per_sm < 1) throw QbError(kError, "cholqr2_panel: kernel does not fit on an SM");
+    }
+    const int grid = std::max(1, std::min(std::min(a.nsub, grid_cap), per_sm * gemm_num_sms()));
+    void* args[] = {&a};
+    QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, kCholThreads, args, C::SMEM, st));
+    QB_LAUNCH_CHECK();
+}
+
+void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t rows, int b, std::int64_t ldy,
+                   double* t1, double* q, std::int64_t ldq, double* g, double* ra, double* rainv, double* rb,
+                   double* rbinv, SmallStatus* st0, SmallStatus* st1) {
+    if (b < 1 || b > kSmallMax) throw QbError(kDimensionError, "cholqr2_panel: width out of range");
+    const int bp = static_cast<int>(round_up(b, 16));
+    PanelArgs a{};
+    a.y = y; a.ldy = ldy; a.t1 = t1; a.q = q; a.ldq = ldq; a.rows = rows; a.b = b;
+    a.g = g; a.ra = ra; a.rainv = rainv; a.rb = rb; a.rbinv = rbinv; a.st0 = st0; a.st1 = st1;
+    const int cap = gemm_num_sms();
+    a.part = ws.get(static_cast<std::size_t>(cap) * bp * bp);
+    switch (bp) {
+        case 16: launch_cholqr2_panel<16, 2>(st, a, cap); break;
+        case 32: launch_cholqr2_panel<32, 2>(st, a, cap); break;
+        case 48: launch_cholqr2_panel<48, 4>(st, a, cap); break;
+        case 64: launch_cholqr2_panel<64, 4>(st, a, cap); break;
+        case 80: launch_cholqr2_panel<80, 7>(st, a, cap); break;
+        case 96: launch_cholqr2_panel<96, 7>(st, a, cap); break;
+        default: launch_cholqr2_panel<112, 7>(st, a, cap); break;
+    }
 }
 
 void trmm_upper_small(cudaStream_t st, const double* a, const double* b, double* c, int n,

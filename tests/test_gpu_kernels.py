@@ -186,6 +186,41 @@ def test_chol_small_breakdown(ctx):
     assert status.value == 1
 
 
+@pytest.mark.parametrize("rows,b,ldy", [(1, 1, 1), (40, 7, 9), (100, 16, 16), (5000, 33, 40), (100001, 50, 50),
+                                        (3000, 64, 64), (3000, 65, 70), (20000, 100, 100), (777, 112, 112)])
+def test_cholqr2_panel(ctx, rows, b, ldy):
+    """Fused one-launch CholQR2: Q orthonormal, Y = Q R with R upper and diag(R) > 0 (the
+    QR factor numpy/LAPACK returns up to signs), R R^{-1} = I; rows beyond a sub-tile,
+    widths off the 16-column padding and strided rows included."""
+    L = _lib()
+    L.qbfac_gpu_test_cholqr2.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_void_p,
+                                         C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+    rs = np.random.default_rng(rows + b)
+    y = rs.standard_normal((rows, b)) * np.logspace(0, -2, b)
+    ypad = np.zeros((rows, ldy))
+    ypad[:, :b] = y
+    import torch
+    yd = torch.as_tensor(ypad, device="cuda")
+    qd = torch.zeros((rows, b), dtype=torch.float64, device="cuda")
+    rd = torch.zeros((112, 112), dtype=torch.float64, device="cuda")
+    rid = torch.zeros((112, 112), dtype=torch.float64, device="cuda")
+    st = C.c_int(-1)
+    torch.cuda.synchronize()
+    assert L.qbfac_gpu_test_cholqr2(ctx.handle, _ptr(yd), rows, b, ldy, _ptr(qd), b, _ptr(rd), _ptr(rid),
+                                    C.byref(st)) == 0, L.qbfac_gpu_last_error(ctx.handle)
+    assert st.value == 0
+    q = qd.cpu().numpy()
+    r = rd.cpu().numpy().T[:b, :b]
+    ri = rid.cpu().numpy().T[:b, :b]
+    assert np.abs(q.T @ q - np.eye(b)).max() < 1e-13
+    assert np.array_equal(np.triu(r), r) and np.all(np.diag(r) > 0)
+    assert np.linalg.norm(q @ r - y) <= 1e-14 * np.linalg.norm(y) * max(1.0, np.sqrt(b))
+    q_ref, r_ref = np.linalg.qr(y)
+    sg = np.sign(np.diag(r_ref))
+    assert np.abs(q - q_ref * sg).max() < 1e-10
+    assert np.linalg.norm(r @ ri - np.eye(b)) < 1e-12 * np.linalg.cond(r)
+
+
 @pytest.mark.parametrize("l", [65, 130, 300, 1000, 2000])
 def test_chol_wide(ctx, l):
     """Blocked Cholesky + R^{-1} in one cooperative launch (partial last tiles included);
