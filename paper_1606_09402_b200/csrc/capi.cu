@@ -362,7 +362,7 @@ int qbfac_gpu_test_cholqr2(qbfac_gpu_ctx* ctx, const double* y, int64_t rows, in
         auto* sts = reinterpret_cast<qbgpu::SmallStatus*>(st.p);
         double* sl = small.p;
         qbgpu::cholqr2_panel(cx.st, cx.ws_panel, y, rows, b, ldy, t1.p, q, ldq, sl, sl + S, sl + 2 * S, sl + 3 * S,
-                             sl + 4 * S, sts, sts + 1);
+                             sl + 4 * S, sts, sts + 1, cx.d_gbar);
         qbgpu::trmm_upper_pair(cx.st, sl + 3 * S, sl + S, r, sl + 2 * S, sl + 4 * S, rinv, b, qbgpu::kSmallMax);
         qbgpu::SmallStatus h[2];
         QB_CUDA(cudaMemcpyAsync(h, sts, sizeof(h), cudaMemcpyDeviceToHost, cx.st));

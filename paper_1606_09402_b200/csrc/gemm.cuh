@@ -80,10 +80,11 @@ void chol_wide(cudaStream_t st, double* w, std::int64_t ldw, int l, double* r, d
 // Fused CholQR2 of a tall row-major panel Y (rows x b, b <= 112) in one cooperative launch:
 // g <- Y^T Y, (ra, rainv) <- chol, t1 <- Y ra^{-1}, g <- t1^T t1, (rb, rbinv) <- chol,
 // q <- t1 rb^{-1}; statuses of both Choleskies in st0 / st1. q may alias y. Small
-// matrices are column-major with ld kSmallMax.
+// matrices are column-major with ld kSmallMax. gbar: two zero-initialised words per
+// context (grid barrier).
 void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t rows, int b, std::int64_t ldy,
                    double* t1, double* q, std::int64_t ldq, double* g, double* ra, double* rainv, double* rb,
-                   double* rbinv, SmallStatus* st0, SmallStatus* st1);
+                   double* rbinv, SmallStatus* st0, SmallStatus* st1, unsigned* gbar);
 // C = A * B for upper-triangular b x b (col-major, ld); C must not alias.
 void trmm_upper_small(cudaStream_t st, const double* a, const double* b, double* c, int n,
                       std::int64_t ld);

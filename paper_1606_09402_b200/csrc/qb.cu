@@ -53,6 +53,8 @@ Context::Context(int dev, int rank_, int world_, const void* nccl_id) : device(d
     QB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     QB_CUDA(cudaMalloc(&d_small, sizeof(double) * kSlot * kNumSlots + 64 * sizeof(double)));
     QB_CUDA(cudaMalloc(&d_status, sizeof(SmallStatus) * 4));
+    QB_CUDA(cudaMalloc(&d_gbar, 64 * sizeof(unsigned)));
+    QB_CUDA(cudaMemset(d_gbar, 0, 64 * sizeof(unsigned)));
     QB_CUDA(cudaMalloc(&d_lazy, sizeof(SmallStatus) * kLazyCap));
     QB_CUDA(cudaMallocHost(&h_lazy, sizeof(SmallStatus) * kLazyCap));
     QB_CUDA(cudaMalloc(&d_ind, sizeof(IndicatorOut)));
@@ -80,6 +82,7 @@ Context::~Context() {
     ws_panel.release();
     if (d_small) cudaFree(d_small);
     if (d_status) cudaFree(d_status);
+    if (d_gbar) cudaFree(d_gbar);
     if (d_lazy) cudaFree(d_lazy);
     if (h_lazy) cudaFreeHost(h_lazy);
     if (d_ind) cudaFree(d_ind);
@@ -272,7 +275,7 @@ public:
             // only when the statuses are checked lazily: the Householder redo restarts the block).
             if (!sharded && rows > 0 && y.rowmajor && qout.rowmajor && (lazy || qout.p != y.p)) {
                 cholqr2_panel(st_, c_.ws_panel, y.p, rows, b, y.ld, t1.p, qout.p, qout.ld, slot(kG), slot(kRa),
-                              slot(kRainv), slot(kRb), slot(kRbinv), st0, st1);
+                              slot(kRainv), slot(kRb), slot(kRbinv), st0, st1, c_.d_gbar);
                 bool ok = true;
                 if (lazy) {
                     ++lazy_n;

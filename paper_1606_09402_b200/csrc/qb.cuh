@@ -54,6 +54,7 @@ struct Context {
     // small device scratch: b x b matrices (ld kSmallMax) and scalars
     double* d_small = nullptr;
     SmallStatus* d_status = nullptr;
+    unsigned* d_gbar = nullptr;  // grid-barrier words of the cooperative kernels (zeroed once)
     IndicatorOut* d_ind = nullptr;
     static constexpr int kLazyCap = 256;    // optimistic CholQR statuses per block
     SmallStatus* d_lazy = nullptr;

@@ -152,21 +152,7 @@ __global__ void colsumsq_stage2(const double* __restrict__ partial, int nblk, st
     if (lane == 0) out[j] = s;
 }
 
-// Cholesky of a b x b Gram (b <= 112) together with R^{-1}, one CTA, everything in
-// registers. The augmented matrix [G | I] is eliminated symmetrically (step k:
-// row_i -= (G(k,i)/piv_k) row_k for i > k); afterwards row k scaled by
-// 1/sqrt(piv_k) is R(k,:) on the left and R^{-T}(k,:) on the right. The upper
-// triangle of G and the lower triangle of the right part are cut into T x T tiles
-// on a 16 x 16 grid and every thread owns ONE tile in registers (136 + 136 tiles).
-// Per step the owners of row k publish it (double-buffered in shared memory); each
-// thread forms 1/piv itself and updates its tile: one barrier and <= 2T + 1 shared
-// loads per thread per step, square roots deferred to the end.
-// A near-identity Gram (max|G - I| <= 1e-8: the second CholQR pass and every
-// re-orthogonalisation) takes the exact-to-rounding first-order path
-// R = I + F, R^{-1} = I - F, F = triu(G - I) - diag(G - I)/2 (error O(|G - I|^2)).
-constexpr int kCholGrid = 16;
-constexpr int kCholTiles = kCholGrid * (kCholGrid + 1);   // 136 left + 136 right
-constexpr int kCholThreads = ((kCholTiles + 31) / 32) * 32;  // 288
+constexpr int kCholThreads = 288;  // 9 warps: 8 DMMA warps + 1
 constexpr double kFirstOrderDev = 1e-8;
 
 // 1/x to full double precision: MUFU reciprocal seed + two Newton steps (no IEEE
@@ -180,157 +166,233 @@ __device__ __forceinline__ double rcp_nr(double x) {
     return fma(y, e, y);
 }
 
-template <int T>
-__device__ __noinline__ void chol_small_block(const double* __restrict__ g, std::int64_t ldg, int b, double* __restrict__ r,
-                                 double* __restrict__ rinv, std::int64_t ldr, SmallStatus* status) {
-    __shared__ double bufL[2][kSmallMax], bufR[2][kSmallMax];
-    __shared__ double s_rsq[kSmallMax], s_sq[kSmallMax];
+// 1/sqrt(x) to ~1 ulp: MUFU seed + two Newton steps (no IEEE sqrt/divide slow-path calls).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = y * fma(-0.5 * x, y * y, 1.5);
+    return y * fma(-0.5 * x, y * y, 1.5);
+}
+
+__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// ---- blocked in-CTA Cholesky + inverse (b <= 112) -----------------------------------
+// G (upper triangle, b x b) is copied into shared memory W (BP x BP, BP = b rounded up to
+// 16, padded with the identity). Right-looking over 16-column panels:
+//   1. warp 0 factors the 16 x 16 diagonal block by symmetric elimination of [D | I] in
+//      registers (lane j < 16 holds column j of D, lane 16 + j column j of I; rows move by
+//      warp shuffles, no CTA barrier), giving R_pp and R_pp^{-1};
+//   2. the row panel R_p,rest = R_pp^{-T} W_p,rest and 3. the trailing update
+//      W_rest -= R_p,rest^T R_p,rest are DMMA (m16n8k4) tile products over all 8 warps.
+// R is written out, then inverted in place block column by block column
+// (Rinv[:c, c:c+16] = -Rinv[:c, :c] R[:c, c:c+16] Rinv_cc). Per 16 columns: one register
+// elimination and 2 tile products, instead of 16 CTA-wide barrier steps.
+// A near-identity Gram (max|G - I| <= 1e-8: every second CholQR pass / re-orthogonalisation)
+// takes the first-order path R = I + F, R^{-1} = I - F, F = triu(G - I) - diag(G - I)/2.
+template <int BP>
+struct CholCfg {
+    static constexpr int LD = BP + 4;   // = 4 mod 16 doubles: conflict-free DMMA fragment loads
+    static constexpr int TLD = 20;
+    static constexpr int P = BP / 16;
+    static constexpr int SMEM_DOUBLES = BP * LD + BP * TLD + P * 16 * TLD + BP;
+    static constexpr int SMEM = SMEM_DOUBLES * 8;
+};
+
+// C(16 mi + ., 8 ni + .) = alpha * sum_k A(16 mi + ., k) B(k, 8 ni + .) (+ C if accumulate)
+// A(m, k) = a[m * am + k * ak], B(k, n) = bsrc[k * bk + n * bn], C(m, n) = c[m * cm + n], k in [k0, k1).
+__device__ __forceinline__ void ct_frag(const double* a, int am, int ak, const double* bsrc, int bk, int bn, double* c,
+                                        int cm, int mi, int ni, int k0, int k1, double alpha, bool accumulate) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int kk = k0; kk < k1; kk += 4) {
+        const double a0 = a[(16 * mi + g) * am + (kk + t) * ak];
+        const double a1 = a[(16 * mi + g + 8) * am + (kk + t) * ak];
+        const double b0 = bsrc[(kk + t) * bk + (8 * ni + g) * bn];
+        dmma_16x8x4(acc, a0, a1, b0);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int m = 16 * mi + g + (e >= 2 ? 8 : 0), n = 8 * ni + 2 * t + (e & 1);
+        double* cp = c + m * cm + n;
+        *cp = accumulate ? *cp + alpha * acc[e] : alpha * acc[e];
+    }
+}
+
+template <int BP>
+__device__ __noinline__ void chol_tile_block(const double* __restrict__ gsrc, std::int64_t ldg, int b,
+                                             double* __restrict__ r, double* __restrict__ rinv, std::int64_t ldr,
+                                             SmallStatus* status, double* sm) {
+    using C = CholCfg<BP>;
+    double* W = sm;                       // BP x LD, row-major; upper = G, then R, then R^{-1}
+    double* Tm = W + BP * C::LD;          // BP x TLD scratch
+    double* Dall = Tm + BP * C::TLD;      // P x (16 x TLD): Rinv_pp, row-major
+    double* dg = Dall + C::P * 16 * C::TLD;  // diag(R)
     __shared__ double s_red[kCholThreads / 32];
     __shared__ double s_dev;
     __shared__ int s_bad;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // tile assignment: t < 136 -> left (upper) tile, else right (lower) tile
-    int side = -1, ti = 0, tj = 0;
-    if (tid < kCholTiles) {
-        int t = tid < kCholTiles / 2 ? tid : tid - kCholTiles / 2;
-        // enumerate (ti, tj) with ti <= tj (row-major over the upper triangle of the tile grid)
-        int row = 0;
-        while (t >= kCholGrid - row) { t -= kCholGrid - row; ++row; }
-        if (tid < kCholTiles / 2) { side = 0; ti = row; tj = row + t; }   // left tile (ti <= tj)
-        else { side = 1; ti = row + t; tj = row; }                       // right tile (ti >= tj)
-    }
-    const int i0 = ti * T, j0 = tj * T;
-    double v[T][T];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nthr = blockDim.x;
     double dev = 0.0;
+    // column-major source: consecutive threads take consecutive rows i of one column j;
+    // 8 loads in flight per thread per round
+    for (int base = 0; base < BP * BP; base += 8 * nthr) {
+        double v[8];
 #pragma unroll
-    for (int a = 0; a < T; ++a)
-#pragma unroll
-        for (int c = 0; c < T; ++c) {
-            const int i = i0 + a, j = j0 + c;
-            double x = 0.0;
-            if (side == 0 && i < b && j < b && i <= j) {
-                x = g[i + static_cast<std::int64_t>(j) * ldg];
-                dev = fmax(dev, fabs(x - (i == j ? 1.0 : 0.0)));
-            } else if (side == 1) {
-                x = (i == j) ? 1.0 : 0.0;
-            }
-            v[a][c] = x;
+        for (int q = 0; q < 8; ++q) {
+            const int idx = base + q * nthr + tid;
+            const int j = idx / BP, i = idx - j * BP;
+            v[q] = (idx < BP * BP && i <= j && j < b) ? __ldcg(gsrc + i + static_cast<std::int64_t>(j) * ldg) : 0.0;
         }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int idx = base + q * nthr + tid;
+            if (idx >= BP * BP) continue;
+            const int j = idx / BP, i = idx - j * BP;
+            double x = v[q];
+            if (i <= j && j < b) dev = fmax(dev, fabs(x - (i == j ? 1.0 : 0.0)));
+            if (j >= b) x = (i == j) ? 1.0 : 0.0;
+            W[i * C::LD + j] = i <= j ? x : 0.0;
+        }
+    }
     for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_down_sync(0xffffffffu, dev, o));
     if (lane == 0) s_red[warp] = dev;
     if (tid == 0) s_bad = -1;
     __syncthreads();
     if (tid == 0) {
         double dv = 0.0;
-        for (int w = 0; w < kCholThreads / 32; ++w) dv = fmax(dv, s_red[w]);
-        s_dev = dv;
+        for (int w = 0; w < nthr / 32; ++w) dv = fmax(dv, s_red[w]);
+        s_dev = isfinite(dv) ? dv : INFINITY;
     }
     __syncthreads();
     if (s_dev <= kFirstOrderDev) {
-#pragma unroll
-        for (int a = 0; a < T; ++a)
-#pragma unroll
-            for (int c = 0; c < T; ++c) {
-                const int i = i0 + a, j = j0 + c;
-                if (side != 0 || i >= b || j >= b || i > j) continue;
-                const double e = i == j ? v[a][c] - 1.0 : v[a][c];
-                r[i + static_cast<std::int64_t>(j) * ldr] = i == j ? 1.0 + 0.5 * e : e;
-                rinv[i + static_cast<std::int64_t>(j) * ldr] = i == j ? 1.0 - 0.5 * e : -e;
-                if (i == j) { s_sq[i] = 1.0 + 0.5 * e; }
-            }
-        // zero strict lower parts
-        for (int idx = tid; idx < b * b; idx += kCholThreads) {
+        for (int idx = tid; idx < b * b; idx += nthr) {
             const int i = idx % b, j = idx / b;
-            if (i > j) {
-                r[i + static_cast<std::int64_t>(j) * ldr] = 0.0;
-                rinv[i + static_cast<std::int64_t>(j) * ldr] = 0.0;
+            double rv = 0.0, iv = 0.0;
+            if (i <= j) {
+                const double e = W[i * C::LD + j] - (i == j ? 1.0 : 0.0);
+                rv = (i == j) ? 1.0 + 0.5 * e : e;
+                iv = (i == j) ? 1.0 - 0.5 * e : -e;
+                if (i == j) dg[i] = rv;
             }
+            r[i + static_cast<std::int64_t>(j) * ldr] = rv;
+            rinv[i + static_cast<std::int64_t>(j) * ldr] = iv;
         }
     } else {
-        // Publication buffers start at zero: entries nobody publishes must read as 0.
-        for (int idx = tid; idx < 2 * kSmallMax; idx += kCholThreads) {
-            (&bufL[0][0])[idx] = 0.0;
-            (&bufR[0][0])[idx] = 0.0;
-        }
-        // The owners of row k publish their T entries of it: left side with entries j <= k
-        // zeroed (the pivot goes to s_sq[k], sanitised: a breakdown is recorded and the
-        // step continues with pivot 1), right side as is (its entries j > k are 0). The
-        // row is selected from registers by compile-time indices (no local memory).
-        auto publish = [&](int k, int buf) {
-            const int a = k - i0;
-            if (side < 0 || a < 0 || a >= T) return;
+        for (int pnl = 0; pnl < C::P; ++pnl) {
+            const int c0 = 16 * pnl, c1 = c0 + 16;
+            double* Dv = Dall + pnl * 16 * C::TLD;
+            if (warp == 0) {
+                // [D | I] elimination, one column per lane
+                const int j = lane & 15;
+                const bool left = lane < 16;
+                double x[16];
 #pragma unroll
-            for (int c = 0; c < T; ++c) {
-                double x = v[0][c];
+                for (int i = 0; i < 16; ++i)
+                    x[i] = left ? W[(c0 + min(i, j)) * C::LD + c0 + max(i, j)] : (i == j ? 1.0 : 0.0);
+                double pv[16];
 #pragma unroll
-                for (int aa = 1; aa < T; ++aa) x = (a == aa) ? v[aa][c] : x;
-                const int j = j0 + c;
-                if (side == 0) {
-                    if (j == k) {
-                        const bool bad = !(x > 0.0) || !isfinite(x);
-                        if (bad && s_bad < 0) s_bad = k;
-                        s_sq[k] = bad ? 1.0 : x;
+                for (int k = 0; k < 16; ++k) {
+                    double piv = __shfl_sync(0xffffffffu, x[k], k);
+                    const bool bad = !(piv > 0.0) || !isfinite(piv);
+                    if (bad) {
+                        if (lane == 0 && s_bad < 0 && c0 + k < b) s_bad = c0 + k;
+                        piv = 1.0;
+                        if (lane == k) x[k] = 1.0;
                     }
-                    bufL[buf][j] = j > k ? x : 0.0;
-                } else {
-                    bufR[buf][j] = x;
+                    pv[k] = piv;
+                    const double pinv = rcp_nr(piv);
+#pragma unroll
+                    for (int i = k + 1; i < 16; ++i) {
+                        const double f = __shfl_sync(0xffffffffu, x[i], k) * pinv;
+                        x[i] = fma(-f, x[k], x[i]);
+                    }
+                }
+                double rsq[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) rsq[k] = rsqrt_nr(pv[k]);  // independent: pipelined
+                // branch-free write-out (left lanes: row k of R_pp; right lanes: R_pp^{-1}(j, k) =
+                // (R_pp^{-T})(k, j) = E(k, j) / sqrt(piv_k), k >= j)
+                double* wcol = W + c0 * C::LD + c0 + j;
+                double* drow = Dv + j * C::TLD;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const double sq = pv[k] * rsq[k], v = x[k] * rsq[k];
+                    double* dst = left ? wcol + k * C::LD : drow + k;
+                    const double val = left ? (k == j ? sq : v) : (k >= j ? v : 0.0);
+                    if (!left || k <= j) *dst = val;
+                    if (lane == 0) dg[c0 + k] = sq;
                 }
             }
-        };
-        __syncthreads();
-        publish(0, 0);
-        __syncthreads();
-        for (int k = 0; k < b; ++k) {
-            const int p = k & 1;
-            // one branch-free update per step for both sides: rows i > k of the tile take
-            // f_i = G(k, i) / piv_k times the published row k (left: G, right: the R^{-T} part)
-            if (side >= 0 && i0 + T - 1 > k) {
-                const double pinv = rcp_nr(s_sq[k]);
-                const double* rb = side == 0 ? bufL[p] : bufR[p];
-                double f[T], rowk[T];
-#pragma unroll
-                for (int a = 0; a < T; ++a) f[a] = (i0 + a > k) ? bufL[p][i0 + a] * pinv : 0.0;
-#pragma unroll
-                for (int c = 0; c < T; ++c) rowk[c] = rb[j0 + c];
-#pragma unroll
-                for (int a = 0; a < T; ++a)
-#pragma unroll
-                    for (int c = 0; c < T; ++c) v[a][c] = fma(-f[a], rowk[c], v[a][c]);
+            __syncthreads();
+            if (c1 < BP) {
+                // 2. row panel (in place): W[c0+m][c1+n] = sum_k Rinv_pp(k, m) W[c0+k][c1+n]
+                const int nf = (BP - c1) / 8;
+                if (warp < 8)
+                    for (int ni = warp; ni < nf; ni += 8)
+                        ct_frag(Dv, 1, C::TLD, W + c0 * C::LD + c1, C::LD, 1, W + c0 * C::LD + c1, C::LD, 0, ni, 0, 16,
+                                1.0, false);
+                __syncthreads();
+                // 3. trailing update on upper fragments: W[c1+m][c1+n] -= sum_k W[c0+k][c1+m] W[c0+k][c1+n]
+                const int nb8 = (BP - c1) / 8;
+                int nfu = 0;
+                for (int mi = 0; mi < (BP - c1) / 16; ++mi) nfu += nb8 - 2 * mi;
+                if (warp < 8)
+                    for (int f = warp; f < nfu; f += 8) {
+                        int e = f, mi = 0;
+                        while (e >= nb8 - 2 * mi) { e -= nb8 - 2 * mi; ++mi; }
+                        const int ni = 2 * mi + e;
+                        ct_frag(W + c0 * C::LD + c1, 1, C::LD, W + c0 * C::LD + c1, C::LD, 1, W + c1 * C::LD + c1, C::LD,
+                                mi, ni, 0, 16, -1.0, true);
+                    }
+                __syncthreads();
             }
-            if (k + 1 < b) publish(k + 1, p ^ 1);
+        }
+        // R out
+        for (int idx = tid; idx < b * b; idx += nthr) {
+            const int i = idx % b, j = idx / b;
+            r[i + static_cast<std::int64_t>(j) * ldr] = i <= j ? W[i * C::LD + j] : 0.0;
+        }
+        __syncthreads();
+        // in-place inversion, block column by block column
+        for (int jb = 0; jb < C::P; ++jb) {
+            const int cj = 16 * jb;
+            const double* Dj = Dall + jb * 16 * C::TLD;
+            if (jb > 0) {
+                // T[0:cj][0:16] = R[0:cj][cj:cj+16] * Rinv_jj
+                const int nfr = jb * 2;
+                if (warp < 8)
+                    for (int f = warp; f < nfr; f += 8)
+                        ct_frag(W + cj, C::LD, 1, Dj, C::TLD, 1, Tm, C::TLD, f >> 1, f & 1, 0, 16, 1.0, false);
+                __syncthreads();
+                // W[0:cj][cj:cj+16] = -Rinv[0:cj][0:cj] * T  (Rinv upper: k from 16 mi)
+                if (warp < 8)
+                    for (int f = warp; f < nfr; f += 8) {
+                        const int mi = f >> 1;
+                        ct_frag(W, C::LD, 1, Tm, C::TLD, 1, W + cj, C::LD, mi, f & 1, 16 * mi, cj, -1.0, false);
+                    }
+            }
+            for (int idx = tid; idx < 256; idx += nthr) {
+                const int i = idx >> 4, k = idx & 15;
+                W[(cj + i) * C::LD + cj + k] = Dj[i * C::TLD + k];
+            }
             __syncthreads();
         }
-        for (int k = tid; k < b; k += kCholThreads) {
-            const double sq = sqrt(s_sq[k]);
-            s_sq[k] = sq;
-            s_rsq[k] = 1.0 / sq;
+        for (int idx = tid; idx < b * b; idx += nthr) {
+            const int i = idx % b, j = idx / b;
+            rinv[i + static_cast<std::int64_t>(j) * ldr] = i <= j ? W[i * C::LD + j] : 0.0;
         }
-        __syncthreads();
-        // row k of the result = row k / sqrt(piv_k); right part transposed into R^{-1}
-#pragma unroll
-        for (int a = 0; a < T; ++a)
-#pragma unroll
-            for (int c = 0; c < T; ++c) {
-                const int i = i0 + a, j = j0 + c;
-                if (side < 0 || i >= b || j >= b) continue;
-                if (side == 0) {
-                    if (i <= j) r[i + static_cast<std::int64_t>(j) * ldr] = i == j ? s_sq[i] : v[a][c] * s_rsq[i];
-                    else r[i + static_cast<std::int64_t>(j) * ldr] = 0.0;
-                } else {
-                    if (j <= i) rinv[j + static_cast<std::int64_t>(i) * ldr] = v[a][c] * s_rsq[i];
-                    if (j < i) {
-                        rinv[i + static_cast<std::int64_t>(j) * ldr] = 0.0;
-                        r[i + static_cast<std::int64_t>(j) * ldr] = 0.0;
-                    }
-                }
-            }
     }
     __syncthreads();
     if (warp == 0 && status) {
         double dmin = INFINITY, dmax = 0.0;
         for (int j = lane; j < b; j += 32) {
-            dmin = fmin(dmin, s_sq[j]);
-            dmax = fmax(dmax, s_sq[j]);
+            dmin = fmin(dmin, dg[j]);
+            dmax = fmax(dmax, dg[j]);
         }
         for (int o = 16; o > 0; o >>= 1) {
             dmin = fmin(dmin, __shfl_down_sync(0xffffffffu, dmin, o));
@@ -344,13 +406,15 @@ __device__ __noinline__ void chol_small_block(const double* __restrict__ g, std:
             status->gram_dev = s_dev;
         }
     }
+    __syncthreads();
 }
 
-template <int T>
+template <int BP>
 __global__ void __launch_bounds__(kCholThreads)
 chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double* __restrict__ r,
                   double* __restrict__ rinv, std::int64_t ldr, SmallStatus* status) {
-    chol_small_block<T>(g, ldg, b, r, rinv, ldr, status);
+    extern __shared__ __align__(16) double ch_smem[];
+    chol_tile_block<BP>(g, ldg, b, r, rinv, ldr, status, ch_smem);
 }
 
 // ---- blocked Cholesky + inverse of an l x l Gram in ONE cooperative launch -----------
@@ -367,13 +431,6 @@ chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double*
 // F (in `rinv`, zero-initialised) ends as R^{-1}: the right half of the elimination of
 // [W | I] kept transposed (F_kk = R_kk^{-1} from phase 1). Two grid barriers per step
 // instead of ~5 dependent launches per 64-column panel.
-__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
-        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
-        : "d"(a0), "d"(a1), "d"(b0));
-}
-
 constexpr int kCwNb = 64;
 constexpr int kCwLd = 68;   // padded shared stride (= 4 mod 16 doubles: conflict-free fragments)
 constexpr int kCwSmemBytes = 2 * kCwNb * kCwLd * 8;
@@ -484,7 +541,8 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
     auto F = [&](int i, int j) { return p.rinv + static_cast<std::int64_t>(i) * kCwNb + static_cast<std::int64_t>(j) * kCwNb * p.ldr; };
     // item e >= 1 of a phase -> CTA 1 + (e-1) % (G-1); item 0 (phase 3: W_{k+1,k+1}) -> CTA 0
     const int e_first = G == 1 ? 1 : cta, e_step = G == 1 ? 1 : G - 1;
-    if (cta == 0) chol_small_block<4>(W(0, 0), p.ldw, sz(0), R(0, 0), F(0, 0), p.ldr, p.stats);
+    static_assert(CholCfg<64>::SMEM <= kCwSmemBytes, "chol workspace");
+    if (cta == 0) chol_tile_block<64>(W(0, 0), p.ldw, sz(0), R(0, 0), F(0, 0), p.ldr, p.stats, cw_smem);
     grid.sync();
     for (int k = 0; k < nt; ++k) {
         const int bk = sz(k);
@@ -521,8 +579,8 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
                 cw_tile_gemm(cw_smem, F(pp, k), 1, p.ldr, R(k, i), 1, p.ldr, F(pp, i), p.ldr, sz(pp), sz(i), bk, -1.0, 1.0);
             }
             if (e == 0)
-                chol_small_block<4>(W(k + 1, k + 1), p.ldw, sz(k + 1), R(k + 1, k + 1), F(k + 1, k + 1), p.ldr,
-                                    p.stats + k + 1);
+                chol_tile_block<64>(W(k + 1, k + 1), p.ldw, sz(k + 1), R(k + 1, k + 1), F(k + 1, k + 1), p.ldr,
+                                    p.stats + k + 1, cw_smem);
         }
         grid.sync();
     }
@@ -536,6 +594,33 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
 // the upper fragments only, written per CTA and reduced over CTAs in a fixed order (so the
 // result is deterministic for a given device); the b x b Choleskies run on CTA 0 between
 // grid barriers. Phase B writes T1 and accumulates its Gram from the same registers.
+// Sub-tiles stream through a STAGES-deep cp.async ring (~64 KB of rows in flight per SM).
+// Grid-wide barrier for cooperative launches (all CTAs co-resident): an arrival counter and
+// a generation word in global memory (bar[0], bar[1]; zero-initialised once per context).
+// Waiting CTAs poll with __nanosleep backoff so the CTA doing serial work between barriers
+// (the Cholesky on CTA 0) does not compete with a storm of polling loads.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            unsigned ns = 32;
+            while (*gen == g) {
+                __nanosleep(ns);
+                ns = ns < 512 ? 2 * ns : 512;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 struct PanelArgs {
     const double* y;
     std::int64_t ldy;
@@ -548,89 +633,129 @@ struct PanelArgs {
     double* g;     // b x b Gram (ld kSmallMax)
     double *ra, *rainv, *rb, *rbinv;  // ld kSmallMax
     SmallStatus *st0, *st1;
+    unsigned* gbar;  // grid barrier words
 };
 
 template <int BP>
 struct PanelCfg {
-    static constexpr int SUB = BP > 96 ? 32 : 64;  // rows per sub-tile (two buffers + R fit in 227 KB)
-    static constexpr int LD = BP + 4;              // = 4 mod 16 doubles (BP multiple of 16)
-    static constexpr int MI = SUB / 16;            // m16 blocks per sub-tile
-    static constexpr int NG = 8 / MI;              // warps sharing one m16 block
+    static constexpr int SUB = BP >= 96 ? 32 : 64;  // rows per sub-tile
+    static constexpr int LD = BP + 4;               // = 4 mod 16 doubles (BP multiple of 16)
+    static constexpr int MI = SUB / 16;             // m16 blocks per sub-tile
+    static constexpr int NG = 8 / MI;               // warps sharing one m16 block
     static constexpr int NFG = (BP / 16) * (BP / 8) - (BP / 16) * (BP / 16 - 1);  // upper Gram fragments
     static constexpr int MAXG = (NFG + 7) / 8;
     static constexpr int MAXT = (BP / 8 + NG - 1) / NG;  // product fragments per warp: mi = w % MI, ni = w / MI + NG j
-    static constexpr int SMEM = (2 * SUB + BP) * LD * 8;
+    // independent accumulator chains per fragment along k (the FP64 MMA pipe needs ~40
+    // MMAs in flight per SM to cover its latency)
+    static constexpr int KSG = MAXG >= 5 ? 1 : (MAXG >= 3 ? 2 : 4);
+    static constexpr int KST = MAXT >= 5 ? 1 : 2;
+    // sub-tile copies in flight: as many as fit next to the triangular factor (~64 KB of rows)
+    static constexpr int STAGES = (4 * SUB + BP) * LD * 8 <= 220 * 1024 ? 4 : 3;
+    static constexpr int SMEM = (STAGES * SUB + BP) * LD * 8;
 };
 
-// Asynchronous variant: 8-byte cp.async copies (zero-filled out of range) into ys;
-// the caller commits / waits (double-buffered sub-tiles).
+// Asynchronous copy of one sub-tile into ys (zero-filled outside rows x b): 16-byte
+// cp.async chunks when every row start is 16-byte aligned and b is even, 8-byte ones
+// otherwise. Commits one group.
 template <int BP>
 __device__ __forceinline__ void panel_stage_async(double* ys, const double* __restrict__ src, std::int64_t ld,
-                                                  std::int64_t r0, std::int64_t rows, int b) {
+                                                  std::int64_t r0, std::int64_t rows, int b, bool vec2) {
     using C = PanelCfg<BP>;
-    for (int idx = threadIdx.x; idx < C::SUB * BP; idx += blockDim.x) {
-        const int r = idx / BP, c = idx - r * BP;
-        const std::int64_t gr = r0 + r;
-        const bool ok = gr < rows && c < b;
-        const double* s = ok ? src + gr * ld + c : src;
-        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(ys + r * C::LD + c));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(s), "r"(ok ? 8 : 0) : "memory");
+    if (vec2) {
+        for (int idx = threadIdx.x; idx < C::SUB * BP / 2; idx += blockDim.x) {
+            const int r = idx / (BP / 2), c = 2 * (idx - r * (BP / 2));
+            const std::int64_t gr = r0 + r;
+            const bool ok = gr < rows && c < b;
+            const double* s = ok ? src + gr * ld + c : src;
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(ys + r * C::LD + c));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(s), "r"(ok ? 16 : 0) : "memory");
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < C::SUB * BP; idx += blockDim.x) {
+            const int r = idx / BP, c = idx - r * BP;
+            const std::int64_t gr = r0 + r;
+            const bool ok = gr < rows && c < b;
+            const double* s = ok ? src + gr * ld + c : src;
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(ys + r * C::LD + c));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(s), "r"(ok ? 8 : 0) : "memory");
+        }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// acc += Ys^T Ys on this warp's upper fragments
+// acc += Ys^T Ys on this warp's upper fragments (KSG interleaved chains along the rows)
 template <int BP>
-__device__ __forceinline__ void panel_gram(const double* ys, double (&acc)[PanelCfg<BP>::MAXG][4],
+__device__ __forceinline__ void panel_gram(const double* ys, double (&acc)[PanelCfg<BP>::MAXG][PanelCfg<BP>::KSG][4],
                                            const int (&fm)[PanelCfg<BP>::MAXG], const int (&fn)[PanelCfg<BP>::MAXG]) {
     using C = PanelCfg<BP>;
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-#pragma unroll 4
-    for (int kk = 0; kk < C::SUB; kk += 4) {
-        const double* row = ys + (kk + t) * C::LD;  // A = Ys^T: a(m, k) = Ys(k, m)
+#pragma unroll 2
+    for (int kk = 0; kk < C::SUB; kk += 4 * C::KSG) {
 #pragma unroll
-        for (int f = 0; f < C::MAXG; ++f) {
-            if (fm[f] < 0) continue;
-            dmma_16x8x4(acc[f], row[16 * fm[f] + g], row[16 * fm[f] + g + 8], row[8 * fn[f] + g]);
+        for (int c = 0; c < C::KSG; ++c) {
+            const double* row = ys + (kk + 4 * c + t) * C::LD;  // A = Ys^T: a(m, k) = Ys(k, m)
+#pragma unroll
+            for (int f = 0; f < C::MAXG; ++f) {
+                if (fm[f] < 0) continue;
+                dmma_16x8x4(acc[f][c], row[16 * fm[f] + g], row[16 * fm[f] + g + 8], row[8 * fn[f] + g]);
+            }
         }
     }
 }
 
 // out fragments = Ys (SUB x BP) * Rs (BP x BP, upper), mi = warp % MI, ni = warp / MI + NG j
+// (KST interleaved chains along k, summed at the end)
 template <int BP>
-__device__ __forceinline__ void panel_trmm(const double* ys, const double* rs, double (&acc)[PanelCfg<BP>::MAXT][4],
+__device__ __forceinline__ void panel_trmm(const double* ys, const double* rs, double (&out)[PanelCfg<BP>::MAXT][4],
                                            int b) {
     using C = PanelCfg<BP>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int mi = warp % C::MI, h = warp / C::MI;
     const int nb8 = (b + 7) >> 3, kmax = (b + 3) & ~3;
+    double acc[C::MAXT][C::KST][4];
 #pragma unroll
     for (int j = 0; j < C::MAXT; ++j)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
-#pragma unroll 4
-    for (int kk = 0; kk < kmax; kk += 4) {
-        const double a0 = ys[(16 * mi + g) * C::LD + kk + t];
-        const double a1 = ys[(16 * mi + g + 8) * C::LD + kk + t];
+        for (int c = 0; c < C::KST; ++c)
 #pragma unroll
-        for (int j = 0; j < C::MAXT; ++j) {
-            const int ni = h + C::NG * j;
-            // R^{-1} upper: column block ni needs k < 8 ni + 8; blocks past b are zero
-            if (ni >= nb8 || kk >= 8 * ni + 8) continue;
-            dmma_16x8x4(acc[j], a0, a1, rs[(kk + t) * C::LD + 8 * ni + g]);
+            for (int e = 0; e < 4; ++e) acc[j][c][e] = 0.0;
+#pragma unroll 2
+    for (int k0 = 0; k0 < kmax; k0 += 4 * C::KST) {
+#pragma unroll
+        for (int c = 0; c < C::KST; ++c) {
+            const int kk = k0 + 4 * c;
+            if (kk >= kmax) continue;
+            const double a0 = ys[(16 * mi + g) * C::LD + kk + t];
+            const double a1 = ys[(16 * mi + g + 8) * C::LD + kk + t];
+#pragma unroll
+            for (int j = 0; j < C::MAXT; ++j) {
+                const int ni = h + C::NG * j;
+                // R^{-1} upper: column block ni needs k < 8 ni + 8; blocks past b are zero
+                if (ni >= nb8 || kk >= 8 * ni + 8) continue;
+                dmma_16x8x4(acc[j][c], a0, a1, rs[(kk + t) * C::LD + 8 * ni + g]);
+            }
         }
     }
+#pragma unroll
+    for (int j = 0; j < C::MAXT; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            double v = acc[j][0][e];
+#pragma unroll
+            for (int c = 1; c < C::KST; ++c) v += acc[j][c][e];
+            out[j][e] = v;
+        }
 }
 
-template <int BP, int T>
+template <int BP>
 __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArgs p) {
     using C = PanelCfg<BP>;
     extern __shared__ __align__(16) double psm[];
-    double* ys2 = psm;                        // two SUB x LD sub-tile buffers
-    double* rs = psm + 2 * C::SUB * C::LD;    // BP x LD triangular factor
-    cg::grid_group grid = cg::this_grid();
+    double* ys2 = psm;                              // STAGES sub-tile buffers (SUB x LD)
+    double* rs = psm + C::STAGES * C::SUB * C::LD;  // BP x LD triangular factor
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const bool mma_warp = warp < 8;
@@ -650,12 +775,14 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
         fm[f] = mi;
         fn[f] = 2 * mi + e;
     }
-    double acc[C::MAXG][4];
+    double acc[C::MAXG][C::KSG][4];
     auto zero_acc = [&]() {
 #pragma unroll
         for (int f = 0; f < C::MAXG; ++f)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) acc[f][e] = 0.0;
+            for (int c = 0; c < C::KSG; ++c)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[f][c][e] = 0.0;
     };
     auto write_part = [&]() {
         double* dst = p.part + static_cast<std::size_t>(cta) * BP * BP;
@@ -665,7 +792,10 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int row = 16 * fm[f] + g + (e >= 2 ? 8 : 0), col = 8 * fn[f] + 2 * t + (e & 1);
-                dst[row + col * BP] = acc[f][e];
+                double v = acc[f][0][e];
+#pragma unroll
+                for (int c = 1; c < C::KSG; ++c) v += acc[f][c][e];
+                dst[row + col * BP] = v;
             }
         }
     };
@@ -685,23 +815,27 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
             rs[k * C::LD + n] = (k < p.b && n < p.b && k <= n) ? __ldcg(rinv + k + n * kSmallMax) : 0.0;
         }
     };
-    // sub-tile loop with the next sub-tile's copy in flight (two shared buffers)
+    // sub-tile loop with STAGES-1 sub-tile copies in flight (one cp.async group per
+    // sub-tile, empty groups past the end keep the group count uniform)
     auto sub_loop = [&](const double* src, std::int64_t ld, auto&& body) {
+        const bool vec2 = (ld % 2 == 0) && (p.b % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(src) & 15) == 0);
+        auto buf = [&](int i) { return ys2 + (i % C::STAGES) * C::SUB * C::LD; };
+        auto issue = [&](int i) {
+            const int sub = cta + i * G;
+            if (sub < p.nsub) panel_stage_async<BP>(buf(i), src, ld, static_cast<std::int64_t>(sub) * C::SUB, p.rows, p.b, vec2);
+            else cp_async_commit();
+        };
+#pragma unroll
+        for (int i = 0; i < C::STAGES - 1; ++i) issue(i);
         int i = 0;
-        if (cta < p.nsub) panel_stage_async<BP>(ys2, src, ld, static_cast<std::int64_t>(cta) * C::SUB, p.rows, p.b);
         for (int sub = cta; sub < p.nsub; sub += G, ++i) {
-            double* cur = ys2 + (i & 1) * C::SUB * C::LD;
-            double* nxt = ys2 + ((i + 1) & 1) * C::SUB * C::LD;
-            if (sub + G < p.nsub) {
-                panel_stage_async<BP>(nxt, src, ld, static_cast<std::int64_t>(sub + G) * C::SUB, p.rows, p.b);
-                cp_async_wait_1();
-            } else {
-                cp_async_wait_0();
-            }
+            issue(i + C::STAGES - 1);
+            cp_async_wait<C::STAGES - 1>();
             __syncthreads();
-            body(cur, static_cast<std::int64_t>(sub) * C::SUB);
+            body(buf(i), static_cast<std::int64_t>(sub) * C::SUB);
             __syncthreads();
         }
+        cp_async_wait<0>();
     };
     // ---- phase A: Gram of Y
     zero_acc();
@@ -709,11 +843,12 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
         if (mma_warp) panel_gram<BP>(cur, acc, fm, fn);
     });
     if (mma_warp) write_part();
-    grid.sync();
+    grid_barrier(p.gbar, G);
     reduce_parts();
-    grid.sync();
-    if (cta == 0) chol_small_block<T>(p.g, kSmallMax, p.b, p.ra, p.rainv, kSmallMax, p.st0);
-    grid.sync();
+    grid_barrier(p.gbar, G);
+    static_assert(CholCfg<BP>::SMEM <= C::SMEM, "chol workspace");
+    if (cta == 0) chol_tile_block<BP>(p.g, kSmallMax, p.b, p.ra, p.rainv, kSmallMax, p.st0, psm);
+    grid_barrier(p.gbar, G);
     // ---- phase B: T1 = Y Ra^{-1} (written out) and the Gram of T1
     stage_r(p.rainv);
     zero_acc();
@@ -737,11 +872,11 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
         if (mma_warp) panel_gram<BP>(cur, acc, fm, fn);
     });
     if (mma_warp) write_part();
-    grid.sync();
+    grid_barrier(p.gbar, G);
     reduce_parts();
-    grid.sync();
-    if (cta == 0) chol_small_block<T>(p.g, kSmallMax, p.b, p.rb, p.rbinv, kSmallMax, p.st1);
-    grid.sync();
+    grid_barrier(p.gbar, G);
+    if (cta == 0) chol_tile_block<BP>(p.g, kSmallMax, p.b, p.rb, p.rbinv, kSmallMax, p.st1, psm);
+    grid_barrier(p.gbar, G);
     // ---- phase D: Q = T1 Rb^{-1}
     stage_r(p.rbinv);
     sub_loop(p.t1, p.b, [&](double* cur, std::int64_t r0) {
@@ -1034,13 +1169,31 @@ void column_sumsq(cudaStream_t st, Workspace& ws, const MatView& v, double* out)
     QB_LAUNCH_CHECK();
 }
 
+template <int BP>
+void launch_chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, double* r, double* rinv,
+                       std::int64_t ldr, SmallStatus* status) {
+    static bool configured = false;
+    if (!configured) {
+        QB_CUDA(cudaFuncSetAttribute(chol_small_kernel<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     CholCfg<BP>::SMEM));
+        configured = true;
+    }
+    chol_small_kernel<BP><<<1, kCholThreads, CholCfg<BP>::SMEM, st>>>(g, ldg, b, r, rinv, ldr, status);
+}
+
 void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, double* r, double* rinv,
                 std::int64_t ldr, SmallStatus* status) {
     if (b < 1 || b > kSmallMax) throw QbError(kDimensionError, "chol_small: block width out of range");
     // tile edge T with 16 * T >= b
-    if (b <= 32) chol_small_kernel<2><<<1, kCholThreads, 0, st>>>(g, ldg, b, r, rinv, ldr, status);
-    else if (b <= 64) chol_small_kernel<4><<<1, kCholThreads, 0, st>>>(g, ldg, b, r, rinv, ldr, status);
-    else chol_small_kernel<7><<<1, kCholThreads, 0, st>>>(g, ldg, b, r, rinv, ldr, status);
+    switch (static_cast<int>(round_up(b, 16))) {
+        case 16: launch_chol_small<16>(st, g, ldg, b, r, rinv, ldr, status); break;
+        case 32: launch_chol_small<32>(st, g, ldg, b, r, rinv, ldr, status); break;
+        case 48: launch_chol_small<48>(st, g, ldg, b, r, rinv, ldr, status); break;
+        case 64: launch_chol_small<64>(st, g, ldg, b, r, rinv, ldr, status); break;
+        case 80: launch_chol_small<80>(st, g, ldg, b, r, rinv, ldr, status); break;
+        case 96: launch_chol_small<96>(st, g, ldg, b, r, rinv, ldr, status); break;
+        default: launch_chol_small<112>(st, g, ldg, b, r, rinv, ldr, status); break;
+    }
     QB_LAUNCH_CHECK();
 }
 
@@ -1061,10 +1214,10 @@ void chol_wide(cudaStream_t st, double* w, std::int64_t ldw, int l, double* r, d
     QB_LAUNCH_CHECK();
 }
 
-template <int BP, int T>
+template <int BP>
 void launch_cholqr2_panel(cudaStream_t st, PanelArgs& a, int grid_cap) {
     using C = PanelCfg<BP>;
-    auto kern = cholqr2_panel_kernel<BP, T>;
+    auto kern = cholqr2_panel_kernel<BP>;
     a.nsub = static_cast<int>(ceil_div(a.rows, C::SUB));
     static int per_sm = 0;
     if (!per_sm) {
@@ -1080,22 +1233,22 @@ void launch_cholqr2_panel(cudaStream_t st, PanelArgs& a, int grid_cap) {
 
 void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t rows, int b, std::int64_t ldy,
                    double* t1, double* q, std::int64_t ldq, double* g, double* ra, double* rainv, double* rb,
-                   double* rbinv, SmallStatus* st0, SmallStatus* st1) {
+                   double* rbinv, SmallStatus* st0, SmallStatus* st1, unsigned* gbar) {
     if (b < 1 || b > kSmallMax) throw QbError(kDimensionError, "cholqr2_panel: width out of range");
     const int bp = static_cast<int>(round_up(b, 16));
     PanelArgs a{};
     a.y = y; a.ldy = ldy; a.t1 = t1; a.q = q; a.ldq = ldq; a.rows = rows; a.b = b;
-    a.g = g; a.ra = ra; a.rainv = rainv; a.rb = rb; a.rbinv = rbinv; a.st0 = st0; a.st1 = st1;
+    a.g = g; a.ra = ra; a.rainv = rainv; a.rb = rb; a.rbinv = rbinv; a.st0 = st0; a.st1 = st1; a.gbar = gbar;
     const int cap = gemm_num_sms();
     a.part = ws.get(static_cast<std::size_t>(cap) * bp * bp);
     switch (bp) {
-        case 16: launch_cholqr2_panel<16, 2>(st, a, cap); break;
-        case 32: launch_cholqr2_panel<32, 2>(st, a, cap); break;
-        case 48: launch_cholqr2_panel<48, 4>(st, a, cap); break;
-        case 64: launch_cholqr2_panel<64, 4>(st, a, cap); break;
-        case 80: launch_cholqr2_panel<80, 7>(st, a, cap); break;
-        case 96: launch_cholqr2_panel<96, 7>(st, a, cap); break;
-        default: launch_cholqr2_panel<112, 7>(st, a, cap); break;
+        case 16: launch_cholqr2_panel<16>(st, a, cap); break;
+        case 32: launch_cholqr2_panel<32>(st, a, cap); break;
+        case 48: launch_cholqr2_panel<48>(st, a, cap); break;
+        case 64: launch_cholqr2_panel<64>(st, a, cap); break;
+        case 80: launch_cholqr2_panel<80>(st, a, cap); break;
+        case 96: launch_cholqr2_panel<96>(st, a, cap); break;
+        default: launch_cholqr2_panel<112>(st, a, cap); break;
     }
 }
 
