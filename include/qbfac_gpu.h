@@ -136,6 +136,31 @@ int qbfac_gpu_matrix_csr(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, int64_t nnz, 
 int qbfac_gpu_matrix_csr_shard(qbfac_gpu_ctx* ctx, int64_t m_global, int64_t row0, int64_t m_local,
                                int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
                                const double* values, qbfac_gpu_matrix** out);
+/* ---- Matrix Market ingest / export (CSR built as
+ * SparseCsrMatrix::from_triplets, sparse_csr.cpp:42-64). Host-only helpers (no
+ * device needed): coordinate or array, real/integer, general; any other banner ->
+ * QBFAC_FORMAT_ERROR; duplicate or out-of-range coordinates -> QBFAC_FORMAT_ERROR;
+ * non-finite values -> QBFAC_ERROR. Two-phase: info, then read into caller buffers
+ * (row_ptr m+1, col_idx/values nnz; dense: column-major with lda >= m). Writers emit
+ * shortest round-trip decimal, so write -> read reproduces every double exactly.
+ * Messages of these context-free calls: qbfac_mtx_last_error(). */
+const char* qbfac_mtx_last_error(void);
+int qbfac_mtx_info(const char* path, int* coordinate, int64_t* m, int64_t* n, int64_t* nnz);
+int qbfac_mtx_read_csr(const char* path, int64_t* row_ptr, int32_t* col_idx, double* values);
+int qbfac_mtx_read_dense(const char* path, double* a, int64_t lda);
+int qbfac_mtx_write_csr(const char* path, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                        const int32_t* col_idx, const double* values);
+int qbfac_mtx_write_dense(const char* path, int64_t m, int64_t n, const double* a, int64_t lda);
+/* read_matrix_market(path) -> MatrixHandle on the device (coordinate -> CSR plus its
+ * device-built transpose, array -> dense). */
+int qbfac_gpu_matrix_mtx(qbfac_gpu_ctx* ctx, const char* path, qbfac_gpu_matrix** out);
+/* shape of a handle and copies of its device arrays back to the host (the reference's
+ * MatrixHandle::matrix() accessors, matrix_handle.hpp:58-74) */
+int qbfac_gpu_matrix_shape(const qbfac_gpu_matrix* mat, int* sparse, int64_t* m, int64_t* n, int64_t* nnz);
+int qbfac_gpu_matrix_export_csr(qbfac_gpu_ctx* ctx, const qbfac_gpu_matrix* mat, int64_t* row_ptr, int32_t* col_idx,
+                                double* values);
+int qbfac_gpu_matrix_export_dense(qbfac_gpu_ctx* ctx, const qbfac_gpu_matrix* mat, double* a, int64_t lda);
+
 void qbfac_gpu_matrix_free(qbfac_gpu_matrix* mat);
 /* Passes counted on this handle so far (PassCounter, matrix_handle.hpp:20-27). */
 int64_t qbfac_gpu_matrix_passes(const qbfac_gpu_matrix* mat);

@@ -75,6 +75,7 @@ def lib():
         L.qbo_csr_frob_sq.argtypes = [I64, I64, I64, P, P, P]
         L.qbo_csr_frob_sq.restype = D
         L.qbo_csr_validate.argtypes = [I64, I64, I64, P, P, P, I64]
+        L.qbo_csr_from_triplets.argtypes = [I64, I64, I64, P, P, P, P, P, P]
         L.qbo_run_dense.argtypes = [I64, I64, P, P, P]
         L.qbo_run_dense.restype = P
         L.qbo_run_csr.argtypes = [I64, I64, I64, P, P, P, P, P]
@@ -207,6 +208,18 @@ def csr_validate(m, n, rp, ci, v) -> str:
     ci = np.ascontiguousarray(ci, dtype=np.int32)
     v = np.ascontiguousarray(v, dtype=np.float64)
     return STATUS[lib().qbo_csr_validate(m, n, len(v), _p(rp), _p(ci), _p(v), len(rp))]
+
+
+def csr_from_triplets(m, n, rows, cols, vals):
+    """SparseCsrMatrix::from_triplets (sparse_csr.cpp:42-64) -> (status, rp, ci, v)."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    cols = np.ascontiguousarray(cols, dtype=np.int64)
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    rp = np.zeros(m + 1, dtype=np.int64)
+    ci = np.zeros(max(len(vals), 1), dtype=np.int32)
+    v = np.zeros(max(len(vals), 1), dtype=np.float64)
+    st = lib().qbo_csr_from_triplets(m, n, len(vals), _p(rows), _p(cols), _p(vals), _p(rp), _p(ci), _p(v))
+    return STATUS[st], rp, ci[:len(vals)], v[:len(vals)]
 
 
 # ---- algorithms ----------------------------------------------------------------

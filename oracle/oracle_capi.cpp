@@ -253,6 +253,24 @@ int qbo_csr_validate(std::int64_t m, std::int64_t n, std::int64_t nnz, const std
     });
 }
 
+// SparseCsrMatrix::from_triplets (sparse_csr.cpp:42-64): sort by (row, col), reject duplicates
+// and out-of-range coordinates, then from_parts validation. Outputs the CSR arrays.
+int qbo_csr_from_triplets(std::int64_t m, std::int64_t n, std::int64_t nt, const std::int64_t* rows,
+                          const std::int64_t* cols, const double* vals, std::int64_t* rp, std::int32_t* ci,
+                          double* v) {
+    qbo_result res{};
+    return guard(&res, [&] {
+        std::vector<SparseCsrMatrix::Triplet> t(static_cast<std::size_t>(nt));
+        for (std::int64_t i = 0; i < nt; ++i)
+            t[i] = SparseCsrMatrix::Triplet{static_cast<qbfac::index>(rows[i]), static_cast<qbfac::index>(cols[i]),
+                                            vals[i]};
+        SparseCsrMatrix a = SparseCsrMatrix::from_triplets(m, n, std::move(t));
+        std::memcpy(rp, a.row_ptr().data(), sizeof(std::int64_t) * (m + 1));
+        std::memcpy(ci, a.col_idx().data(), sizeof(std::int32_t) * a.nnz());
+        std::memcpy(v, a.values().data(), sizeof(double) * a.nnz());
+    });
+}
+
 // ---- algorithms --------------------------------------------------------------
 void* qbo_run_dense(std::int64_t m, std::int64_t n, const double* a, const qbo_params* p,
                     qbo_result* res) {

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/qbfac_gpu.h"
+#include "mtx.cuh"
 #include "qb.cuh"
 
 struct qbfac_gpu_ctx {
@@ -138,6 +139,110 @@ int qbfac_gpu_matrix_csr_shard(qbfac_gpu_ctx* ctx, int64_t m_global, int64_t row
         h->ctx = ctx;
         h->m = qbgpu::make_csr(*ctx->c, m_global, row0, m_local, n, nnz, row_ptr, col_idx, values);
         *out = h.release();
+    });
+}
+
+// ---- Matrix Market and matrix export ------------------------------------
+const char* qbfac_mtx_last_error(void) { return g_create_error.c_str(); }
+
+int qbfac_mtx_info(const char* path, int* coordinate, int64_t* m, int64_t* n, int64_t* nnz) {
+    return guard(nullptr, [&] {
+        const auto i = qbgpu::mtx_info(path);
+        *coordinate = i.coordinate ? 1 : 0;
+        *m = i.m;
+        *n = i.n;
+        *nnz = i.nnz;
+    });
+}
+
+int qbfac_mtx_read_csr(const char* path, int64_t* row_ptr, int32_t* col_idx, double* values) {
+    return guard(nullptr, [&] {
+        qbgpu::MtxInfo i{};
+        std::vector<int64_t> rp;
+        std::vector<int32_t> ci;
+        std::vector<double> v;
+        qbgpu::mtx_read_csr(path, i, rp, ci, v);
+        std::memcpy(row_ptr, rp.data(), sizeof(int64_t) * rp.size());
+        if (!v.empty()) {
+            std::memcpy(col_idx, ci.data(), sizeof(int32_t) * ci.size());
+            std::memcpy(values, v.data(), sizeof(double) * v.size());
+        }
+    });
+}
+
+int qbfac_mtx_read_dense(const char* path, double* a, int64_t lda) {
+    return guard(nullptr, [&] {
+        qbgpu::MtxInfo i{};
+        std::vector<double> v;
+        qbgpu::mtx_read_dense(path, i, v);
+        for (int64_t j = 0; j < i.n; ++j)
+            for (int64_t r = 0; r < i.m; ++r) a[r + j * lda] = v[static_cast<size_t>(r + j * i.m)];
+    });
+}
+
+int qbfac_mtx_write_csr(const char* path, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                        const int32_t* col_idx, const double* values) {
+    return guard(nullptr, [&] { qbgpu::mtx_write_csr(path, m, n, nnz, row_ptr, col_idx, values); });
+}
+
+int qbfac_mtx_write_dense(const char* path, int64_t m, int64_t n, const double* a, int64_t lda) {
+    return guard(nullptr, [&] { qbgpu::mtx_write_dense(path, m, n, a, lda); });
+}
+
+int qbfac_gpu_matrix_mtx(qbfac_gpu_ctx* ctx, const char* path, qbfac_gpu_matrix** out) {
+    if (!ctx || !out) return QBFAC_ERROR;
+    *out = nullptr;
+    return guard(ctx, [&] {
+        auto h = std::make_unique<qbfac_gpu_matrix>();
+        h->ctx = ctx;
+        qbgpu::MtxInfo i{};
+        const auto head = qbgpu::mtx_info(path);
+        if (head.coordinate) {
+            std::vector<int64_t> rp;
+            std::vector<int32_t> ci;
+            std::vector<double> v;
+            qbgpu::mtx_read_csr(path, i, rp, ci, v);
+            h->m = qbgpu::make_csr(*ctx->c, i.m, 0, i.m, i.n, i.nnz, rp.data(), ci.data(), v.data());
+        } else {
+            std::vector<double> a;
+            qbgpu::mtx_read_dense(path, i, a);
+            h->m = qbgpu::make_dense(*ctx->c, i.m, 0, i.m, i.n, a.data(), std::max<int64_t>(i.m, 1), false);
+        }
+        *out = h.release();
+    });
+}
+
+int qbfac_gpu_matrix_shape(const qbfac_gpu_matrix* mat, int* sparse, int64_t* m, int64_t* n, int64_t* nnz) {
+    if (!mat || !mat->m) return QBFAC_ERROR;
+    *sparse = mat->m->sparse ? 1 : 0;
+    *m = mat->m->m;
+    *n = mat->m->n;
+    *nnz = mat->m->sparse ? mat->m->nnz : mat->m->m * mat->m->n;
+    return QBFAC_OK;
+}
+
+int qbfac_gpu_matrix_export_csr(qbfac_gpu_ctx* ctx, const qbfac_gpu_matrix* mat, int64_t* row_ptr, int32_t* col_idx,
+                                double* values) {
+    return guard(ctx, [&] {
+        const auto& a = *mat->m;
+        if (!a.sparse) throw qbgpu::QbError(qbgpu::kDimensionError, "export_csr: dense matrix");
+        QB_CUDA(cudaMemcpyAsync(row_ptr, a.rp, sizeof(int64_t) * (a.m + 1), cudaMemcpyDeviceToHost, ctx->c->st));
+        if (a.nnz > 0) {
+            QB_CUDA(cudaMemcpyAsync(col_idx, a.ci, sizeof(int32_t) * a.nnz, cudaMemcpyDeviceToHost, ctx->c->st));
+            QB_CUDA(cudaMemcpyAsync(values, a.v, sizeof(double) * a.nnz, cudaMemcpyDeviceToHost, ctx->c->st));
+        }
+        QB_CUDA(cudaStreamSynchronize(ctx->c->st));
+    });
+}
+
+int qbfac_gpu_matrix_export_dense(qbfac_gpu_ctx* ctx, const qbfac_gpu_matrix* mat, double* a, int64_t lda) {
+    return guard(ctx, [&] {
+        const auto& x = *mat->m;
+        if (x.sparse) throw qbgpu::QbError(qbgpu::kDimensionError, "export_dense: sparse matrix");
+        if (x.m > 0 && x.n > 0)
+            QB_CUDA(cudaMemcpy2DAsync(a, sizeof(double) * lda, x.a, sizeof(double) * x.lda, sizeof(double) * x.m, x.n,
+                                      cudaMemcpyDeviceToHost, ctx->c->st));
+        QB_CUDA(cudaStreamSynchronize(ctx->c->st));
     });
 }
 

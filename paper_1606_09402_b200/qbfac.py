@@ -134,6 +134,16 @@ def lib():
         L.qbfac_gpu_result_copy_trace.restype = I64
         L.qbfac_gpu_result_free.argtypes = [P]
         L.qbfac_gpu_validate_epsilon.argtypes = [D, D, D, P]
+        L.qbfac_mtx_last_error.restype = C.c_char_p
+        L.qbfac_mtx_info.argtypes = [C.c_char_p, P, P, P, P]
+        L.qbfac_mtx_read_csr.argtypes = [C.c_char_p, P, P, P]
+        L.qbfac_mtx_read_dense.argtypes = [C.c_char_p, P, I64]
+        L.qbfac_mtx_write_csr.argtypes = [C.c_char_p, I64, I64, I64, P, P, P]
+        L.qbfac_mtx_write_dense.argtypes = [C.c_char_p, I64, I64, P, I64]
+        L.qbfac_gpu_matrix_mtx.argtypes = [P, C.c_char_p, PP]
+        L.qbfac_gpu_matrix_shape.argtypes = [P, P, P, P, P]
+        L.qbfac_gpu_matrix_export_csr.argtypes = [P, P, P, P, P]
+        L.qbfac_gpu_matrix_export_dense.argtypes = [P, P, P, I64]
         _lib = L
     return _lib
 
@@ -295,6 +305,42 @@ class QBFactorization:
 # ---- MatrixHandle (matrix_handle.hpp:41-86) ------------------------------------------------
 
 
+def _mtx_check(st: int):
+    _raise(st, lib().qbfac_mtx_last_error().decode())
+
+
+def read_matrix_market(path: str):
+    """Host read of a Matrix Market file: returns ("csr", m, n, row_ptr,
+    col_idx, values) built like SparseCsrMatrix::from_triplets, or ("dense", a) column-major."""
+    coord, m, n, nnz = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
+    bp = os.fsencode(path)
+    _mtx_check(lib().qbfac_mtx_info(bp, C.byref(coord), C.byref(m), C.byref(n), C.byref(nnz)))
+    if coord.value:
+        rp = np.zeros(m.value + 1, dtype=np.int64)
+        ci = np.zeros(max(nnz.value, 1), dtype=np.int32)
+        v = np.zeros(max(nnz.value, 1), dtype=np.float64)
+        _mtx_check(lib().qbfac_mtx_read_csr(bp, _p(rp), _p(ci), _p(v)))
+        return "csr", m.value, n.value, rp, ci[:nnz.value], v[:nnz.value]
+    a = np.zeros((m.value, n.value), dtype=np.float64, order="F")
+    _mtx_check(lib().qbfac_mtx_read_dense(bp, _p(a), max(m.value, 1)))
+    return "dense", a
+
+
+def write_matrix_market(path: str, a=None, csr=None):
+    """write_matrix_market: `a` dense (array format) or `csr` = (m, n,
+    row_ptr, col_idx, values) (coordinate format); shortest round-trip decimals."""
+    bp = os.fsencode(path)
+    if csr is not None:
+        m, n, rp, ci, v = csr
+        rp = np.ascontiguousarray(rp, dtype=np.int64)
+        ci = np.ascontiguousarray(ci, dtype=np.int32)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        _mtx_check(lib().qbfac_mtx_write_csr(bp, m, n, len(v), _p(rp), _p(ci), _p(v)))
+    else:
+        a = np.asfortranarray(a, dtype=np.float64)
+        _mtx_check(lib().qbfac_mtx_write_dense(bp, a.shape[0], a.shape[1], _p(a), max(a.shape[0], 1)))
+
+
 class MatrixHandle:
     """A resident on the device (dense column-major or CSR + device-built transposed CSR)."""
 
@@ -349,6 +395,30 @@ class MatrixHandle:
         ctx.check(lib().qbfac_gpu_matrix_csr_shard(ctx.handle, m_global, row0, m, n, len(v), _p(rp), _p(ci),
                                                    _p(v), C.byref(h)))
         return MatrixHandle(h, ctx, m, n, True)
+
+    @staticmethod
+    def from_mtx(path: str, ctx: Optional[Context] = None) -> "MatrixHandle":
+        """read_matrix_market(path) straight into device memory."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        ctx.check(lib().qbfac_gpu_matrix_mtx(ctx.handle, os.fsencode(path), C.byref(h)))
+        sp, m, n, nnz = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
+        lib().qbfac_gpu_matrix_shape(h, C.byref(sp), C.byref(m), C.byref(n), C.byref(nnz))
+        return MatrixHandle(h, ctx, m.value, n.value, bool(sp.value))
+
+    def export(self):
+        """Device arrays back to the host: (row_ptr, col_idx, values) or the dense array."""
+        sp, m, n, nnz = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
+        lib().qbfac_gpu_matrix_shape(self._h, C.byref(sp), C.byref(m), C.byref(n), C.byref(nnz))
+        if sp.value:
+            rp = np.zeros(m.value + 1, dtype=np.int64)
+            ci = np.zeros(max(nnz.value, 1), dtype=np.int32)
+            v = np.zeros(max(nnz.value, 1), dtype=np.float64)
+            self.ctx.check(lib().qbfac_gpu_matrix_export_csr(self.ctx.handle, self._h, _p(rp), _p(ci), _p(v)))
+            return rp, ci[:nnz.value], v[:nnz.value]
+        a = np.zeros((m.value, n.value), dtype=np.float64, order="F")
+        self.ctx.check(lib().qbfac_gpu_matrix_export_dense(self.ctx.handle, self._h, _p(a), max(m.value, 1)))
+        return a
 
     def rows(self):
         return self.m
