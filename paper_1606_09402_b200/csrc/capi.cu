@@ -87,7 +87,10 @@ const char* qbfac_gpu_last_error(const qbfac_gpu_ctx* ctx) {
 }
 
 int qbfac_gpu_synchronize(qbfac_gpu_ctx* ctx) {
-    return guard(ctx, [&] { QB_CUDA(cudaStreamSynchronize(ctx->c->st)); });
+    return guard(ctx, [&] {
+        QB_CUDA(cudaStreamSynchronize(ctx->c->st_copy));
+        QB_CUDA(cudaStreamSynchronize(ctx->c->st));
+    });
 }
 
 void* qbfac_gpu_stream(qbfac_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c->st) : nullptr; }
@@ -120,6 +123,18 @@ int qbfac_gpu_matrix_dense_device(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, cons
         auto h = std::make_unique<qbfac_gpu_matrix>();
         h->ctx = ctx;
         h->m = qbgpu::make_dense(*ctx->c, m, 0, m, n, dev_a, lda, true);
+        *out = h.release();
+    });
+}
+
+int qbfac_gpu_matrix_dense_async(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
+                                 int64_t chunk_rows, qbfac_gpu_matrix** out) {
+    if (!ctx || !out) return QBFAC_ERROR;
+    *out = nullptr;
+    return guard(ctx, [&] {
+        auto h = std::make_unique<qbfac_gpu_matrix>();
+        h->ctx = ctx;
+        h->m = qbgpu::make_dense_async(*ctx->c, m, n, a, lda, chunk_rows);
         *out = h.release();
     });
 }

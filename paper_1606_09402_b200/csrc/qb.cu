@@ -51,6 +51,7 @@ Context::Context(int dev, int rank_, int world_, const void* nccl_id) : device(d
         throw QbError(kError, std::string("qbfac_gpu needs an sm_100 (B200) device, found ") + prop.name);
     sms = prop.multiProcessorCount;
     QB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    QB_CUDA(cudaStreamCreateWithFlags(&st_copy, cudaStreamNonBlocking));
     QB_CUDA(cudaMalloc(&d_small, sizeof(double) * kSlot * kNumSlots + 64 * sizeof(double)));
     QB_CUDA(cudaMalloc(&d_status, sizeof(SmallStatus) * 4));
     QB_CUDA(cudaMalloc(&d_gbar, 64 * sizeof(unsigned)));
@@ -80,6 +81,7 @@ Context::~Context() {
     ws_hh.release();
     ws_sp.release();
     ws_panel.release();
+    if (st_copy) cudaStreamDestroy(st_copy);
     if (d_small) cudaFree(d_small);
     if (d_status) cudaFree(d_status);
     if (d_gbar) cudaFree(d_gbar);
@@ -93,6 +95,10 @@ Context::~Context() {
 }
 
 Matrix::~Matrix() {
+    for (auto& ch : pending) {
+        cudaEventSynchronize(ch.ready);
+        cudaEventDestroy(ch.ready);
+    }
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (a && owns_a) cudaFree(a);
@@ -130,6 +136,44 @@ std::unique_ptr<Matrix> make_dense(Context& c, std::int64_t m_global, std::int64
     QB_CUDA(cudaStreamSynchronize(c.st));
     if (m > 0 && n > 0 && !std::isfinite(c.h_scalar[0])) throw QbError(kError, "from_data: non-finite entry");
     return mat;
+}
+
+std::unique_ptr<Matrix> make_dense_async(Context& c, std::int64_t m, std::int64_t n, const double* a,
+                                         std::int64_t lda, std::int64_t chunk_rows) {
+    if (m < 0 || n < 0 || lda < std::max<std::int64_t>(1, m))
+        throw QbError(kDimensionError, "matrix_dense: bad dimensions");
+    auto mat = std::make_unique<Matrix>();
+    mat->ctx = &c;
+    mat->m = m;
+    mat->n = n;
+    mat->m_global = m;
+    mat->lda = std::max<std::int64_t>(8, round_up(m, 8));
+    QB_CUDA(cudaMalloc(&mat->a, sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1)));
+    if (mat->lda != m) {
+        QB_CUDA(cudaMemsetAsync(mat->a, 0, sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1), c.st_copy));
+    }
+    if (m == 0 || n == 0) return mat;
+    // ~8 row chunks of whole 128-row GEMM tiles
+    if (chunk_rows <= 0) chunk_rows = std::max<std::int64_t>(1024, round_up(ceil_div(m, 8), 128));
+    for (std::int64_t r0 = 0; r0 < m; r0 += chunk_rows) {
+        const std::int64_t rows = std::min(chunk_rows, m - r0);
+        QB_CUDA(cudaMemcpy2DAsync(mat->a + r0, mat->lda * sizeof(double), a + r0, lda * sizeof(double),
+                                  rows * sizeof(double), n, cudaMemcpyHostToDevice, c.st_copy));
+        cudaEvent_t ev;
+        QB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        QB_CUDA(cudaEventRecord(ev, c.st_copy));
+        mat->pending.push_back(Matrix::Chunk{r0 + rows, ev});
+    }
+    mat->check_finite = true;
+    return mat;
+}
+
+void Matrix::wait_resident(cudaStream_t s) {
+    for (auto& ch : pending) {
+        QB_CUDA(cudaStreamWaitEvent(s, ch.ready, 0));
+        cudaEventDestroy(ch.ready);
+    }
+    pending.clear();
 }
 
 std::unique_ptr<Matrix> make_csr(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
@@ -190,12 +234,26 @@ public:
             const CsrView av = a_.csr();
             double* part = av.heavy.nseg ? c_.ws_sp.get(csr_spmm_scratch(av, std::min<int>(static_cast<int>(x.cols), 256))) : nullptr;
             csr_spmm(st_, av, x.p, x.ld, y.p, y.ld, static_cast<int>(x.cols), alpha, beta, c_.sms, part);
+        } else if (!a_.pending.empty()) {
+            // first pass over an asynchronously uploaded A: one GEMM per row chunk as it lands
+            std::int64_t r0 = 0;
+            for (auto& ch : a_.pending) {
+                QB_CUDA(cudaStreamWaitEvent(st_, ch.ready, 0));
+                const std::int64_t rows = ch.row_end - r0;
+                MatView ab{a_.a + r0, rows, a_.n, a_.lda, false};
+                MatView yb = y.rowmajor ? MatView{y.p + r0 * y.ld, rows, y.cols, y.ld, true}
+                                        : MatView{y.p + r0, rows, y.cols, y.ld, false};
+                gemm(alpha, ab, x, beta, yb);
+                r0 = ch.row_end;
+            }
+            a_.wait_resident(st_);
         } else {
             gemm(alpha, a_.dense_view(), x, beta, y);
         }
     }
     // Y (n x w) = A^T X (X: m x w), summed over ranks.
     void apply_t(const MatView& x, const MatView& y) {
+        a_.wait_resident(st_);
         const bool contiguous = (y.rowmajor && y.ld == y.cols) || (!y.rowmajor && y.ld == y.rows);
         if (c_.world > 1 && !contiguous) {
             // allreduce needs a packed buffer: compute there, reduce, scatter into y
@@ -224,11 +282,16 @@ public:
     }
 
     double frob_device(double* out) {  // ||A||_F^2 into device scalar `out` (+ allreduce)
+        a_.wait_resident(st_);
         if (a_.sparse) sum_squares_vec(st_, c_.ws_red, a_.v, a_.nnz, out);
         else sum_squares(st_, c_.ws_red, a_.dense_view(), out);
         c_.allreduce(out, 1);
         QB_CUDA(cudaMemcpyAsync(c_.h_scalar, out, sizeof(double), cudaMemcpyDeviceToHost, st_));
         QB_CUDA(cudaStreamSynchronize(st_));
+        if (a_.check_finite) {  // deferred DenseMatrix::from_data check of an async upload
+            if (!std::isfinite(c_.h_scalar[0])) throw QbError(kError, "from_data: non-finite entry");
+            a_.check_finite = false;
+        }
         return c_.h_scalar[0];
     }
 

@@ -45,6 +45,7 @@ struct DBuf {
 struct Context {
     int device = 0;
     cudaStream_t st = nullptr;
+    cudaStream_t st_copy = nullptr;  // host->device uploads overlapped with compute
     int sms = 148;
     Workspace ws_gemm, ws_red, ws_hh, ws_sp, ws_panel;
     RngTables rng;
@@ -90,6 +91,16 @@ struct Matrix {
     std::int32_t* ct_ci = nullptr;
     double* ct_v = nullptr;
     HeavyPlan heavy, heavy_t;  // heavy-row segment plans of the CSR and its transpose
+    // Asynchronous dense upload (qbfac_gpu_matrix_dense_async): row chunks [row_end of the
+    // previous, row_end) become resident when their event completes on ctx->st_copy. The
+    // first A*X pass consumes them chunk by chunk; every other use waits for all of them.
+    struct Chunk {
+        std::int64_t row_end;
+        cudaEvent_t ready;
+    };
+    std::vector<Chunk> pending;
+    bool check_finite = false;  // validate ||A||^2 at the first norm (from_data, dense_matrix.cpp:17-18)
+    void wait_resident(cudaStream_t s);
 
     ~Matrix();
     MatView dense_view() const { return MatView{a, m, n, lda, false}; }
@@ -99,6 +110,10 @@ struct Matrix {
 
 std::unique_ptr<Matrix> make_dense(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
                                    std::int64_t n, const double* a, std::int64_t lda, bool device_src);
+// Chunked asynchronous upload of a host dense matrix (pinned memory gives a true overlap;
+// the host buffer must stay unchanged until the matrix has been consumed or synchronized).
+std::unique_ptr<Matrix> make_dense_async(Context& c, std::int64_t m, std::int64_t n, const double* a,
+                                         std::int64_t lda, std::int64_t chunk_rows);
 std::unique_ptr<Matrix> make_csr(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
                                  std::int64_t n, std::int64_t nnz, const std::int64_t* rp,
                                  const std::int32_t* ci, const double* v);

@@ -116,6 +116,7 @@ def lib():
         L.qbfac_gpu_kernel_launches.restype = I64
         L.qbfac_gpu_matrix_dense.argtypes = [P, I64, I64, P, I64, PP]
         L.qbfac_gpu_matrix_dense_device.argtypes = [P, I64, I64, P, I64, PP]
+        L.qbfac_gpu_matrix_dense_async.argtypes = [P, I64, I64, P, I64, I64, PP]
         L.qbfac_gpu_matrix_dense_shard.argtypes = [P, I64, I64, I64, I64, P, I64, PP]
         L.qbfac_gpu_matrix_csr.argtypes = [P, I64, I64, I64, P, P, P, PP]
         L.qbfac_gpu_matrix_csr_shard.argtypes = [P, I64, I64, I64, I64, I64, P, P, P, PP]
@@ -357,6 +358,20 @@ class MatrixHandle:
         return MatrixHandle(h, ctx, m, n, False)
 
     @staticmethod
+    def dense_async(a: np.ndarray, ctx: Optional[Context] = None, chunk_rows: int = 0) -> "MatrixHandle":
+        """Chunked asynchronous upload (H2D overlapped with the first pass of the next run).
+        `a` must be column-major (Fortran-ordered, ideally pinned) and is kept alive by the handle."""
+        ctx = ctx or default_context()
+        if not (a.flags.f_contiguous and a.dtype == np.float64):
+            a = np.asfortranarray(a, dtype=np.float64)
+        m, n = a.shape
+        h = C.c_void_p()
+        ctx.check(lib().qbfac_gpu_matrix_dense_async(ctx.handle, m, n, _p(a), max(m, 1), chunk_rows, C.byref(h)))
+        mh = MatrixHandle(h, ctx, m, n, False)
+        mh._host_ref = a
+        return mh
+
+    @staticmethod
     def dense_device(ptr: int, m: int, n: int, lda: int, ctx: Optional[Context] = None) -> "MatrixHandle":
         """A already in device memory (column-major, leading dimension lda); copied."""
         ctx = ctx or default_context()
@@ -477,13 +492,19 @@ class DeviceResult:
     def rank(self) -> int:
         return int(self.info.rank)
 
-    def q(self) -> np.ndarray:
-        q = np.empty((int(self.info.m), self.rank), order="F")
-        self.ctx.check(lib().qbfac_gpu_result_copy_q(self._h, _p(q), max(int(self.info.m), 1)))
+    def q(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Q (m x rank, column-major); `out`: caller buffer (e.g. pinned) with >= m*rank doubles."""
+        m = int(self.info.m)
+        q = np.empty((m, self.rank), order="F") if out is None else out.reshape(-1)[:m * self.rank].reshape(
+            (m, self.rank), order="F")
+        self.ctx.check(lib().qbfac_gpu_result_copy_q(self._h, _p(q), max(m, 1)))
         return q
 
-    def b(self) -> np.ndarray:
-        b = np.empty((self.rank, int(self.info.n)), order="F")
+    def b(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """B (rank x n, column-major); `out`: caller buffer with >= rank*n doubles."""
+        n = int(self.info.n)
+        b = np.empty((self.rank, n), order="F") if out is None else out.reshape(-1)[:self.rank * n].reshape(
+            (self.rank, n), order="F")
         self.ctx.check(lib().qbfac_gpu_result_copy_b(self._h, _p(b), max(self.rank, 1)))
         return b
 

@@ -266,3 +266,39 @@ def test_cfg3_full_size_vs_oracle_golden(ctx):
     assert np.max(np.abs(s - sr) / sr) <= 1e-10
     err = csr_explicit_error(csr, got.Q, got.B)
     assert abs(err - gold["explicit_error"]) <= 1e-10 * gold["explicit_error"]
+
+
+@pytest.mark.parametrize("alg,chunk", [("fp", 0), ("fp", 96), ("ei", 200)])
+def test_async_upload_overlapped_first_pass(ctx, oracle, alg, chunk):
+    """qbfac_gpu_matrix_dense_async: the first A*X pass consumes row chunks as their H2D copy
+    lands; the factorization matches the resident-A one (and the oracle)."""
+    from paper_1606_09402_b200 import qbfac
+    import torch
+    a = _matrix2(500)
+    eps = 1e-3 * np.linalg.norm(a)
+    pinned = torch.empty((500, 500), dtype=torch.float64, pin_memory=True)
+    pinned.copy_(torch.as_tensor(np.ascontiguousarray(a.T)))
+    a_f = pinned.numpy().T  # Fortran view of pinned memory
+    if alg == "fp":
+        run = lambda h: qbfac.rand_qb_fp(h, eps, 10, 1, 200, qbfac.RngStream(4), max_rank=200)
+        ref = None
+    else:
+        run = lambda h: qbfac.rand_qb_ei(h, qbfac.StopRule.fixed_precision(eps), 10, 1, qbfac.RngStream(4))
+        ref = oracle.run("ei", a, b=10, power=1, eps_abs=eps, seed=4)
+    got_async = run(qbfac.MatrixHandle.dense_async(a_f, ctx, chunk_rows=chunk))
+    got_res = run(qbfac.MatrixHandle.dense(a, ctx))
+    assert got_async.rank == got_res.rank and got_async.passes == got_res.passes
+    if alg == "ei":
+        assert got_async.rank == ref.rank
+    s1, s2 = _sv(got_async.B), _sv(got_res.B)
+    assert np.max(np.abs(s1 - s2) / s2) < 1e-12
+    assert abs(got_async.error_indicator - got_res.error_indicator) <= 1e-12 * got_res.norm_a_sq
+
+
+def test_async_upload_rejects_non_finite(ctx):
+    from paper_1606_09402_b200 import qbfac
+    a = _matrix2(200)
+    a[17, 3] = np.nan
+    h = qbfac.MatrixHandle.dense_async(np.asfortranarray(a), ctx)
+    with pytest.raises(qbfac.Error):
+        qbfac.rand_qb_fp(h, 1e-2, 10, 0, 50, qbfac.RngStream(1), max_rank=50)
