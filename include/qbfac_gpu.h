@@ -140,6 +140,14 @@ int qbfac_gpu_matrix_dense_shard(qbfac_gpu_ctx* ctx, int64_t m_global, int64_t r
  * norm computation instead of at upload. */
 int qbfac_gpu_matrix_dense_async(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
                                  int64_t chunk_rows, qbfac_gpu_matrix** out);
+/* Host-streamed dense matrix — the RowStream of single_pass_fp (matrix_handle.hpp:30-37,
+ * SPEC.md:300-308): A stays in host memory (column-major, lda; borrowed, must outlive the
+ * run) and QBFAC_ALG_SINGLE_PASS streams row chunks (chunk_rows, 0 = ~128 MB) through a
+ * 3-deep device ring, overlapping each chunk's copy with G_c = A_c Omega, H += A_c^T G_c and
+ * ||A_c||^2 of the previous ones. Pinned host memory gives full-rate DMA. Any other use of
+ * the handle returns QBFAC_ERROR. */
+int qbfac_gpu_matrix_dense_stream(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
+                                  int64_t chunk_rows, qbfac_gpu_matrix** out);
 int qbfac_gpu_matrix_csr(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
                          const int32_t* col_idx, const double* values, qbfac_gpu_matrix** out);
 int qbfac_gpu_matrix_csr_shard(qbfac_gpu_ctx* ctx, int64_t m_global, int64_t row0, int64_t m_local,

@@ -139,6 +139,18 @@ int qbfac_gpu_matrix_dense_async(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, const
     });
 }
 
+int qbfac_gpu_matrix_dense_stream(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
+                                  int64_t chunk_rows, qbfac_gpu_matrix** out) {
+    if (!ctx || !out) return QBFAC_ERROR;
+    *out = nullptr;
+    return guard(ctx, [&] {
+        auto h = std::make_unique<qbfac_gpu_matrix>();
+        h->ctx = ctx;
+        h->m = qbgpu::make_dense_stream(*ctx->c, m, n, a, lda, chunk_rows);
+        *out = h.release();
+    });
+}
+
 int qbfac_gpu_matrix_csr(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
                          const int32_t* col_idx, const double* values, qbfac_gpu_matrix** out) {
     return qbfac_gpu_matrix_csr_shard(ctx, m, 0, m, n, nnz, row_ptr, col_idx, values, out);

@@ -168,6 +168,25 @@ std::unique_ptr<Matrix> make_dense_async(Context& c, std::int64_t m, std::int64_
     return mat;
 }
 
+std::unique_ptr<Matrix> make_dense_stream(Context& c, std::int64_t m, std::int64_t n, const double* a,
+                                          std::int64_t lda, std::int64_t chunk_rows) {
+    if (m < 0 || n < 0 || lda < std::max<std::int64_t>(1, m) || (m > 0 && n > 0 && !a))
+        throw QbError(kDimensionError, "matrix_dense_stream: bad dimensions");
+    auto mat = std::make_unique<Matrix>();
+    mat->ctx = &c;
+    mat->m = m;
+    mat->n = n;
+    mat->m_global = m;
+    mat->host_stream = true;
+    mat->host_a = a;
+    mat->host_lda = lda;
+    // ~128 MB per chunk, whole 128-row GEMM tiles
+    if (chunk_rows <= 0)
+        chunk_rows = std::max<std::int64_t>(128, round_up((std::int64_t{128} << 20) / (8 * std::max<std::int64_t>(n, 1)), 128));
+    mat->chunk_rows = chunk_rows;
+    return mat;
+}
+
 void Matrix::wait_resident(cudaStream_t s) {
     for (auto& ch : pending) {
         QB_CUDA(cudaStreamWaitEvent(s, ch.ready, 0));
@@ -229,6 +248,7 @@ public:
 
     // Y (m x w) = A X (X: n x w). Dense: DMMA GEMM; sparse: CSR SpMM.
     void apply(const MatView& x, const MatView& y, double alpha = 1.0, double beta = 0.0) {
+        if (a_.host_stream) throw QbError(kError, "host-streamed matrix: only single_pass_fp consumes a RowStream");
         if (a_.sparse) {
             if (!x.rowmajor || !y.rowmajor) throw QbError(kInternal, "sparse pass needs row-major blocks");
             const CsrView av = a_.csr();
@@ -251,8 +271,61 @@ public:
             gemm(alpha, a_.dense_view(), x, beta, y);
         }
     }
+    // One pass over a host-streamed A (single_pass_fp): row chunks are copied
+    // on the copy stream into a 3-deep device ring while the compute stream forms, per chunk,
+    // G_c = A_c Omega, H += A_c^T G_c and ||A_c||^2 (summed in chunk order). Returns ||A||^2.
+    double stream_single_pass(const MatView& om, const MatView& g, const MatView& h) {
+        if (!a_.host_stream) throw QbError(kInternal, "stream_single_pass on a resident matrix");
+        const std::int64_t m = a_.m, n = a_.n, cr = a_.chunk_rows;
+        const std::int64_t nchunk = ceil_div(m, cr);
+        constexpr int kRing = 3;
+        const std::int64_t ld = round_up(cr, 8);
+        DBuf ring(static_cast<std::size_t>(kRing) * ld * std::max<std::int64_t>(n, 1), st_);
+        DBuf norms(static_cast<std::size_t>(std::max<std::int64_t>(nchunk, 1)), st_);
+        cudaEvent_t landed[kRing], freed[kRing];
+        for (int i = 0; i < kRing; ++i) {
+            QB_CUDA(cudaEventCreateWithFlags(&landed[i], cudaEventDisableTiming));
+            QB_CUDA(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
+        }
+        // the ring is allocated on the compute stream: make the copy stream wait for it
+        cudaEvent_t ready;
+        QB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        QB_CUDA(cudaEventRecord(ready, st_));
+        QB_CUDA(cudaStreamWaitEvent(c_.st_copy, ready, 0));
+        for (std::int64_t ci = 0; ci < nchunk; ++ci) {
+            const int slot = static_cast<int>(ci % kRing);
+            const std::int64_t r0 = ci * cr, rows = std::min(cr, m - r0);
+            double* buf = ring.p + static_cast<std::size_t>(slot) * ld * n;
+            if (ci >= kRing) QB_CUDA(cudaStreamWaitEvent(c_.st_copy, freed[slot], 0));
+            QB_CUDA(cudaMemcpy2DAsync(buf, ld * sizeof(double), a_.host_a + r0, a_.host_lda * sizeof(double),
+                                      rows * sizeof(double), n, cudaMemcpyHostToDevice, c_.st_copy));
+            QB_CUDA(cudaEventRecord(landed[slot], c_.st_copy));
+            QB_CUDA(cudaStreamWaitEvent(st_, landed[slot], 0));
+            MatView ac{buf, rows, n, ld, false};
+            MatView gc = g.rowmajor ? MatView{g.p + r0 * g.ld, rows, g.cols, g.ld, true}
+                                    : MatView{g.p + r0, rows, g.cols, g.ld, false};
+            gemm(1.0, ac, om, 0.0, gc);
+            sum_squares(st_, c_.ws_red, ac, norms.p + ci);
+            gemm(1.0, ac.t(), gc, ci == 0 ? 0.0 : 1.0, h);
+            QB_CUDA(cudaEventRecord(freed[slot], st_));
+        }
+        std::vector<double> hn(static_cast<std::size_t>(nchunk));
+        if (nchunk) QB_CUDA(cudaMemcpyAsync(hn.data(), norms.p, sizeof(double) * nchunk, cudaMemcpyDeviceToHost, st_));
+        QB_CUDA(cudaStreamSynchronize(st_));
+        for (int i = 0; i < kRing; ++i) {
+            cudaEventDestroy(landed[i]);
+            cudaEventDestroy(freed[i]);
+        }
+        cudaEventDestroy(ready);
+        double nrm = 0.0;
+        for (double x : hn) nrm += x;
+        if (!std::isfinite(nrm)) throw QbError(kError, "from_data: non-finite entry");  // dense_matrix.cpp:17-18
+        return nrm;
+    }
+
     // Y (n x w) = A^T X (X: m x w), summed over ranks.
     void apply_t(const MatView& x, const MatView& y) {
+        if (a_.host_stream) throw QbError(kError, "host-streamed matrix: only single_pass_fp consumes a RowStream");
         a_.wait_resident(st_);
         const bool contiguous = (y.rowmajor && y.ld == y.cols) || (!y.rowmajor && y.ld == y.rows);
         if (c_.world > 1 && !contiguous) {
@@ -282,6 +355,7 @@ public:
     }
 
     double frob_device(double* out) {  // ||A||_F^2 into device scalar `out` (+ allreduce)
+        if (a_.host_stream) throw QbError(kError, "host-streamed matrix: only single_pass_fp consumes a RowStream");
         a_.wait_resident(st_);
         if (a_.sparse) sum_squares_vec(st_, c_.ws_red, a_.v, a_.nnz, out);
         else sum_squares(st_, c_.ws_red, a_.dense_view(), out);
@@ -731,6 +805,8 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
 // ---- randQB_FP / fixed rank / single pass --------------------------------------------
 std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
     if (p.b < 1) throw QbError(kDimensionError, "rand_qb_fp: block size must be >= 1");
+    if (a.host_stream && (p.alg != 3 || p.power != 0))
+        throw QbError(kError, "host-streamed matrix: only single_pass_fp consumes a RowStream");
     Engine eng(c, a);
     const std::int64_t m = a.m, n = a.n, mg = a.m_global;
     const bool fixed = p.alg != 1;           // Alg. 3 / single pass: fixed rank l = k + s
@@ -792,6 +868,12 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
             eng.apply_t(gv, omv); a.passes += 1;
             eng.orth_wide(omv, false, wtmp, m2);
         }
+        if (a.host_stream) {                                                       // steps 7-9, one stream
+            norm_a_sq = eng.stream_single_pass(omv, gv, hv);
+            e_host = norm_a_sq;
+            s.set_e(norm_a_sq);
+            a.passes += 2;
+        } else {
         eng.apply(omv, gv); a.passes += 1;                                         // step 7
         if (restart == 0) {                                                        // step 9
             norm_a_sq = eng.frob_device(s.d_e);  // same logical pass (multiply_with_norm)
@@ -802,6 +884,7 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
             }
         }
         eng.apply_t(gv, hv); a.passes += 1;                                        // step 8
+        }
         bool stop = false;
         for (std::int64_t off = 0; off < l; off += p.b) {                          // steps 10-21
             const std::int64_t bi = std::min(p.b, l - off);

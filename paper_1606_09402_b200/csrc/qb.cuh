@@ -100,6 +100,11 @@ struct Matrix {
     };
     std::vector<Chunk> pending;
     bool check_finite = false;  // validate ||A||^2 at the first norm (from_data, dense_matrix.cpp:17-18)
+    // Host-streamed dense rows (qbfac_gpu_matrix_dense_stream, the RowStream of
+    // matrix_handle.hpp:30-37): A stays in host memory and single_pass_fp streams row chunks.
+    bool host_stream = false;
+    const double* host_a = nullptr;
+    std::int64_t host_lda = 0, chunk_rows = 0;
     void wait_resident(cudaStream_t s);
 
     ~Matrix();
@@ -114,6 +119,10 @@ std::unique_ptr<Matrix> make_dense(Context& c, std::int64_t m_global, std::int64
 // the host buffer must stay unchanged until the matrix has been consumed or synchronized).
 std::unique_ptr<Matrix> make_dense_async(Context& c, std::int64_t m, std::int64_t n, const double* a,
                                          std::int64_t lda, std::int64_t chunk_rows);
+// Host-streamed dense matrix (borrowed host pointer, column-major, lda): consumed only by
+// single_pass_fp, which streams row chunks through a device ring.
+std::unique_ptr<Matrix> make_dense_stream(Context& c, std::int64_t m, std::int64_t n, const double* a,
+                                          std::int64_t lda, std::int64_t chunk_rows);
 std::unique_ptr<Matrix> make_csr(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
                                  std::int64_t n, std::int64_t nnz, const std::int64_t* rp,
                                  const std::int32_t* ci, const double* v);

@@ -114,6 +114,9 @@ def synthesize_torch(m: int, n: int, sigma: np.ndarray, seed: int, noise: float 
 
     def dev_gauss(rows, cols, stream, skip):
         t = torch.empty((cols, rows), dtype=torch.float64, device=device)  # column-major rows x cols
+        # the library writes on its own stream: torch's pending work on this (possibly just
+        # recycled) block must finish first
+        torch.cuda.synchronize()
         ctx.check(lib().qbfac_gpu_gaussian_device(ctx.handle, seed, stream, skip, rows, cols,
                                                   C.c_void_p(t.data_ptr()), rows))
         ctx.synchronize()

@@ -117,6 +117,7 @@ def lib():
         L.qbfac_gpu_matrix_dense.argtypes = [P, I64, I64, P, I64, PP]
         L.qbfac_gpu_matrix_dense_device.argtypes = [P, I64, I64, P, I64, PP]
         L.qbfac_gpu_matrix_dense_async.argtypes = [P, I64, I64, P, I64, I64, PP]
+        L.qbfac_gpu_matrix_dense_stream.argtypes = [P, I64, I64, P, I64, I64, PP]
         L.qbfac_gpu_matrix_dense_shard.argtypes = [P, I64, I64, I64, I64, P, I64, PP]
         L.qbfac_gpu_matrix_csr.argtypes = [P, I64, I64, I64, P, P, P, PP]
         L.qbfac_gpu_matrix_csr_shard.argtypes = [P, I64, I64, I64, I64, I64, P, P, P, PP]
@@ -367,6 +368,20 @@ class MatrixHandle:
         m, n = a.shape
         h = C.c_void_p()
         ctx.check(lib().qbfac_gpu_matrix_dense_async(ctx.handle, m, n, _p(a), max(m, 1), chunk_rows, C.byref(h)))
+        mh = MatrixHandle(h, ctx, m, n, False)
+        mh._host_ref = a
+        return mh
+
+    @staticmethod
+    def dense_stream(a: np.ndarray, ctx: Optional[Context] = None, chunk_rows: int = 0) -> "MatrixHandle":
+        """Host-resident A read as a row stream by single_pass_fp only (matrix_handle.hpp:30-37);
+        `a` column-major (ideally pinned), kept alive by the handle."""
+        ctx = ctx or default_context()
+        if not (a.flags.f_contiguous and a.dtype == np.float64):
+            a = np.asfortranarray(a, dtype=np.float64)
+        m, n = a.shape
+        h = C.c_void_p()
+        ctx.check(lib().qbfac_gpu_matrix_dense_stream(ctx.handle, m, n, _p(a), max(m, 1), chunk_rows, C.byref(h)))
         mh = MatrixHandle(h, ctx, m, n, False)
         mh._host_ref = a
         return mh

@@ -302,3 +302,40 @@ def test_async_upload_rejects_non_finite(ctx):
     h = qbfac.MatrixHandle.dense_async(np.asfortranarray(a), ctx)
     with pytest.raises(qbfac.Error):
         qbfac.rand_qb_fp(h, 1e-2, 10, 0, 50, qbfac.RngStream(1), max_rank=50)
+
+
+@pytest.mark.parametrize("chunk,pinned", [(0, True), (128, True), (100, False)])
+def test_single_pass_host_stream(ctx, oracle, chunk, pinned):
+    """single_pass_fp over a host-resident RowStream (matrix_handle.hpp:30-37): row chunks are
+    streamed through a device ring (copies overlapped with G_c = A_c Omega, H += A_c^T G_c);
+    same result as the resident single pass and within the reference lanes' spread of the oracle."""
+    from paper_1606_09402_b200 import matgen, qbfac
+    import torch
+    from oracle import lanes
+    a = matgen.cfg4_matrix(m=1200, n=800, r=60, seed=4)
+    if pinned:
+        buf = torch.empty((800, 1200), dtype=torch.float64, pin_memory=True)
+        buf.copy_(torch.as_tensor(np.ascontiguousarray(a.T)))
+        a_host = buf.numpy().T
+    else:
+        a_host = np.asfortranarray(a)
+    got = qbfac.single_pass_fp(qbfac.MatrixHandle.dense_stream(a_host, ctx, chunk_rows=chunk), 60, 20,
+                               qbfac.RngStream(42))
+    res = qbfac.single_pass_fp(qbfac.MatrixHandle.dense(a, ctx), 60, 20, qbfac.RngStream(42))
+    assert got.passes == 1 and got.rank == res.rank == 60
+    assert abs(got.norm_a_sq - res.norm_a_sq) <= 1e-13 * res.norm_a_sq
+    s1, s2 = _sv(got.B), _sv(res.B)
+    assert np.max(np.abs(s1 - s2) / s2) < 1e-9
+    ref = oracle.run("single_pass", a, b=20, fixed_rank=(60, 0), seed=42)
+    lane = lanes.run_scalar("single_pass", a, b=20, fixed_rank=(60, 0), seed=42)
+    _compare(got, ref, a=a, oracle=oracle, lane=lane)
+
+
+def test_host_stream_only_single_pass(ctx):
+    from paper_1606_09402_b200 import qbfac
+    a = np.asfortranarray(_matrix2(100))
+    h = qbfac.MatrixHandle.dense_stream(a, ctx)
+    with pytest.raises(qbfac.Error):
+        qbfac.rand_qb_ei(h, qbfac.StopRule.fixed_precision(1e-2 * np.linalg.norm(a)), 10, 0, qbfac.RngStream(1))
+    with pytest.raises(qbfac.Error):
+        qbfac.rand_qb_fp(h, 1e-2 * np.linalg.norm(a), 10, 0, 50, qbfac.RngStream(1))
