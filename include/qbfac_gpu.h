@@ -207,6 +207,13 @@ int qbfac_gpu_result_copy_q(qbfac_gpu_result* res, double* q, int64_t ldq);
 int qbfac_gpu_result_copy_b(qbfac_gpu_result* res, double* b, int64_t ldb);
 /* E after every block boundary (Theorem 2 checks); returns the count written. */
 int64_t qbfac_gpu_result_copy_trace(qbfac_gpu_result* res, double* out, int64_t cap);
+/* qb_to_svd(f, k) (PAPER Eq. 1.3): truncated SVD of Q*B computed on the
+ * device — Q_b = orth(B^T) (wide CholQR2 / BCGS2), N = B Q_b, one-sided Jacobi N W = U_r S,
+ * U = Q U_r(:, 1..k), V = Q_b W(:, 1..k). Outputs: u (m x k, ldu >= m), s (k, non-increasing),
+ * v (n x k, ldv >= n), column-major host buffers; k > rank -> QBFAC_DIMENSION_ERROR.
+ * `sweeps` (optional) receives the Jacobi sweep count. */
+int qbfac_gpu_result_svd(qbfac_gpu_result* res, int64_t k, double* u, int64_t ldu, double* s, double* v,
+                         int64_t ldv, int* sweeps);
 void qbfac_gpu_result_free(qbfac_gpu_result* res);
 
 /* Theorem 3 validity: returns 1 iff eps > sqrt(4 u / delta) ||A||_F. */

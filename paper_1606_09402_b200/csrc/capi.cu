@@ -424,6 +424,15 @@ int64_t qbfac_gpu_result_copy_trace(qbfac_gpu_result* res, double* out, int64_t 
     return static_cast<int64_t>(tr.size());
 }
 
+int qbfac_gpu_result_svd(qbfac_gpu_result* res, int64_t k, double* u, int64_t ldu, double* s, double* v,
+                         int64_t ldv, int* sweeps) {
+    if (!res) return QBFAC_ERROR;
+    return guard(res->ctx, [&] {
+        const int sw = qbgpu::qb_to_svd(*res->ctx->c, *res->r, k, u, ldu, s, v, ldv);
+        if (sweeps) *sweeps = sw;
+    });
+}
+
 void qbfac_gpu_result_free(qbfac_gpu_result* res) {
     if (!res) return;
     if (res->ctx && res->ctx->c) cudaSetDevice(res->ctx->c->device);

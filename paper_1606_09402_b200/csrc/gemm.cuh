@@ -77,6 +77,10 @@ void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, doubl
 // per 64-column diagonal block.
 void chol_wide(cudaStream_t st, double* w, std::int64_t ldw, int l, double* r, double* rinv, std::int64_t ldr,
                SmallStatus* stats);
+// One-sided Jacobi SVD of the r x r column-major N in place (N W = U Sigma, W must hold I on
+// entry): one cooperative launch, returns the number of sweeps.
+int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, int max_sweeps = 40);
+
 // Fused CholQR2 of a tall row-major panel Y (rows x b, b <= 112) in one cooperative launch:
 // g <- Y^T Y, (ra, rainv) <- chol, t1 <- Y ra^{-1}, g <- t1^T t1, (rb, rbinv) <- chol,
 // q <- t1 rb^{-1}; statuses of both Choleskies in st0 / st1. q may alias y. Small

@@ -978,6 +978,87 @@ void test_orth_wide(Context& c, const MatView& x, bool force_bcgs2) {
     QB_CUDA(cudaStreamSynchronize(c.st));
 }
 
+// ---- qb_to_svd (PAPER Eq. 1.3) ---------------------------------------
+// B (r x n) = N Q_b^T with Q_b = orth(B^T) (n x r, the wide CholQR2 / BCGS2 of the power step)
+// and N = B Q_b (r x r); one-sided Jacobi N W = U_r Sigma; then U = Q U_r(:, top k),
+// V = Q_b W(:, top k). Everything runs on the device; only Sigma (r doubles, for the order)
+// and the k columns of U, V leave it.
+namespace {
+__global__ void gather_scale_kernel(const double* __restrict__ src, int r, const int* __restrict__ idx,
+                                    const double* __restrict__ scale, int k, double* __restrict__ dst) {
+    const std::int64_t total = static_cast<std::int64_t>(r) * k;
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e % r), t = static_cast<int>(e / r);
+        const double sc = scale ? scale[t] : 1.0;
+        dst[e] = src[i + static_cast<std::int64_t>(idx[t]) * r] * sc;
+    }
+}
+}  // namespace
+
+int qb_to_svd(Context& c, Result& r, std::int64_t k, double* u_out, std::int64_t ldu, double* s_out, double* v_out,
+              std::int64_t ldv) {
+    const std::int64_t rk = r.rank, m = r.m, n = r.n;
+    if (k < 0 || k > rk) throw QbError(kDimensionError, "qb_to_svd: k too large");
+    if (k == 0) return 0;
+    if (ldu < m || ldv < n) throw QbError(kDimensionError, "qb_to_svd: leading dimension too small");
+    Matrix dummy;
+    Engine eng(c, dummy);
+    cudaStream_t st = c.st;
+    // Q_b = orth(B^T) on a packed copy
+    DBuf x(static_cast<std::size_t>(n) * rk, st);
+    MatView xv{x.p, n, rk, rk, true};
+    copy_matrix(st, r.bt_view(), xv);
+    DBuf tmp(static_cast<std::size_t>(std::max<std::int64_t>(n, 1)) * 64, st);
+    DBuf sbuf(static_cast<std::size_t>(std::max<std::int64_t>(rk, 64)) * 64, st);
+    eng.orth_wide(xv, false, tmp, sbuf);
+    // N = B Q_b (r x r, column-major), W = I
+    DBuf nm(static_cast<std::size_t>(rk) * rk, st), wm(static_cast<std::size_t>(rk) * rk, st);
+    MatView nv{nm.p, rk, rk, rk, false}, wv{wm.p, rk, rk, rk, false};
+    eng.gemm(1.0, r.bt_view().t(), xv, 0.0, nv);
+    set_identity(st, wv);
+    const int sweeps = jacobi_svd(st, nm.p, wm.p, static_cast<int>(rk), c.d_gbar);
+    // Sigma_j = ||N(:, j)||, descending order
+    DBuf nrm(static_cast<std::size_t>(rk), st);
+    column_sumsq(st, c.ws_red, nv, nrm.p);
+    std::vector<double> hs(static_cast<std::size_t>(rk));
+    QB_CUDA(cudaMemcpyAsync(hs.data(), nrm.p, sizeof(double) * rk, cudaMemcpyDeviceToHost, st));
+    QB_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> idx(static_cast<std::size_t>(rk));
+    for (std::int64_t i = 0; i < rk; ++i) idx[i] = static_cast<int>(i);
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return hs[a] > hs[b]; });
+    std::vector<double> sig(static_cast<std::size_t>(k)), inv(static_cast<std::size_t>(k));
+    for (std::int64_t t = 0; t < k; ++t) {
+        sig[t] = std::sqrt(hs[idx[t]]);
+        inv[t] = sig[t] > 0.0 ? 1.0 / sig[t] : 0.0;
+    }
+    DBuf aux(static_cast<std::size_t>(2 * k + 1), st);
+    int* d_idx = reinterpret_cast<int*>(aux.p);  // k ints in the first k/2 + 1 doubles
+    double* d_inv = aux.p + k;
+    QB_CUDA(cudaMemcpyAsync(d_idx, idx.data(), sizeof(int) * k, cudaMemcpyHostToDevice, st));
+    QB_CUDA(cudaMemcpyAsync(d_inv, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st));
+    DBuf uk(static_cast<std::size_t>(rk) * k, st), wk(static_cast<std::size_t>(rk) * k, st);
+    const int blocks = static_cast<int>(std::min<std::int64_t>(ceil_div(rk * k, 256), 4096));
+    gather_scale_kernel<<<blocks, 256, 0, st>>>(nm.p, static_cast<int>(rk), d_idx, d_inv, static_cast<int>(k), uk.p);
+    QB_LAUNCH_CHECK();
+    gather_scale_kernel<<<blocks, 256, 0, st>>>(wm.p, static_cast<int>(rk), d_idx, nullptr, static_cast<int>(k), wk.p);
+    QB_LAUNCH_CHECK();
+    // U = Q U_r(:, top k), V = Q_b W(:, top k), both column-major for the copy-out
+    DBuf ud(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * k, st), vd(static_cast<std::size_t>(n) * k, st);
+    MatView ukv{uk.p, rk, k, rk, false}, wkv{wk.p, rk, k, rk, false};
+    MatView udv{ud.p, m, k, std::max<std::int64_t>(m, 1), false}, vdv{vd.p, n, k, n, false};
+    eng.gemm(1.0, r.q_view(), ukv, 0.0, udv);
+    eng.gemm(1.0, xv, wkv, 0.0, vdv);
+    if (m > 0)
+        QB_CUDA(cudaMemcpy2DAsync(u_out, ldu * sizeof(double), ud.p, m * sizeof(double), m * sizeof(double), k,
+                                  cudaMemcpyDeviceToHost, st));
+    QB_CUDA(cudaMemcpy2DAsync(v_out, ldv * sizeof(double), vd.p, n * sizeof(double), n * sizeof(double), k,
+                              cudaMemcpyDeviceToHost, st));
+    QB_CUDA(cudaStreamSynchronize(st));
+    std::copy(sig.begin(), sig.end(), s_out);
+    return sweeps;
+}
+
 // ---- operator layer ------------------------------------------------------------------
 double frob_norm_sq(Context& c, Matrix& a) {
     Engine eng(c, a);

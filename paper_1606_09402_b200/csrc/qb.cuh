@@ -154,6 +154,11 @@ struct Result {
 
 std::unique_ptr<Result> run(Context& c, Matrix& a, const Params& p);
 
+// qb_to_svd: top-k U (m x k), S, V (n x k) of Q B into host buffers
+// (column-major, ldu >= m, ldv >= n); returns the Jacobi sweep count.
+int qb_to_svd(Context& c, Result& r, std::int64_t k, double* u, std::int64_t ldu, double* s, double* v,
+              std::int64_t ldv);
+
 // Kernel-level hook (include/qbfac_gpu_testing.h): orthonormalise a wide row-major panel.
 void test_orth_wide(Context& c, const MatView& x, bool force_bcgs2);
 

@@ -895,6 +895,82 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
     });
 }
 
+// ---- one-sided Jacobi SVD of a small square matrix (qb_to_svd) ---------
+// Hestenes one-sided Jacobi on the columns of N (r x r, column-major): rotations from the
+// right orthogonalise the columns, N W = U Sigma, W accumulates the rotations (W starts as
+// I). Round-robin (circle method) ordering: each step rotates r/2 disjoint column pairs,
+// one warp per pair (column dots reduced in a fixed order: deterministic), steps separated
+// by the nanosleep grid barrier; a sweep without any rotation above tol ends the loop.
+// One-sided Jacobi keeps high relative accuracy for the small singular values.
+struct JacobiArgs {
+    double* nmat;
+    double* w;
+    int r, rp, max_sweeps;
+    double tol;
+    unsigned* gbar;
+    unsigned* rotated;  // per-sweep rotation counters (zeroed before the launch)
+    int* sweeps_out;
+};
+
+__global__ void __launch_bounds__(256) jacobi_svd_kernel(JacobiArgs p) {
+    const int lane = threadIdx.x & 31;
+    const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int r = p.r, rp = p.rp, half = rp / 2;
+    int sweep = 0;
+    for (; sweep < p.max_sweeps; ++sweep) {
+        for (int step = 0; step < rp - 1; ++step) {
+            for (int t = gwarp; t < half; t += nwarps) {
+                // circle method: player rp-1 fixed, the others rotate
+                int a, b;
+                if (t == 0) {
+                    a = step;
+                    b = rp - 1;
+                } else {
+                    a = (step + t) % (rp - 1);
+                    b = (step - t + (rp - 1)) % (rp - 1);
+                }
+                if (a > b) { const int x = a; a = b; b = x; }
+                if (b >= r) continue;
+                double* cp = p.nmat + static_cast<std::int64_t>(a) * r;
+                double* cq = p.nmat + static_cast<std::int64_t>(b) * r;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = lane; i < r; i += 32) {
+                    const double x = cp[i], y = cq[i];
+                    al = fma(x, x, al);
+                    be = fma(y, y, be);
+                    ga = fma(x, y, ga);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o);
+                    be += __shfl_xor_sync(0xffffffffu, be, o);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+                }
+                if (!(fabs(ga) > p.tol * sqrt(al * be))) continue;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+                for (int i = lane; i < r; i += 32) {
+                    const double x = cp[i], y = cq[i];
+                    cp[i] = c * x - sn * y;
+                    cq[i] = sn * x + c * y;
+                }
+                double* wp = p.w + static_cast<std::int64_t>(a) * r;
+                double* wq = p.w + static_cast<std::int64_t>(b) * r;
+                for (int i = lane; i < r; i += 32) {
+                    const double x = wp[i], y = wq[i];
+                    wp[i] = c * x - sn * y;
+                    wq[i] = sn * x + c * y;
+                }
+                if (lane == 0) atomicAdd(p.rotated + sweep, 1u);
+            }
+            grid_barrier(p.gbar, gridDim.x);
+        }
+        if (*reinterpret_cast<volatile unsigned*>(p.rotated + sweep) == 0) break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.sweeps_out = sweep;
+}
+
 // C = A * B for upper-triangular n x n operands staged in shared memory; blockIdx.x
 // selects one of two independent products so R = Rb*Ra and Rinv = Ra^{-1} Rb^{-1}
 // are formed in one launch.
@@ -1250,6 +1326,26 @@ void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t
         case 96: launch_cholqr2_panel<96>(st, a, cap); break;
         default: launch_cholqr2_panel<112>(st, a, cap); break;
     }
+}
+
+int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, int max_sweeps) {
+    if (r < 1) return 0;
+    const int rp = r + (r & 1);
+    const int grid = std::max(1, std::min(gemm_num_sms(), (rp / 2 + 7) / 8));
+    unsigned* rotated = nullptr;
+    int* sweeps = nullptr;
+    QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rotated), sizeof(unsigned) * (max_sweeps + 1) + sizeof(int), st));
+    sweeps = reinterpret_cast<int*>(rotated + max_sweeps + 1);
+    QB_CUDA(cudaMemsetAsync(rotated, 0, sizeof(unsigned) * (max_sweeps + 1) + sizeof(int), st));
+    JacobiArgs a{nmat, w, r, rp, max_sweeps, 1e-15, gbar, rotated, sweeps};
+    void* args[] = {&a};
+    QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_svd_kernel), grid, 256, args, 0, st));
+    QB_LAUNCH_CHECK();
+    int h = 0;
+    QB_CUDA(cudaMemcpyAsync(&h, sweeps, sizeof(int), cudaMemcpyDeviceToHost, st));
+    QB_CUDA(cudaStreamSynchronize(st));
+    QB_CUDA(cudaFreeAsync(rotated, st));
+    return h;
 }
 
 void trmm_upper_small(cudaStream_t st, const double* a, const double* b, double* c, int n,

@@ -135,6 +135,7 @@ def lib():
         L.qbfac_gpu_result_copy_trace.argtypes = [P, P, I64]
         L.qbfac_gpu_result_copy_trace.restype = I64
         L.qbfac_gpu_result_free.argtypes = [P]
+        L.qbfac_gpu_result_svd.argtypes = [P, I64, P, I64, P, P, I64, P]
         L.qbfac_gpu_validate_epsilon.argtypes = [D, D, D, P]
         L.qbfac_mtx_last_error.restype = C.c_char_p
         L.qbfac_mtx_info.argtypes = [C.c_char_p, P, P, P, P]
@@ -497,8 +498,30 @@ class MatrixHandle:
 # ---- algorithms ------------------------------------------------------------------------------
 
 
+@dataclass
+class TruncatedSvd:
+    """U (m x k), S (k, non-increasing), V (n x k), A ~ U diag(S) V^T."""
+    U: np.ndarray
+    S: np.ndarray
+    V: np.ndarray
+    sweeps: int = 0
+
+
 class DeviceResult:
     """Result resident on the device; Q/B are copied to the host on demand."""
+
+    def svd(self, k: Optional[int] = None) -> TruncatedSvd:
+        """qb_to_svd(f, k) on the device: orth(B^T), one-sided Jacobi of the
+        r x r factor, U = Q U_r, V = Q_b W."""
+        k = self.rank if k is None else k
+        m, n = int(self.info.m), int(self.info.n)
+        u = np.zeros((m, k), order="F")
+        sv = np.zeros(k)
+        v = np.zeros((n, k), order="F")
+        sw = C.c_int(0)
+        self.ctx.check(lib().qbfac_gpu_result_svd(self._h, k, _p(u), max(m, 1), _p(sv), _p(v), max(n, 1),
+                                                  C.byref(sw)))
+        return TruncatedSvd(u, sv, v, sw.value)
 
     def __init__(self, h, ctx: Context, info: Info):
         self._h, self.ctx, self.info = h, ctx, info
