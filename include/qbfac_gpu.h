@@ -63,7 +63,12 @@ enum qbfac_alg {
     QBFAC_ALG_EI = 0,
     QBFAC_ALG_FP = 1,
     QBFAC_ALG_FP_FIXED_RANK = 2,
-    QBFAC_ALG_SINGLE_PASS = 3
+    QBFAC_ALG_SINGLE_PASS = 3,
+    /* baselines: randQB (l = k + s, power), randQB_b (stop rule, b; dense A),
+     * adaptive range finder (eps_abs = spectral tolerance, b = r window, max_rank) */
+    QBFAC_ALG_QB = 4,
+    QBFAC_ALG_QB_B = 5,
+    QBFAC_ALG_RANGE_FINDER = 6
 };
 
 /* StopRule plus the algorithm parameters of SPEC.md:273-308. */

@@ -24,7 +24,7 @@ REFERENCE_SRC = "/root/reference/proj"
 TERMINATION = {0: "rank_reached", 1: "tolerance_met", 2: "sketch_exhausted", 3: "rank_collapse"}
 STATUS = {0: "ok", 1: "DimensionError", 2: "SingularityError", 3: "ToleranceFloorError",
           4: "FormatError", 5: "ResourceError", 6: "Error", 7: "other"}
-ALG = {"ei": 0, "fp": 1, "fp_fixed_rank": 2, "single_pass": 3}
+ALG = {"ei": 0, "fp": 1, "fp_fixed_rank": 2, "single_pass": 3, "qb": 4, "qb_b": 5, "arf": 6}
 
 
 class QboParams(C.Structure):

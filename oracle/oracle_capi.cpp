@@ -26,7 +26,7 @@ using namespace qbfac;
 extern "C" {
 
 struct qbo_params {
-    std::int32_t alg;          // 0 EI, 1 FP, 2 FP fixed rank, 3 single pass
+    std::int32_t alg;          // 0 EI, 1 FP, 2 FP fixed rank, 3 single pass, 4 randQB, 5 randQB_b, 6 range finder
     std::int32_t mode;         // 0 fixed_rank, 1 fixed_precision
     std::int64_t b, power, k, s, max_rank, l_budget, max_restarts;
     double eps_abs;
@@ -113,6 +113,15 @@ QBFactorization run(const MatrixHandle& a, const qbo_params& p) {
             f.passes = a.passes();
             return f;
         }
+        case 4:
+            return rand_qb(a, p.k + p.s, static_cast<int>(p.power), rng);
+        case 5: {
+            StopRule stop = p.mode == 1 ? StopRule::fixed_precision(p.eps_abs)
+                                        : StopRule::fixed_rank(p.k, p.s);
+            return rand_qb_b(a, stop, p.b, rng);
+        }
+        case 6:
+            return adaptive_range_finder(a, p.eps_abs, p.b, rng, p.max_rank);
         default:
             throw Error("unknown algorithm id");
     }

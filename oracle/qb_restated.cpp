@@ -191,6 +191,143 @@ index fp_block(QBState& st, const DenseMatrix& yi, const DenseMatrix& hi, const 
 
 }  // namespace
 
+// ---- baselines ----------------------------------------------------------------------
+namespace {
+// orth with the reference's deficiency rule: leading columns before the first |R_jj| <=
+// 1e-12 max|R_jj| (qr.hpp:20-21); `collapsed` is set when columns were dropped.
+DenseMatrix orth_leading(const DenseMatrix& y, bool& collapsed) {
+    QrResult qr = orth_qr(y);
+    const index d = leading_rank(qr.r);
+    if (d < y.cols()) collapsed = true;
+    return qr.q.leading_columns(d);
+}
+}  // namespace
+
+QBFactorization rand_qb(const MatrixHandle& a, index l, int power, RngStream& rng) {
+    const index m = a.rows(), n = a.cols();
+    if (l == 0 || l > std::min(m, n)) throw DimensionError("rand_qb: l must be in [1, min(m, n)]");
+    const std::int64_t p0 = a.passes();
+    bool collapsed = false;
+    DenseMatrix omega = gaussian(n, l, rng);
+    DenseMatrix q = orth_leading(a.multiply(omega, false), collapsed);
+    for (int p = 0; p < power; ++p) {
+        DenseMatrix w = orth_leading(a.multiply(q, true), collapsed);
+        q = orth_leading(a.multiply(w, false), collapsed);
+    }
+    DenseMatrix bt = a.multiply(q, true);
+    QBState st(m, n);
+    st.q = std::move(q);
+    st.bt = std::move(bt);
+    st.k = st.q.cols();
+    st.e = -1.0;  // SPEC.md:212 sentinel: randQB keeps no error indicator
+    return finish(st, &a, p0, collapsed ? Termination::rank_collapse : Termination::rank_reached, 0.0);
+}
+
+QBFactorization rand_qb_b(const MatrixHandle& a, const StopRule& stop, index b, RngStream& rng) {
+    if (b == 0) throw DimensionError("rand_qb_b: block size must be >= 1");
+    if (a.is_sparse()) throw DimensionError("rand_qb_b: dense A only (the residual is dense)");
+    const index m = a.rows(), n = a.cols();
+    const std::int64_t p0 = a.passes();
+    const bool fixed_prec = stop.mode == StopRule::Mode::fixed_precision;
+    const index cap = fixed_prec ? std::min(m, n) : std::min(std::min(m, n), stop.k + stop.s);
+    const double eps2 = stop.eps * stop.eps;
+    DenseMatrix res = a.dense();  // explicit residual R = A - Q B
+    QBState st(m, n);
+    double norm_a_sq = 0.0;
+    Termination term = Termination::rank_reached;
+    while (true) {
+        if (st.k >= cap) { term = Termination::rank_reached; break; }
+        st.e = frob_norm_sq(res);                       // ||R||_F^2 (one pass over R)
+        a.pass_counter().add(1);
+        if (st.k == 0) {
+            norm_a_sq = st.e;
+            if (fixed_prec) check_eps(stop.eps, norm_a_sq);
+        }
+        if (fixed_prec && st.e < eps2) { term = Termination::tolerance_met; break; }
+        const index bi = std::min(b, cap - st.k);
+        DenseMatrix omega = gaussian(n, bi, rng);
+        DenseMatrix y = multiply(res, omega);           // R Omega_i
+        a.pass_counter().add(1);
+        QrResult qr1 = orth_qr(y);
+        index d = leading_rank(qr1.r);
+        if (d == 0) { term = Termination::rank_collapse; break; }
+        DenseMatrix qi = qr1.q.leading_columns(d);
+        if (st.k > 0) {                                  // re-orthogonalisation against Q
+            st.project_out(qi);
+            QrResult qr2 = orth_qr(qi);
+            const index d2 = leading_rank(qr2.r);
+            if (d2 == 0) { term = Termination::rank_collapse; break; }
+            d = std::min(d, d2);
+            qi = qr2.q.leading_columns(d);
+        }
+        DenseMatrix bti = multiply_at_b(res, qi);       // B_i^T = R^T Q_i
+        a.pass_counter().add(1);
+        const index k0 = st.k;
+        const bool met = st.append(qi, bti, fixed_prec, eps2);
+        const index kept = st.k - k0;
+        DenseMatrix qk = st.q.column_range(k0, st.k), bk = st.bt.column_range(k0, st.k);
+        multiply_acc(res, qk, bk.transposed(), -1.0);   // R -= Q_i B_i
+        a.pass_counter().add(1);
+        if (met) { term = Termination::tolerance_met; break; }
+        if (kept < bi) { term = Termination::rank_collapse; break; }
+    }
+    st.trace.clear();
+    return finish(st, &a, p0, term, norm_a_sq);
+}
+
+QBFactorization adaptive_range_finder(const MatrixHandle& a, double tol_spectral, index r, RngStream& rng,
+                                      index max_rank) {
+    if (r == 0) throw DimensionError("adaptive_range_finder: r must be >= 1");
+    const index m = a.rows(), n = a.cols();
+    const std::int64_t p0 = a.passes();
+    index cap = std::min(m, n);
+    if (max_rank > 0) cap = std::min(cap, max_rank);
+    const double thr = tol_spectral / (10.0 * std::sqrt(2.0 / 3.14159265358979323846));
+    const auto& kt = kernels::active_kernels();
+    auto nrm = [&](const DenseMatrix& v) { return std::sqrt(kt.sum_sq(v.data(), v.rows())); };
+    QBState st(m, n);
+    // y_1..y_r = A omega_i (r passes)
+    std::vector<DenseMatrix> ys;
+    {
+        DenseMatrix om = gaussian(n, r, rng);
+        for (index i = 0; i < r; ++i) ys.push_back(a.multiply(om.column_range(i, i + 1), false));
+    }
+    auto project = [&](DenseMatrix& v) {  // v - Q (Q^T v)
+        if (st.k == 0) return;
+        DenseMatrix c = multiply_at_b(st.q, v);
+        multiply_acc(v, st.q, c, -1.0);
+    };
+    index head = 0;  // ys[head .. head + r) is the current window
+    Termination term = Termination::tolerance_met;
+    while (true) {
+        double mx = 0.0;
+        for (index i = 0; i < r; ++i) mx = std::max(mx, nrm(ys[head + i]));
+        if (!(mx > thr)) { term = Termination::tolerance_met; break; }
+        if (st.k >= cap) { term = Termination::rank_reached; break; }
+        DenseMatrix y = ys[head];
+        project(y);                                      // y_j = (I - Q Q^T) y_j
+        const double yn = nrm(y);
+        if (!(yn > 0.0)) { term = Termination::rank_collapse; break; }
+        for (index i = 0; i < m; ++i) y(i, 0) /= yn;    // q_j
+        st.q.append_columns(y);
+        st.k += 1;
+        DenseMatrix om = gaussian(n, 1, rng);            // omega_{j+r}
+        DenseMatrix ynew = a.multiply(om, false);        // one pass
+        project(ynew);
+        for (index i = 1; i < r; ++i) {                  // y_i -= q_j (q_j^T y_i)
+            DenseMatrix& v = ys[head + i];
+            double c = 0.0;
+            for (index t = 0; t < m; ++t) c += y(t, 0) * v(t, 0);
+            for (index t = 0; t < m; ++t) v(t, 0) -= c * y(t, 0);
+        }
+        ys.push_back(std::move(ynew));
+        ++head;
+    }
+    st.bt = a.multiply(st.q, true);                      // B = Q^T A (one pass)
+    st.e = -1.0;
+    return finish(st, &a, p0, term, 0.0);
+}
+
 EpsilonCheck validate_epsilon(double eps, double frob_a, double delta) {
     const double floor = std::sqrt(4.0 * kEpsMach / delta) * frob_a;
     return {eps > floor, floor};

@@ -75,6 +75,20 @@ QBFactorization rand_qb_fp_fixed_rank(const MatrixHandle& a, index k, index s, i
 // Remark 4.2.
 QBFactorization single_pass_fp(RowStream& stream, index l, index b, RngStream& rng);
 
+// ---- baselines (§8(f) 4) ----
+// randQB (Fig. 1a): Q = orth of the power-iterated sketch (orth after every application of
+// A and A^T), B = Q^T A; passes = 2 + 2P; E is the -1 sentinel; a deficient QR keeps the
+// leading columns and ends rank_collapse.
+QBFactorization rand_qb(const MatrixHandle& a, index l, int power, RngStream& rng);
+// randQB_b (Fig. 1b): explicit residual R (dense A only); per block: E = ||R||_F^2 (pass),
+// Y = R Omega_i (pass), Q_i = orth(Y) re-orthogonalised against Q, B_i = Q_i^T R (pass) with the
+// row-by-row truncation of PAPER.md:206-220 on E, R -= Q_i B_i (pass): 4 passes per block.
+QBFactorization rand_qb_b(const MatrixHandle& a, const StopRule& stop, index b, RngStream& rng);
+// Adaptive randomized range finder (Eq. 2.4, Halko et al. Alg. 4.2): Q grows one vector at a
+// time until the last r residual samples are all below tol / (10 sqrt(2/pi)); B = Q^T A.
+QBFactorization adaptive_range_finder(const MatrixHandle& a, double tol_spectral, index r, RngStream& rng,
+                                      index max_rank = 0);
+
 // ||A - QB||_F streamed over column blocks of 256 (+1 pass).
 double explicit_error(const MatrixHandle& a, const DenseMatrix& q, const DenseMatrix& b);
 

@@ -1073,12 +1073,233 @@ void multiply(Context& c, Matrix& a, const MatView& x, const MatView& y, bool tr
     a.passes += 1;
 }
 
+// ---- baselines (§8(f) 4) ---------------------------------------------
+// Orthonormal basis of Y's leading columns with the reference's deficiency rule; returns
+// the kept width (panels <= 112 columns: exact Householder decision on CholQR failure;
+// wider: wide CholQR2 / BCGS2, full width).
+int orth_any(Engine& eng, const MatView& y, bool sharded, DBuf& tmp, DBuf& sbuf) {
+    if (y.cols <= kSmallMax) return eng.orth_block(y, y, kR1, kR1inv, sharded, tmp, false);
+    eng.orth_wide(y, sharded, tmp, sbuf);
+    return static_cast<int>(y.cols);
+}
+
+// randQB (Fig. 1a): Q = orth((A A^T)^P A Omega) with orth after every application, B = Q^T A.
+std::unique_ptr<Result> run_qb(Context& c, Matrix& a, const Params& p) {
+    const std::int64_t m = a.m, n = a.n, l = p.k + p.s;
+    if (l < 1 || l > std::min(a.m_global, n)) throw QbError(kDimensionError, "rand_qb: l must be in [1, min(m, n)]");
+    Engine eng(c, a);
+    const bool sharded = c.world > 1;
+    const std::int64_t passes0 = a.passes;
+    State s(c, eng, m, n, l);
+    DBuf om(static_cast<std::size_t>(n) * even(l), c.st);
+    DBuf tmp(static_cast<std::size_t>(std::max<std::int64_t>(std::max(m, n), 1)) * 64, c.st);
+    DBuf sbuf(static_cast<std::size_t>(std::max<std::int64_t>(l, 64)) * 64, c.st);
+    MatView omv{om.p, n, l, l, true};
+    gaussian_fill(c.st, c.rng, p.seed, p.stream, 0, omv);
+    std::int64_t d = l;
+    bool collapsed = false;
+    MatView y{s.q.p, m, d, s.ld, true};
+    eng.apply(omv, y); a.passes += 1;
+    auto orth_y = [&](const MatView& v) {
+        const int dd = orth_any(eng, v, sharded && v.rows == m, tmp, sbuf);
+        if (dd < v.cols) collapsed = true;
+        return static_cast<std::int64_t>(dd);
+    };
+    d = orth_y(y);
+    for (std::int64_t it = 0; it < p.power && d > 0; ++it) {
+        MatView w{om.p, n, d, d, true};
+        eng.apply_t(MatView{s.q.p, m, d, s.ld, true}, w); a.passes += 1;
+        d = orth_y(w);
+        if (d == 0) break;
+        MatView yy{s.q.p, m, d, s.ld, true};
+        eng.apply(MatView{om.p, n, d, d, true}, yy); a.passes += 1;
+        d = orth_y(yy);
+    }
+    s.k = d;
+    if (d > 0) { eng.apply_t(s.qk(), s.btk()); }
+    a.passes += 1;
+    s.set_e(-1.0);  // SPEC.md:212 sentinel: no error indicator
+    auto r = finish(s, a, passes0, collapsed ? 3 : 0, 0.0);
+    r->hh_fallbacks = eng.hh_fallbacks;
+    return r;
+}
+
+// randQB_b (Fig. 1b): explicit residual, 4 passes per block.
+std::unique_ptr<Result> run_qb_b(Context& c, Matrix& a, const Params& p) {
+    if (p.b < 1) throw QbError(kDimensionError, "rand_qb_b: block size must be >= 1");
+    if (a.sparse || a.host_stream) throw QbError(kDimensionError, "rand_qb_b: dense A only (the residual is dense)");
+    a.wait_resident(c.st);
+    const std::int64_t m = a.m, n = a.n;
+    const bool fixed_prec = p.mode == 1;
+    std::int64_t cap = std::min(a.m_global, n);
+    if (!fixed_prec) cap = std::min(cap, p.k + p.s);
+    Engine eng(c, a);
+    const bool sharded = c.world > 1;
+    const std::int64_t passes0 = a.passes;
+    State s(c, eng, m, n, cap);
+    s.eps2 = fixed_prec ? p.eps_abs * p.eps_abs : 0.0;
+    // residual R = A (column-major, same layout as A)
+    DBuf res(static_cast<std::size_t>(a.lda) * std::max<std::int64_t>(n, 1), c.st);
+    MatView rv{res.p, m, n, a.lda, false};
+    copy_matrix(c.st, a.dense_view(), rv);
+    const std::int64_t bmax = std::min<std::int64_t>(p.b, std::max<std::int64_t>(cap, 1));
+    DBuf om(static_cast<std::size_t>(n) * even(bmax), c.st);
+    DBuf tmp(static_cast<std::size_t>(std::max<std::int64_t>(std::max(m, n), 1)) * even(bmax), c.st);
+    DBuf mbuf(static_cast<std::size_t>(std::max<std::int64_t>(cap, 1)) * even(bmax), c.st);
+    double norm_a_sq = 0.0;
+    int term = 0;
+    std::int64_t g_used = 0, blocks = 0;
+    while (true) {
+        if (s.k >= cap) { term = 0; break; }
+        sum_squares(c.st, c.ws_red, rv, s.d_e);              // E = ||R||_F^2 (one pass over R)
+        c.allreduce(s.d_e, 1);
+        a.passes += 1;
+        const double e = s.get_e();
+        if (!std::isfinite(e)) throw QbError(kError, "from_data: non-finite entry");
+        if (s.k == 0) {
+            norm_a_sq = e;
+            if (fixed_prec) check_eps(p.eps_abs, norm_a_sq);
+        }
+        if (fixed_prec && e < s.eps2) { term = 1; break; }
+        const std::int64_t bi = std::min(p.b, cap - s.k);
+        ++blocks;
+        MatView omv{om.p, n, bi, bi, true};
+        gaussian_fill(c.st, c.rng, p.seed, p.stream, static_cast<std::uint64_t>(g_used), omv);
+        g_used += n * bi;
+        MatView qs = s.qslot(bi);
+        eng.gemm(1.0, rv, omv, 0.0, qs);                    // Y = R Omega_i
+        a.passes += 1;
+        int d = eng.orth_block(qs, qs, kR1, kR1inv, sharded, tmp, false);
+        if (d > 0 && s.k > 0) {                              // re-orthogonalisation against Q
+            MatView qd = s.qslot(d);
+            MatView md{mbuf.p, s.k, d, d, true};
+            eng.gemm(1.0, s.qk().t(), qd, 0.0, md);
+            eng.allreduce_view(md);
+            eng.gemm(-1.0, s.qk(), md, 1.0, qd);
+            d = std::min(d, eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp, false));
+        }
+        if (d == 0) { term = 3; break; }
+        MatView bts = s.btslot(d);
+        eng.gemm(1.0, rv.t(), s.qslot(d), 0.0, bts);         // B_i^T = R^T Q_i
+        eng.allreduce_view(bts);
+        a.passes += 1;
+        const auto [keep, met] = s.indicator(d, fixed_prec);  // rows of B_i enter E
+        eng.gemm(-1.0, s.qslot(keep), s.btslot(keep).t(), 1.0, rv);  // R -= Q_i B_i
+        a.passes += 1;
+        s.k += keep;
+        if (met) { term = 1; break; }
+        if (keep < bi) { term = 3; break; }
+    }
+    s.trace.clear();
+    auto r = finish(s, a, passes0, term, norm_a_sq);
+    r->gaussians_used = g_used;
+    r->blocks = blocks;
+    r->hh_fallbacks = eng.hh_fallbacks;
+    return r;
+}
+
+// Adaptive randomized range finder (Eq. 2.4; Halko et al. Alg. 4.2): Q grows one vector at a
+// time; stops when the r most recent residual samples are all <= tol / (10 sqrt(2/pi)).
+std::unique_ptr<Result> run_arf(Context& c, Matrix& a, const Params& p) {
+    const std::int64_t r = p.b;
+    if (r < 1) throw QbError(kDimensionError, "adaptive_range_finder: r must be >= 1");
+    if (c.world > 1) throw QbError(kError, "adaptive_range_finder: single GPU only");
+    const std::int64_t m = a.m, n = a.n;
+    std::int64_t cap = std::min(m, n);
+    if (p.max_rank > 0) cap = std::min(cap, p.max_rank);
+    Engine eng(c, a);
+    const std::int64_t passes0 = a.passes;
+    State s(c, eng, m, n, cap);
+    const double thr = p.eps_abs / (10.0 * std::sqrt(2.0 / 3.14159265358979323846));
+    // window of r samples, column-major m x r (each sample contiguous), plus scratch
+    DBuf win(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * r, c.st);
+    DBuf om(static_cast<std::size_t>(n) * r, c.st);
+    DBuf yv(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)), c.st);
+    DBuf cv(static_cast<std::size_t>(std::max<std::int64_t>(cap, r) + 1), c.st);
+    DBuf nrm(static_cast<std::size_t>(r + 1), c.st);
+    std::vector<double> hn(static_cast<std::size_t>(r + 1));
+    std::uint64_t g_used = 0;
+    {   // y_1..y_r = A omega_i, one pass each
+        MatView omv{om.p, n, r, r, true};
+        gaussian_fill(c.st, c.rng, p.seed, p.stream, 0, omv);
+        g_used = static_cast<std::uint64_t>(n * r);
+        MatView wv{win.p, m, r, std::max<std::int64_t>(m, 1), false};
+        for (std::int64_t i = 0; i < r; ++i) {
+            MatView oi{om.p + i, n, 1, r, true};
+            MatView yi{win.p + i * m, m, 1, 1, true};
+            eng.apply(oi, yi);
+            a.passes += 1;
+        }
+        (void)wv;
+    }
+    auto project = [&](double* v) {  // v -= Q (Q^T v)
+        if (s.k == 0) return;
+        MatView vv{v, m, 1, 1, true};
+        MatView cc{cv.p, s.k, 1, 1, true};
+        eng.gemm(1.0, s.qk().t(), vv, 0.0, cc);
+        eng.gemm(-1.0, s.qk(), cc, 1.0, vv);
+    };
+    std::int64_t head = 0;
+    int term = 1;
+    while (true) {
+        MatView wv{win.p, m, r, std::max<std::int64_t>(m, 1), false};
+        column_sumsq(c.st, c.ws_red, wv, nrm.p);
+        QB_CUDA(cudaMemcpyAsync(hn.data(), nrm.p, sizeof(double) * r, cudaMemcpyDeviceToHost, c.st));
+        QB_CUDA(cudaStreamSynchronize(c.st));
+        double mx = 0.0;
+        for (std::int64_t i = 0; i < r; ++i) mx = std::max(mx, std::sqrt(hn[i]));
+        if (!(mx > thr)) { term = 1; break; }
+        if (s.k >= cap) { term = 0; break; }
+        // q_j = (I - Q Q^T) y_head, normalised
+        double* yh = win.p + head * m;
+        QB_CUDA(cudaMemcpyAsync(yv.p, yh, sizeof(double) * m, cudaMemcpyDeviceToDevice, c.st));
+        project(yv.p);
+        MatView y1{yv.p, m, 1, 1, true};
+        column_sumsq(c.st, c.ws_red, MatView{yv.p, m, 1, std::max<std::int64_t>(m, 1), false}, nrm.p + r);
+        QB_CUDA(cudaMemcpyAsync(hn.data() + r, nrm.p + r, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+        QB_CUDA(cudaStreamSynchronize(c.st));
+        const double yn = std::sqrt(hn[r]);
+        if (!(yn > 0.0)) { term = 3; break; }
+        scale_matrix(c.st, y1, 1.0 / yn);
+        MatView qj = s.qslot(1);
+        copy_matrix(c.st, y1, qj);
+        // omega_{j+r}: one pass; then all window samples lose their q_j component
+        MatView o1{om.p, n, 1, 1, true};
+        gaussian_fill(c.st, c.rng, p.seed, p.stream, g_used, o1);
+        g_used += static_cast<std::uint64_t>(n);
+        s.k += 1;
+        MatView whead{yh, m, 1, 1, true};
+        eng.apply(o1, whead);
+        a.passes += 1;
+        // the new sample is projected against Q (with q_j); the others lose q_j's component
+        project(yh);
+        for (std::int64_t i = 0; i < r; ++i) {
+            if (i == head) continue;
+            double* yi = win.p + i * m;
+            MatView vi{yi, m, 1, 1, true};
+            MatView cc{cv.p, 1, 1, 1, true};
+            eng.gemm(1.0, y1.t(), vi, 0.0, cc);
+            eng.gemm(-1.0, y1, cc, 1.0, vi);
+        }
+        head = (head + 1) % r;
+    }
+    if (s.k > 0) eng.apply_t(s.qk(), s.btk());
+    a.passes += 1;
+    s.set_e(-1.0);
+    auto res = finish(s, a, passes0, term, 0.0);
+    res->gaussians_used = static_cast<std::int64_t>(g_used);
+    return res;
+}
+
 std::unique_ptr<Result> run(Context& c, Matrix& a, const Params& p) {
     Timer t(c.st);
     std::unique_ptr<Result> r;
     switch (p.alg) {
         case 0: r = run_ei(c, a, p); break;
         case 1: case 2: case 3: r = run_fp(c, a, p); break;
+        case 4: r = run_qb(c, a, p); break;
+        case 5: r = run_qb_b(c, a, p); break;
+        case 6: r = run_arf(c, a, p); break;
         default: throw QbError(kError, "unknown algorithm id");
     }
     r->device_ms = t.stop();

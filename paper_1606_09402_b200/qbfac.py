@@ -600,6 +600,37 @@ def rand_qb_ei(A: MatrixHandle, stop: StopRule, b: int, P: int, rng: RngStream,
     return _to_host(res)
 
 
+def rand_qb(A: MatrixHandle, l: int, P: int, rng: RngStream) -> QBFactorization:
+    """randQB (Fig. 1a): Q = orth of the power-iterated sketch, B = Q^T A,
+    passes = 2 + 2P, E = -1 (no indicator)."""
+    if rng.consumed:
+        raise Error("rand_qb: the device path needs a fresh RngStream")
+    res = run_device(A, alg=4, mode=0, b=l, power=P, k=l, s=0, seed=rng.seed_, stream=rng.stream_)
+    rng.consumed += A.n * l
+    return _to_host(res)
+
+
+def rand_qb_b(A: MatrixHandle, stop: StopRule, b: int, rng: RngStream) -> QBFactorization:
+    """randQB_b (Fig. 1b): explicit residual (dense A), 4 passes per block."""
+    if rng.consumed:
+        raise Error("rand_qb_b: the device path needs a fresh RngStream")
+    res = run_device(A, alg=5, mode=1 if stop.mode == "fixed_precision" else 0, b=b, k=stop.k, s=stop.s,
+                     eps_abs=stop.eps, seed=rng.seed_, stream=rng.stream_)
+    rng.consumed += int(res.info.gaussians_used)
+    return _to_host(res)
+
+
+def adaptive_range_finder(A: MatrixHandle, tol_spectral: float, r: int, rng: RngStream,
+                          max_rank: int = 0) -> QBFactorization:
+    """Adaptive randomized range finder (Eq. 2.4): one vector at a time until the
+    last r residual samples are below tol / (10 sqrt(2/pi)); B = Q^T A at the end."""
+    if rng.consumed:
+        raise Error("adaptive_range_finder: the device path needs a fresh RngStream")
+    res = run_device(A, alg=6, b=r, max_rank=max_rank, eps_abs=tol_spectral, seed=rng.seed_, stream=rng.stream_)
+    rng.consumed += int(res.info.gaussians_used)
+    return _to_host(res)
+
+
 def rand_qb_fp(A: MatrixHandle, eps: float, b: int, P: int, l_budget: int, rng: RngStream,
                max_rank: int = 0, max_restarts: int = 8) -> QBFactorization:
     """Alg. 4 on the device."""
