@@ -81,6 +81,154 @@ __device__ __forceinline__ void row_dot(const std::int32_t* __restrict__ ci, con
     for (int q = 0; q < NQ; ++q) acc[q] = (acc[q] + a1[q]) + (a2[q] + a3[q]);
 }
 
+// 16-byte variant: lane owns the column pairs (2 lane + 64 q, +1), so one load instruction
+// moves a 512-byte slice of an X row (half the L2 requests of the 8-byte version). Needs
+// ldx even and a 16-byte aligned x; for odd w the pair straddling w reads the row padding,
+// whose lane-local accumulator is never stored.
+template <int NQ2>
+__device__ __forceinline__ void row_dot2(const std::int32_t* __restrict__ ci, const double* __restrict__ v,
+                                         const double* __restrict__ x, std::int64_t ldx, int w, std::int64_t e0,
+                                         std::int64_t e1, int lane, double2 (&acc)[NQ2]) {
+    double2 a1[NQ2], a2[NQ2], a3[NQ2];
+#pragma unroll
+    for (int q = 0; q < NQ2; ++q) a1[q] = a2[q] = a3[q] = make_double2(0.0, 0.0);
+    for (std::int64_t eb = e0; eb < e1; eb += 32) {
+        const int cnt = static_cast<int>(e1 - eb < 32 ? e1 - eb : 32);
+        std::int32_t my_c = 0;
+        double my_v = 0.0;
+        if (lane < cnt) {
+            my_c = __ldg(ci + eb + lane);
+            my_v = __ldg(v + eb + lane);
+        }
+        int j = 0;
+        for (; j + 4 <= cnt; j += 4) {
+            const double2* x0 = reinterpret_cast<const double2*>(x + static_cast<std::int64_t>(__shfl_sync(0xffffffffu, my_c, j)) * ldx);
+            const double2* x1 = reinterpret_cast<const double2*>(x + static_cast<std::int64_t>(__shfl_sync(0xffffffffu, my_c, j + 1)) * ldx);
+            const double2* x2 = reinterpret_cast<const double2*>(x + static_cast<std::int64_t>(__shfl_sync(0xffffffffu, my_c, j + 2)) * ldx);
+            const double2* x3 = reinterpret_cast<const double2*>(x + static_cast<std::int64_t>(__shfl_sync(0xffffffffu, my_c, j + 3)) * ldx);
+            const double v0 = __shfl_sync(0xffffffffu, my_v, j), v1 = __shfl_sync(0xffffffffu, my_v, j + 1);
+            const double v2 = __shfl_sync(0xffffffffu, my_v, j + 2), v3 = __shfl_sync(0xffffffffu, my_v, j + 3);
+            double2 g0[NQ2], g1[NQ2], g2[NQ2], g3[NQ2];
+#pragma unroll
+            for (int q = 0; q < NQ2; ++q) {
+                const int pc = lane + 32 * q;  // pair index
+                const bool ok = 2 * pc < w;
+                const double2 z = make_double2(0.0, 0.0);
+                g0[q] = ok ? __ldg(x0 + pc) : z;
+                g1[q] = ok ? __ldg(x1 + pc) : z;
+                g2[q] = ok ? __ldg(x2 + pc) : z;
+                g3[q] = ok ? __ldg(x3 + pc) : z;
+            }
+#pragma unroll
+            for (int q = 0; q < NQ2; ++q) {
+                acc[q].x = fma(v0, g0[q].x, acc[q].x);
+                acc[q].y = fma(v0, g0[q].y, acc[q].y);
+                a1[q].x = fma(v1, g1[q].x, a1[q].x);
+                a1[q].y = fma(v1, g1[q].y, a1[q].y);
+                a2[q].x = fma(v2, g2[q].x, a2[q].x);
+                a2[q].y = fma(v2, g2[q].y, a2[q].y);
+                a3[q].x = fma(v3, g3[q].x, a3[q].x);
+                a3[q].y = fma(v3, g3[q].y, a3[q].y);
+            }
+        }
+        for (; j < cnt; ++j) {
+            const double2* xr = reinterpret_cast<const double2*>(x + static_cast<std::int64_t>(__shfl_sync(0xffffffffu, my_c, j)) * ldx);
+            const double a = __shfl_sync(0xffffffffu, my_v, j);
+#pragma unroll
+            for (int q = 0; q < NQ2; ++q) {
+                const int pc = lane + 32 * q;
+                if (2 * pc < w) {
+                    const double2 g = __ldg(xr + pc);
+                    acc[q].x = fma(a, g.x, acc[q].x);
+                    acc[q].y = fma(a, g.y, acc[q].y);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ2; ++q) {
+        acc[q].x = (acc[q].x + a1[q].x) + (a2[q].x + a3[q].x);
+        acc[q].y = (acc[q].y + a1[q].y) + (a2[q].y + a3[q].y);
+    }
+}
+
+template <int NQ2>
+__device__ __forceinline__ void store_row2(double* __restrict__ yr, int w, int lane, const double2 (&acc)[NQ2],
+                                           double alpha, double beta) {
+#pragma unroll
+    for (int q = 0; q < NQ2; ++q) {
+        const int col = 2 * (lane + 32 * q);
+        if (col + 1 < w) {
+            double2 r = make_double2(alpha * acc[q].x, alpha * acc[q].y);
+            if (beta != 0.0) {
+                const double2 o = *reinterpret_cast<const double2*>(yr + col);
+                r.x += beta * o.x;
+                r.y += beta * o.y;
+            }
+            *reinterpret_cast<double2*>(yr + col) = r;
+        } else if (col < w) {
+            const double r = alpha * acc[q].x;
+            yr[col] = beta == 0.0 ? r : r + beta * yr[col];
+        }
+    }
+}
+
+template <int NQ2>
+__global__ void __launch_bounds__(256, 4)
+csr_spmm_kernel2(std::int64_t rows, const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
+                 const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx,
+                 double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, bool y_vec) {
+    const int lane = threadIdx.x & 31;
+    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (std::int64_t i = warp; i < rows; i += nwarps) {
+        const std::int64_t e0 = rp[i], e1 = rp[i + 1];
+        if (e1 - e0 > kHeavyRow) continue;  // heavy rows: segment kernels
+        double2 acc[NQ2];
+#pragma unroll
+        for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
+        row_dot2<NQ2>(ci, v, x, ldx, w, e0, e1, lane, acc);
+        double* yr = y + i * ldy;
+        if (y_vec) {
+            store_row2<NQ2>(yr, w, lane, acc, alpha, beta);
+        } else {
+#pragma unroll
+            for (int q = 0; q < NQ2; ++q)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = 2 * (lane + 32 * q) + h;
+                    if (col < w) {
+                        const double r = alpha * (h ? acc[q].y : acc[q].x);
+                        yr[col] = beta == 0.0 ? r : r + beta * yr[col];
+                    }
+                }
+        }
+    }
+}
+
+template <int NQ2>
+__global__ void __launch_bounds__(256)
+csr_segment_kernel2(std::int64_t nseg, const std::int64_t* __restrict__ seg, const std::int32_t* __restrict__ ci,
+                    const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx, int w,
+                    double* __restrict__ partial) {
+    const int lane = threadIdx.x & 31;
+    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (std::int64_t s = warp; s < nseg; s += nwarps) {
+        double2 acc[NQ2];
+#pragma unroll
+        for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
+        row_dot2<NQ2>(ci, v, x, ldx, w, seg[nseg + s], seg[2 * nseg + s], lane, acc);
+#pragma unroll
+        for (int q = 0; q < NQ2; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int col = 2 * (lane + 32 * q) + h;
+                if (col < w) partial[s * w + col] = h ? acc[q].y : acc[q].x;
+            }
+    }
+}
+
 // Heavy-row segments: warp per segment, partial row into partial[seg * w + col].
 template <int NQ>
 __global__ void __launch_bounds__(256)
@@ -287,6 +435,25 @@ void free_heavy_plan(HeavyPlan& p) {
 }
 
 namespace {
+template <int NQ2>
+void spmm_launch2(cudaStream_t st, const CsrView& a, const double* x, std::int64_t ldx, double* y, std::int64_t ldy,
+                  int w, double alpha, double beta, int sms, double* partial) {
+    const int threads = 256;
+    const int blocks = static_cast<int>(std::max<std::int64_t>(
+        1, std::min<std::int64_t>(ceil_div(a.rows * 32, threads), 16L * sms)));
+    const bool y_vec = (ldy % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(y) & 15) == 0);
+    csr_spmm_kernel2<NQ2><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, y_vec);
+    QB_LAUNCH_CHECK();
+    if (a.heavy.nseg > 0) {
+        const int sb = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(a.heavy.nseg * 32, threads), 16L * sms)));
+        csr_segment_kernel2<NQ2><<<sb, threads, 0, st>>>(a.heavy.nseg, a.heavy.seg, a.ci, a.v, x, ldx, w, partial);
+        QB_LAUNCH_CHECK();
+        csr_heavy_combine_kernel<<<static_cast<int>(std::min<std::int64_t>(a.heavy.nrows, 65535)), 128, 0, st>>>(
+            a.heavy.nrows, a.heavy.rows, partial, y, ldy, w, alpha, beta);
+        QB_LAUNCH_CHECK();
+    }
+}
+
 template <int NQ>
 void spmm_launch(cudaStream_t st, const CsrView& a, const double* x, std::int64_t ldx, double* y, std::int64_t ldy,
                  int w, double alpha, double beta, int sms, double* partial) {
@@ -310,6 +477,10 @@ void csr_spmm(cudaStream_t st, const CsrView& a, const double* x, std::int64_t l
               int w, double alpha, double beta, int sms, double* partial) {
     if (a.rows == 0 || w == 0) return;
     if (a.heavy.nseg > 0 && !partial) throw QbError(kInternal, "csr_spmm: heavy rows need scratch");
+    const bool x_vec = (ldx % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(x) & 15) == 0) && (ldx >= w + (w & 1));
+    // 16-byte gathers measured faster for 32 < w <= 64 only (config 3: +10-16 %); wider blocks
+    // (config 5, w = 100) lose occupancy to the larger register footprint
+    if (x_vec && w > 32 && w <= 64) return spmm_launch2<1>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
     if (w <= 32) return spmm_launch<1>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
     if (w <= 64) return spmm_launch<2>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
     if (w <= 128) return spmm_launch<4>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
