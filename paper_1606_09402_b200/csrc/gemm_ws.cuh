@@ -163,6 +163,13 @@ template <int BM, int BN>
 __device__ __forceinline__ void ws_decode_item(const WsArgs& p, int it, int& mt, int& nt, int& kz) {
     kz = it / p.tiles;
     int t = it - kz * p.tiles;
+    if (p.flags & kGemmTriB) {
+        // triangular B: tile column nt needs (nt + 1) * BN of K; longest tiles first (LPT),
+        // m-fastest, so the static persistent schedule ends on the short ones
+        mt = t % p.tiles_m;
+        nt = p.tiles_n - 1 - t / p.tiles_m;
+        return;
+    }
     if (!(p.flags & kGemmUpperC)) {
         nt = t % p.tiles_n;
         mt = t / p.tiles_n;
