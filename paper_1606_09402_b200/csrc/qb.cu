@@ -715,7 +715,15 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
     }
     const std::int64_t bmax = std::min<std::int64_t>(p.b, std::max<std::int64_t>(cap, 1));
     const std::int64_t bpad = even(bmax);
-    DBuf om(static_cast<std::size_t>(n) * bpad, c.st);
+    // Omega_i of several blocks is drawn by ONE launch (the blocks consume consecutive
+    // n x b_i pieces of the column-major stream, so block j of a batch is columns
+    // [j b, j b + b_i) of an n x (nb b) draw); batches are capped at ~256 MB.
+    const std::int64_t nblk_total = ceil_div(std::max<std::int64_t>(cap, 1), bmax);
+    const std::int64_t nb_batch = std::max<std::int64_t>(
+        1, std::min<std::int64_t>(nblk_total, (std::int64_t{256} << 20) / (8 * std::max<std::int64_t>(n, 1) * bmax)));
+    const std::int64_t ldom = even(nb_batch * bmax);
+    DBuf om(static_cast<std::size_t>(n) * ldom, c.st);
+    std::int64_t batch_first = -1, batch_cols = 0;  // draw offset (in blocks) and width of the current batch
     DBuf y(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * bpad, c.st);
     DBuf tmp(static_cast<std::size_t>(std::max<std::int64_t>(std::max<std::int64_t>(m, n), 1)) * bpad, c.st);
     DBuf z(p.power > 0 ? static_cast<std::size_t>(n) * bpad : 0, c.st);
@@ -726,7 +734,15 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
         const std::int64_t bi = std::min(p.b, cap - s.k);
         ++blocks;
         const std::int64_t passes_before = a.passes;
-        MatView omv{om.p, n, bi, bi, true};
+        // blocks before the last are full width, so block j starts at draw g_used = j * n * bmax
+        const std::int64_t jblk = g_used / (n * bmax);
+        if (batch_first < 0 || jblk >= batch_first + nb_batch || g_used % (n * bmax) != 0) {
+            batch_first = jblk;
+            batch_cols = std::min(nb_batch * bmax, cap - s.k);
+            MatView all{om.p, n, batch_cols, ldom, true};
+            gaussian_fill(c.st, c.rng, p.seed, p.stream, static_cast<std::uint64_t>(g_used), all);  // step 4
+        }
+        MatView omv{om.p + (jblk - batch_first) * bmax, n, bi, ldom, true};
         MatView yv{y.p, m, bi, bi, true};
         MatView mv{mbuf.p, s.k, bi, bi, true};
         int d = 0, keep = 0;
@@ -736,8 +752,7 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
         for (int attempt = 0; attempt < 2; ++attempt) {
             a.passes = passes_before;
             eng.begin_block(/*optimistic=*/true, /*force_hh=*/attempt > 0);
-            gaussian_fill(c.st, c.rng, p.seed, p.stream, static_cast<std::uint64_t>(g_used), omv);  // step 4
-            // step 5: Y = A Omega_i - Q (B Omega_i)
+            // step 5: Y = A Omega_i - Q (B Omega_i)   (Omega_i drawn with its batch above)
             eng.apply(omv, yv); a.passes += 1;
             if (s.k > 0) {
                 eng.gemm(1.0, s.btk().t(), omv, 0.0, mv);
