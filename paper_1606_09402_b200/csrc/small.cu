@@ -648,7 +648,7 @@ struct PanelCfg {
     // independent accumulator chains per fragment along k (the FP64 MMA pipe needs ~40
     // MMAs in flight per SM to cover its latency)
     static constexpr int KSG = MAXG >= 5 ? 1 : (MAXG >= 3 ? 2 : 4);
-    static constexpr int KST = MAXT >= 5 ? 1 : 2;
+    static constexpr int KST = (MAXT >= 5 || BP >= 96) ? 1 : 2;  // wide panels: registers go to the Gram fragments
     // sub-tile copies in flight: as many as fit next to the triangular factor (~64 KB of rows)
     static constexpr int STAGES = (4 * SUB + BP) * LD * 8 <= 220 * 1024 ? 4 : 3;
     static constexpr int SMEM = (STAGES * SUB + BP) * LD * 8;
