@@ -23,6 +23,7 @@
 #include "qb.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <tuple>
@@ -110,6 +111,10 @@ Matrix::~Matrix() {
     if (ct_v) cudaFree(ct_v);
     free_heavy_plan(heavy);
     free_heavy_plan(heavy_t);
+    for (void* p : {static_cast<void*>(s_rp), static_cast<void*>(s_ci), static_cast<void*>(s_v),
+                    static_cast<void*>(d_rows), static_cast<void*>(d_cols), static_cast<void*>(d_r),
+                    static_cast<void*>(d_c)})
+        if (p) cudaFree(p);
 }
 
 std::unique_ptr<Matrix> make_dense(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
@@ -223,8 +228,86 @@ std::unique_ptr<Matrix> make_csr(Context& c, std::int64_t m_global, std::int64_t
     const int flags = csr_validate(c.st, m, n, nnz, mat->rp, mat->ci, mat->v, c.sms);
     if (flags & 1) throw QbError(kFormatError, "csr: invalid structure (row_ptr / column indices)");
     if (flags & 2) throw QbError(kError, "csr: non-finite value");
-    csr_transpose(c.st, m, n, nnz, mat->rp, mat->ci, mat->v, mat->ct_rp, mat->ct_ci, mat->ct_v, c.sms);
-    mat->heavy = make_heavy_plan(rp, m, c.st);
+    // Power-law matrices: rows with >= max(1024, n/16) entries and (outside those rows) columns
+    // with >= max(4096, m/16) entries are stored dense and multiplied on the FP64 tensor cores;
+    // a dense block costs 2w flops per stored element on DMMA, a CSR entry an 8w-byte L2/HBM
+    // gather, which DMMA beats above ~6 % density (config 5 measured best at 1/16 among 1/8,
+    // 1/16, 1/32; QBFAC_DENSE_DIVR / _DIVC override, QBFAC_CSR_DENSE=0 disables). Blocks are
+    // capped at 4 GB each.
+    const char* hyb_env = std::getenv("QBFAC_CSR_DENSE");
+    const bool hyb_ok = !(hyb_env && hyb_env[0] == '0') && m > 0 && n > 0 && nnz > 0;
+    std::vector<std::int32_t> rowmap, colmap;
+    std::vector<std::int64_t> drows, dcols;
+    std::int64_t extracted = 0;
+    if (hyb_ok) {
+        const int div_r = std::getenv("QBFAC_DENSE_DIVR") ? std::atoi(std::getenv("QBFAC_DENSE_DIVR")) : 16;
+        const int div_c = std::getenv("QBFAC_DENSE_DIVC") ? std::atoi(std::getenv("QBFAC_DENSE_DIVC")) : 16;
+        const std::int64_t row_thr = std::max<std::int64_t>(1024, n / div_r), col_thr = std::max<std::int64_t>(4096, m / div_c);
+        const std::int64_t cap_rows = (std::int64_t{4} << 30) / (8 * n), cap_cols = (std::int64_t{4} << 30) / (8 * m);
+        rowmap.assign(static_cast<std::size_t>(m), -1);
+        std::vector<std::pair<std::int64_t, std::int64_t>> rl;
+        for (std::int64_t i = 0; i < m; ++i)
+            if (rp[i + 1] - rp[i] >= row_thr) rl.push_back({rp[i + 1] - rp[i], i});
+        std::stable_sort(rl.begin(), rl.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+        if (static_cast<std::int64_t>(rl.size()) > cap_rows) rl.resize(static_cast<std::size_t>(cap_rows));
+        for (const auto& x : rl) drows.push_back(x.second);
+        std::sort(drows.begin(), drows.end());
+        for (std::size_t r = 0; r < drows.size(); ++r) {
+            rowmap[static_cast<std::size_t>(drows[r])] = static_cast<std::int32_t>(r);
+            extracted += rp[drows[r] + 1] - rp[drows[r]];
+        }
+        std::vector<std::int64_t> cc(static_cast<std::size_t>(n), 0);
+        for (std::int64_t i = 0; i < m; ++i)
+            if (rowmap[i] < 0)
+                for (std::int64_t e = rp[i]; e < rp[i + 1]; ++e) ++cc[ci[e]];
+        std::vector<std::pair<std::int64_t, std::int64_t>> cl;
+        for (std::int64_t j = 0; j < n; ++j)
+            if (cc[j] >= col_thr) cl.push_back({cc[j], j});
+        std::stable_sort(cl.begin(), cl.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+        if (static_cast<std::int64_t>(cl.size()) > cap_cols) cl.resize(static_cast<std::size_t>(cap_cols));
+        colmap.assign(static_cast<std::size_t>(n), -1);
+        for (const auto& x : cl) dcols.push_back(x.second);
+        std::sort(dcols.begin(), dcols.end());
+        for (std::size_t j = 0; j < dcols.size(); ++j) {
+            colmap[static_cast<std::size_t>(dcols[j])] = static_cast<std::int32_t>(j);
+            extracted += cc[dcols[j]];
+        }
+    }
+    if (hyb_ok && 20 * extracted >= nnz) {  // worth it when >= 5 % of the entries move to DMMA
+        mat->dr = static_cast<std::int64_t>(drows.size());
+        mat->dc = static_cast<std::int64_t>(dcols.size());
+        std::int32_t *d_rowmap = nullptr, *d_colmap = nullptr;
+        QB_CUDA(cudaMalloc(&d_rowmap, sizeof(std::int32_t) * m));
+        QB_CUDA(cudaMalloc(&d_colmap, sizeof(std::int32_t) * n));
+        QB_CUDA(cudaMemcpyAsync(d_rowmap, rowmap.data(), sizeof(std::int32_t) * m, cudaMemcpyHostToDevice, c.st));
+        QB_CUDA(cudaMemcpyAsync(d_colmap, colmap.data(), sizeof(std::int32_t) * n, cudaMemcpyHostToDevice, c.st));
+        if (mat->dr) {
+            QB_CUDA(cudaMalloc(&mat->d_rows, sizeof(std::int64_t) * mat->dr));
+            QB_CUDA(cudaMemcpyAsync(mat->d_rows, drows.data(), sizeof(std::int64_t) * mat->dr, cudaMemcpyHostToDevice, c.st));
+            QB_CUDA(cudaMalloc(&mat->d_r, sizeof(double) * mat->dr * n));
+            QB_CUDA(cudaMemsetAsync(mat->d_r, 0, sizeof(double) * mat->dr * n, c.st));
+        }
+        if (mat->dc) {
+            QB_CUDA(cudaMalloc(&mat->d_cols, sizeof(std::int64_t) * mat->dc));
+            QB_CUDA(cudaMemcpyAsync(mat->d_cols, dcols.data(), sizeof(std::int64_t) * mat->dc, cudaMemcpyHostToDevice, c.st));
+            QB_CUDA(cudaMalloc(&mat->d_c, sizeof(double) * mat->dc * m));
+            QB_CUDA(cudaMemsetAsync(mat->d_c, 0, sizeof(double) * mat->dc * m, c.st));
+        }
+        QB_CUDA(cudaMalloc(&mat->s_rp, sizeof(std::int64_t) * (m + 1)));
+        mat->s_nnz = csr_split_dense(c.st, m, n, mat->rp, mat->ci, mat->v, d_rowmap, d_colmap, mat->s_rp, &mat->s_ci,
+                                     &mat->s_v, mat->d_r, mat->d_c, c.sms);
+        QB_CUDA(cudaStreamSynchronize(c.st));
+        cudaFree(d_rowmap);
+        cudaFree(d_colmap);
+        csr_transpose(c.st, m, n, mat->s_nnz, mat->s_rp, mat->s_ci, mat->s_v, mat->ct_rp, mat->ct_ci, mat->ct_v, c.sms);
+        std::vector<std::int64_t> s_rp_host(static_cast<std::size_t>(m + 1));
+        QB_CUDA(cudaMemcpyAsync(s_rp_host.data(), mat->s_rp, sizeof(std::int64_t) * (m + 1), cudaMemcpyDeviceToHost, c.st));
+        QB_CUDA(cudaStreamSynchronize(c.st));
+        mat->heavy = make_heavy_plan(s_rp_host.data(), m, c.st);
+    } else {
+        csr_transpose(c.st, m, n, nnz, mat->rp, mat->ci, mat->v, mat->ct_rp, mat->ct_ci, mat->ct_v, c.sms);
+        mat->heavy = make_heavy_plan(rp, m, c.st);
+    }
     std::vector<std::int64_t> ct_rp_host(static_cast<std::size_t>(n + 1));
     QB_CUDA(cudaMemcpyAsync(ct_rp_host.data(), mat->ct_rp, sizeof(std::int64_t) * (n + 1), cudaMemcpyDeviceToHost, c.st));
     QB_CUDA(cudaStreamSynchronize(c.st));
@@ -254,6 +337,20 @@ public:
             const CsrView av = a_.csr();
             double* part = av.heavy.nseg ? c_.ws_sp.get(csr_spmm_scratch(av, std::min<int>(static_cast<int>(x.cols), 256))) : nullptr;
             csr_spmm(st_, av, x.p, x.ld, y.p, y.ld, static_cast<int>(x.cols), alpha, beta, c_.sms, part);
+            if (a_.hybrid()) {
+                const int w = static_cast<int>(x.cols);
+                if (a_.dr) {  // y[R] += alpha D_r X
+                    DBuf t(static_cast<std::size_t>(a_.dr) * w, st_);
+                    gemm(1.0, MatView{a_.d_r, a_.dr, a_.n, a_.n, true}, x, 0.0, MatView{t.p, a_.dr, w, w, true});
+                    scatter_add_rows(st_, t.p, a_.d_rows, a_.dr, w, alpha, y.p, y.ld);
+                }
+                if (a_.dc) {  // y += alpha D_c X[C]
+                    DBuf xc(static_cast<std::size_t>(a_.dc) * w, st_);
+                    gather_rows(st_, x.p, x.ld, a_.d_cols, a_.dc, w, xc.p);
+                    gemm(alpha, MatView{a_.d_c, a_.m, a_.dc, std::max<std::int64_t>(a_.m, 1), false},
+                         MatView{xc.p, a_.dc, w, w, true}, 1.0, y);
+                }
+            }
         } else if (!a_.pending.empty()) {
             // first pass over an asynchronously uploaded A: one GEMM per row chunk as it lands
             std::int64_t r0 = 0;
@@ -342,6 +439,20 @@ public:
             const CsrView av = a_.csr_t();
             double* part = av.heavy.nseg ? c_.ws_sp.get(csr_spmm_scratch(av, std::min<int>(static_cast<int>(x.cols), 256))) : nullptr;
             csr_spmm(st_, av, x.p, x.ld, y.p, y.ld, static_cast<int>(x.cols), 1.0, 0.0, c_.sms, part);
+            if (a_.hybrid()) {
+                const int w = static_cast<int>(x.cols);
+                if (a_.dr) {  // z += D_r^T X[R]
+                    DBuf xr(static_cast<std::size_t>(a_.dr) * w, st_);
+                    gather_rows(st_, x.p, x.ld, a_.d_rows, a_.dr, w, xr.p);
+                    gemm(1.0, MatView{a_.d_r, a_.dr, a_.n, a_.n, true}.t(), MatView{xr.p, a_.dr, w, w, true}, 1.0, y);
+                }
+                if (a_.dc) {  // z[C] += D_c^T X
+                    DBuf t(static_cast<std::size_t>(a_.dc) * w, st_);
+                    gemm(1.0, MatView{a_.d_c, a_.m, a_.dc, std::max<std::int64_t>(a_.m, 1), false}.t(), x, 0.0,
+                         MatView{t.p, a_.dc, w, w, true});
+                    scatter_add_rows(st_, t.p, a_.d_cols, a_.dc, w, 1.0, y.p, y.ld);
+                }
+            }
         } else {
             gemm(1.0, a_.dense_view().t(), x, 0.0, y);
         }

@@ -91,6 +91,18 @@ struct Matrix {
     std::int32_t* ct_ci = nullptr;
     double* ct_v = nullptr;
     HeavyPlan heavy, heavy_t;  // heavy-row segment plans of the CSR and its transpose
+    // Hybrid split of power-law matrices (make_csr): the SpMM runs on the remainder S
+    // (s_* arrays, transposed into ct_*), dense rows / dense columns go to DMMA GEMMs.
+    std::int64_t s_nnz = 0;
+    std::int64_t* s_rp = nullptr;
+    std::int32_t* s_ci = nullptr;
+    double* s_v = nullptr;
+    std::int64_t dr = 0, dc = 0;
+    std::int64_t* d_rows = nullptr;  // dr row indices (local)
+    std::int64_t* d_cols = nullptr;  // dc column indices
+    double* d_r = nullptr;           // dr x n, row-major
+    double* d_c = nullptr;           // m x dc, column-major (ld m)
+    bool hybrid() const { return d_r || d_c; }
     // Asynchronous dense upload (qbfac_gpu_matrix_dense_async): row chunks [row_end of the
     // previous, row_end) become resident when their event completes on ctx->st_copy. The
     // first A*X pass consumes them chunk by chunk; every other use waits for all of them.
@@ -109,8 +121,10 @@ struct Matrix {
 
     ~Matrix();
     MatView dense_view() const { return MatView{a, m, n, lda, false}; }
-    CsrView csr() const { return CsrView{m, n, nnz, rp, ci, v, heavy}; }
-    CsrView csr_t() const { return CsrView{n, m, nnz, ct_rp, ct_ci, ct_v, heavy_t}; }
+    CsrView csr() const {
+        return hybrid() ? CsrView{m, n, s_nnz, s_rp, s_ci, s_v, heavy} : CsrView{m, n, nnz, rp, ci, v, heavy};
+    }
+    CsrView csr_t() const { return CsrView{n, m, hybrid() ? s_nnz : nnz, ct_rp, ct_ci, ct_v, heavy_t}; }
 };
 
 std::unique_ptr<Matrix> make_dense(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,

@@ -507,6 +507,116 @@ int csr_validate(cudaStream_t st, std::int64_t m, std::int64_t n, std::int64_t n
     return flags;
 }
 
+namespace {
+// warp per row: kept entries of row i (rowmap[i] < 0 and colmap[col] < 0)
+__global__ void split_count_kernel(std::int64_t m, const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
+                                   const std::int32_t* __restrict__ rowmap, const std::int32_t* __restrict__ colmap,
+                                   int* __restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (std::int64_t i = warp; i < m; i += nwarps) {
+        int c = 0;
+        if (rowmap[i] < 0)
+            for (std::int64_t e = rp[i] + lane; e < rp[i + 1]; e += 32) c += colmap[ci[e]] < 0 ? 1 : 0;
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) cnt[i] = c;
+    }
+}
+
+// warp per row: order-preserving compaction into S, dense entries into D_r / D_c
+__global__ void split_fill_kernel(std::int64_t m, std::int64_t n, const std::int64_t* __restrict__ rp,
+                                  const std::int32_t* __restrict__ ci, const double* __restrict__ v,
+                                  const std::int32_t* __restrict__ rowmap, const std::int32_t* __restrict__ colmap,
+                                  const std::int64_t* __restrict__ s_rp, std::int32_t* __restrict__ s_ci,
+                                  double* __restrict__ s_v, double* __restrict__ d_r, double* __restrict__ d_c) {
+    const int lane = threadIdx.x & 31;
+    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (std::int64_t i = warp; i < m; i += nwarps) {
+        const int r = rowmap[i];
+        std::int64_t out = s_rp[i];
+        for (std::int64_t eb = rp[i]; eb < rp[i + 1]; eb += 32) {
+            const std::int64_t e = eb + lane;
+            const bool in = e < rp[i + 1];
+            const std::int32_t c = in ? ci[e] : 0;
+            const double x = in ? v[e] : 0.0;
+            const int j = in ? colmap[c] : -1;
+            if (r >= 0) {
+                if (in) d_r[static_cast<std::int64_t>(r) * n + c] = x;
+                continue;
+            }
+            if (in && j >= 0) d_c[i + static_cast<std::int64_t>(j) * m] = x;
+            const bool keep = in && j < 0;
+            const unsigned mask = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const std::int64_t pos = out + __popc(mask & ((1u << lane) - 1u));
+                s_ci[pos] = c;
+                s_v[pos] = x;
+            }
+            out += __popc(mask);
+        }
+    }
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ src, std::int64_t lds, const std::int64_t* __restrict__ idx,
+                                   std::int64_t k, int w, double* __restrict__ dst) {
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < k * w;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t r = e / w;
+        dst[e] = src[idx[r] * lds + (e - r * w)];
+    }
+}
+
+__global__ void scatter_add_rows_kernel(const double* __restrict__ src, const std::int64_t* __restrict__ idx, std::int64_t k,
+                                        int w, double alpha, double* __restrict__ dst, std::int64_t ldd) {
+    for (std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; e < k * w;
+         e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t r = e / w;
+        double* d = dst + idx[r] * ldd + (e - r * w);
+        *d = fma(alpha, src[e], *d);
+    }
+}
+}  // namespace
+
+std::int64_t csr_split_dense(cudaStream_t st, std::int64_t m, std::int64_t n, const std::int64_t* rp,
+                             const std::int32_t* ci, const double* v, const std::int32_t* rowmap,
+                             const std::int32_t* colmap, std::int64_t* s_rp, std::int32_t** s_ci, double** s_v,
+                             double* d_r, double* d_c, int sms) {
+    int* cnt = nullptr;
+    QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cnt), sizeof(int) * std::max<std::int64_t>(m, 1), st));
+    const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(m * 32, 256), 16L * sms)));
+    split_count_kernel<<<blocks, 256, 0, st>>>(m, rp, ci, rowmap, colmap, cnt);
+    QB_LAUNCH_CHECK();
+    scan_kernel<<<1, 1024, 0, st>>>(m, cnt, s_rp);
+    QB_LAUNCH_CHECK();
+    QB_CUDA(cudaFreeAsync(cnt, st));
+    std::int64_t snnz = 0;
+    QB_CUDA(cudaMemcpyAsync(&snnz, s_rp + m, sizeof(std::int64_t), cudaMemcpyDeviceToHost, st));
+    QB_CUDA(cudaStreamSynchronize(st));
+    QB_CUDA(cudaMalloc(s_ci, sizeof(std::int32_t) * std::max<std::int64_t>(snnz, 1)));
+    QB_CUDA(cudaMalloc(s_v, sizeof(double) * std::max<std::int64_t>(snnz, 1)));
+    split_fill_kernel<<<blocks, 256, 0, st>>>(m, n, rp, ci, v, rowmap, colmap, s_rp, *s_ci, *s_v, d_r, d_c);
+    QB_LAUNCH_CHECK();
+    return snnz;
+}
+
+void gather_rows(cudaStream_t st, const double* src, std::int64_t lds, const std::int64_t* idx, std::int64_t k, int w,
+                 double* dst) {
+    if (k * w == 0) return;
+    gather_rows_kernel<<<static_cast<int>(std::min<std::int64_t>(ceil_div(k * w, 256), 4096)), 256, 0, st>>>(
+        src, lds, idx, k, w, dst);
+    QB_LAUNCH_CHECK();
+}
+
+void scatter_add_rows(cudaStream_t st, const double* src, const std::int64_t* idx, std::int64_t k, int w, double alpha,
+                      double* dst, std::int64_t ldd) {
+    if (k * w == 0) return;
+    scatter_add_rows_kernel<<<static_cast<int>(std::min<std::int64_t>(ceil_div(k * w, 256), 4096)), 256, 0, st>>>(
+        src, idx, k, w, alpha, dst, ldd);
+    QB_LAUNCH_CHECK();
+}
+
 void csr_transpose(cudaStream_t st, std::int64_t m, std::int64_t n, std::int64_t nnz, const std::int64_t* rp,
                    const std::int32_t* ci, const double* v, std::int64_t* ct_rp, std::int32_t* ct_ci,
                    double* ct_v, int sms) {

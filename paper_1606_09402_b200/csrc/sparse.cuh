@@ -42,6 +42,22 @@ inline std::size_t csr_spmm_scratch(const CsrView& a, int w) { return static_cas
 int csr_validate(cudaStream_t st, std::int64_t m, std::int64_t n, std::int64_t nnz, const std::int64_t* rp,
                  const std::int32_t* ci, const double* v, int sms);
 
+// Hybrid split of a power-law CSR (A = S + P_R^T D_r + D_c P_C^T): rows flagged in rowflag
+// (entire rows) go to the dense row block D_r (dr x n, row-major), entries of the columns with
+// colmap[c] = j >= 0 (outside flagged rows) to the dense column block D_c (m x dc, column-major,
+// ld m); everything else stays in S (same order). d_r / d_c must be zeroed; s_rp has m+1 slots.
+// Returns nnz(S).
+std::int64_t csr_split_dense(cudaStream_t st, std::int64_t m, std::int64_t n, const std::int64_t* rp,
+                             const std::int32_t* ci, const double* v, const std::int32_t* rowmap,
+                             const std::int32_t* colmap, std::int64_t* s_rp, std::int32_t** s_ci, double** s_v,
+                             double* d_r, double* d_c, int sms);
+// dst(k x w, row-major ld w) = src rows idx[0..k) (row-major ld lds)
+void gather_rows(cudaStream_t st, const double* src, std::int64_t lds, const std::int64_t* idx, std::int64_t k, int w,
+                 double* dst);
+// dst rows idx[i] += alpha * src row i (rows distinct: no races)
+void scatter_add_rows(cudaStream_t st, const double* src, const std::int64_t* idx, std::int64_t k, int w, double alpha,
+                      double* dst, std::int64_t ldd);
+
 // Builds the CSR of A^T (n x m) with row-ascending entries per column.
 void csr_transpose(cudaStream_t st, std::int64_t m, std::int64_t n, std::int64_t nnz, const std::int64_t* rp,
                    const std::int32_t* ci, const double* v, std::int64_t* ct_rp, std::int32_t* ct_ci,
