@@ -849,6 +849,42 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
     static_assert(CholCfg<BP>::SMEM <= C::SMEM, "chol workspace");
     if (cta == 0) chol_tile_block<BP>(p.g, kSmallMax, p.b, p.ra, p.rainv, kSmallMax, p.st0, psm);
     grid_barrier(p.gbar, G);
+    // A near-orthonormal panel (Gram within 1e-8 of I: every re-orthogonalisation) needs one
+    // pass: Q = Y Ra^{-1} is orthonormal to O(u) already, so phase B writes Q and the second
+    // Gram / Cholesky / product are skipped (Rb = I, its status reports a clean identity).
+    const bool one_pass = __ldcg(&p.st0->gram_dev) <= kFirstOrderDev && __ldcg(&p.st0->breakdown) == 0;
+    if (one_pass) {
+        stage_r(p.rainv);
+        sub_loop(p.y, p.ldy, [&](double* cur, std::int64_t r0) {
+            if (mma_warp) {
+                double tacc[C::MAXT][4];
+                panel_trmm<BP>(cur, rs, tacc, p.b);
+                const int mi = warp % C::MI, h = warp / C::MI;
+#pragma unroll
+                for (int j = 0; j < C::MAXT; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int row = 16 * mi + g + (e >= 2 ? 8 : 0), col = 8 * (h + C::NG * j) + 2 * t + (e & 1);
+                        if (r0 + row < p.rows && col < p.b) p.q[(r0 + row) * p.ldq + col] = tacc[j][e];
+                    }
+            }
+        });
+        if (cta == 0) {
+            for (int idx = tid; idx < p.b * p.b; idx += blockDim.x) {
+                const int i = idx % p.b, j = idx / p.b;
+                p.rb[i + j * kSmallMax] = i == j ? 1.0 : 0.0;
+                p.rbinv[i + j * kSmallMax] = i == j ? 1.0 : 0.0;
+            }
+            if (tid == 0) {
+                p.st1->breakdown = 0;
+                p.st1->bad_index = -1;
+                p.st1->diag_min = 1.0;
+                p.st1->diag_max = 1.0;
+                p.st1->gram_dev = 0.0;
+            }
+        }
+        return;
+    }
     // ---- phase B: T1 = Y Ra^{-1} (written out) and the Gram of T1
     stage_r(p.rainv);
     zero_acc();
