@@ -297,6 +297,28 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
             for (int j = 0; j < T::NI; ++j)
 #pragma unroll
                 for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+        // beta != 0 (skinny updates Y -= Q M): the C fragment is loaded before the main loop
+        // so its latency hides behind the MMAs instead of stalling the epilogue
+        constexpr bool kPrefetchC = T::MI * T::NI * 4 <= 32;
+        double cpre[kPrefetchC ? T::MI : 1][kPrefetchC ? T::NI : 1][4];
+        const bool use_pre = kPrefetchC && p.beta != 0.0 && !p.partial;
+        if constexpr (kPrefetchC) {
+            if (use_pre) {
+#pragma unroll
+                for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                    for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int row = m0 + wm * T::WTM + i * 16 + g + (r >= 2 ? 8 : 0);
+                            const int col = n0 + wn * T::WTN + j * 8 + 2 * t + (r & 1);
+                            cpre[i][j][r] = (row < p.M && col < p.N)
+                                                ? __ldcg(p.c_row ? p.C + static_cast<std::int64_t>(row) * p.ldc + col
+                                                                 : p.C + row + static_cast<std::int64_t>(col) * p.ldc)
+                                                : 0.0;
+                        }
+            }
+        }
         for (int kt = 0; kt < ntiles; ++kt) {
             mbar_wait(&full[stage], phase);
             const double* a_s = sA + stage * T::A_STAGE;
@@ -348,7 +370,10 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
                             double* cp = p.c_row ? p.C + static_cast<std::int64_t>(row) * p.ldc + col
                                                  : p.C + row + static_cast<std::int64_t>(col) * p.ldc;
                             const double v = p.alpha * acc[i][j][r];
-                            *cp = p.beta == 0.0 ? v : v + p.beta * (*cp);
+                            double old_c = 0.0;
+                            if constexpr (kPrefetchC) old_c = use_pre ? cpre[i][j][r] : (p.beta == 0.0 ? 0.0 : *cp);
+                            else old_c = p.beta == 0.0 ? 0.0 : *cp;
+                            *cp = p.beta == 0.0 ? v : v + p.beta * old_c;
                         }
                     }
                 }
