@@ -228,7 +228,7 @@ def main():
     # caller-allocated pinned output buffers (the C-ABI's two-phase copy-out)
     q_out = torch.empty(n * CFG["max_rank"], dtype=torch.float64, pin_memory=True).numpy()
     b_out = torch.empty(n * CFG["max_rank"], dtype=torch.float64, pin_memory=True).numpy()
-    e2e_times, h2d, d2h = [], 0, 0
+    e2e_times, h2d, d2h, phases = [], 0, 0, []
     for s in range(max(2, min(args.steps, 5))):
         ctx.synchronize()
         barrier()
@@ -236,16 +236,35 @@ def main():
         # H2D of A (8*n*n bytes) in row chunks on the copy stream; the first pass G = A*Omega
         # consumes each chunk as it lands (qbfac_gpu_matrix_dense_async)
         h = qbfac.MatrixHandle.dense_async(a_view, ctx)
+        t1 = time.perf_counter()
         r = factorize_h(qbfac, h, eps)
+        t2 = time.perf_counter()
         q = r.q(q_out)                                      # D2H of Q
         b = r.b(b_out)                                      # D2H of B
+        t3 = time.perf_counter()
         r.free()
         h.free()
         ctx.synchronize()
         e2e_times.append(time.perf_counter() - t0)
+        phases.append((t1 - t0, t2 - t1, t3 - t2, e2e_times[-1] - (t3 - t0)))
         h2d = 8 * n * n
         d2h = 8 * (q.size + b.size)
     t_e2e = max_over_ranks(float(np.median(e2e_times)))
+    ph = np.median(np.array(phases), axis=0) * 1e3
+    # the link this e2e rides on: a plain pinned H2D of A, same bytes
+    dev_a = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    h2d_s = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dev_a.copy_(host_a, non_blocking=True)
+        torch.cuda.synchronize()
+        h2d_s.append(time.perf_counter() - t0)
+    del dev_a
+    e2e_extra = {"phases_ms": {"handle": round(float(ph[0]), 3), "run": round(float(ph[1]), 3),
+                               "d2h_q_b": round(float(ph[2]), 3), "free_sync": round(float(ph[3]), 3)},
+                 "h2d_link_gbs": round(8 * n * n / min(h2d_s) / 1e9, 2),
+                 "all_s": [round(t, 5) for t in e2e_times]}
 
     # ---- roofline: the dominant kernel (DMMA pass G = A * Omega at width l~) ----
     w = CFG["l_budget"]
@@ -312,7 +331,7 @@ def main():
                        "blocks": info["blocks"], "householder_fallbacks": info["householder_fallbacks"],
                        "l2": "inputs larger than L2 (A = 512 MB)", "parallelism": f"replicas x{world}"},
             "clocks": clk,
-            "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, **e2e_extra},
             "gpu_launches": int(launches * args.steps),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
