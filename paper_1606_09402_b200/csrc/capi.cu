@@ -512,6 +512,13 @@ int qbfac_gpu_test_cholqr2(qbfac_gpu_ctx* ctx, const double* y, int64_t rows, in
     });
 }
 
+int qbfac_gpu_test_panel_trace(qbfac_gpu_ctx* ctx, unsigned long long* out) {
+    return guard(ctx, [&] {
+        QB_CUDA(cudaStreamSynchronize(ctx->c->st));
+        qbgpu::panel_trace(out);
+    });
+}
+
 int qbfac_gpu_test_householder(qbfac_gpu_ctx* ctx, double* y, int64_t m, int b, int64_t ld, double* r) {
     return guard(ctx, [&] {
         auto& cx = *ctx->c;

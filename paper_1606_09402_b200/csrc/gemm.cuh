@@ -69,6 +69,7 @@ struct SmallStatus {
 
 // b x b Gram G (col-major, ld) -> R = chol(G) upper (col-major ldr), Rinv = R^{-1}
 // (upper, col-major). One CTA. b <= kSmallMax.
+constexpr int kPanelTraceSlots = 12;
 constexpr int kSmallMax = 112;  // chol_small keeps [G | I] (b x 2b) in shared memory
 void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, double* r,
                 double* rinv, std::int64_t ldr, SmallStatus* status);
@@ -86,6 +87,7 @@ int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, 
 // q <- t1 rb^{-1}; statuses of both Choleskies in st0 / st1. q may alias y. Small
 // matrices are column-major with ld kSmallMax. gbar: two zero-initialised words per
 // context (grid barrier).
+void panel_trace(unsigned long long* out);  // phase timestamps of the last panel launch
 void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t rows, int b, std::int64_t ldy,
                    double* t1, double* q, std::int64_t ldq, double* g, double* ra, double* rainv, double* rb,
                    double* rbinv, SmallStatus* st0, SmallStatus* st1, unsigned* gbar);

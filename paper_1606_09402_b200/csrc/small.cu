@@ -223,10 +223,18 @@ __device__ __forceinline__ void ct_frag(const double* a, int am, int ak, const d
     }
 }
 
+// clock64 stamps of the last in-CTA Cholesky run by CTA 0 (thread 0), for the per-step
+// breakdown (qbfac_gpu_test_chol_trace): 0 start, 1 loaded, 2+3p / 3+3p / 4+3p panel p
+// eliminated / row panel / trailing update, 16 R written, 17+jb inverse block column jb, 31 end.
+__device__ long long g_chol_trace[32];
+__device__ __forceinline__ void chol_mark(int slot, bool on = true) {
+    if (on && blockIdx.x == 0 && threadIdx.x == 0) g_chol_trace[slot] = clock64();
+}
+
 template <int BP>
-__device__ __noinline__ void chol_tile_block(const double* __restrict__ gsrc, std::int64_t ldg, int b,
+__device__ __forceinline__ void chol_tile_block(const double* __restrict__ gsrc, std::int64_t ldg, int b,
                                              double* __restrict__ r, double* __restrict__ rinv, std::int64_t ldr,
-                                             SmallStatus* status, double* sm) {
+                                             SmallStatus* status, double* sm, bool trace = true) {
     using C = CholCfg<BP>;
     double* W = sm;                       // BP x LD, row-major; upper = G, then R, then R^{-1}
     double* Tm = W + BP * C::LD;          // BP x TLD scratch
@@ -238,6 +246,7 @@ __device__ __noinline__ void chol_tile_block(const double* __restrict__ gsrc, st
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nthr = blockDim.x;
     double dev = 0.0;
+    chol_mark(0, trace);
     // column-major source: consecutive threads take consecutive rows i of one column j;
     // 8 loads in flight per thread per round
     for (int base = 0; base < BP * BP; base += 8 * nthr) {
@@ -269,6 +278,7 @@ __device__ __noinline__ void chol_tile_block(const double* __restrict__ gsrc, st
         s_dev = isfinite(dv) ? dv : INFINITY;
     }
     __syncthreads();
+    chol_mark(1, trace);
     if (s_dev <= kFirstOrderDev) {
         for (int idx = tid; idx < b * b; idx += nthr) {
             const int i = idx % b, j = idx / b;
@@ -329,6 +339,7 @@ __device__ __noinline__ void chol_tile_block(const double* __restrict__ gsrc, st
                 }
             }
             __syncthreads();
+            chol_mark(2 + 3 * pnl, trace);
             if (c1 < BP) {
                 // 2. row panel (in place): W[c0+m][c1+n] = sum_k Rinv_pp(k, m) W[c0+k][c1+n]
                 const int nf = (BP - c1) / 8;
@@ -337,6 +348,7 @@ __device__ __noinline__ void chol_tile_block(const double* __restrict__ gsrc, st
                         ct_frag(Dv, 1, C::TLD, W + c0 * C::LD + c1, C::LD, 1, W + c0 * C::LD + c1, C::LD, 0, ni, 0, 16,
                                 1.0, false);
                 __syncthreads();
+                chol_mark(3 + 3 * pnl, trace);
                 // 3. trailing update on upper fragments: W[c1+m][c1+n] -= sum_k W[c0+k][c1+m] W[c0+k][c1+n]
                 const int nb8 = (BP - c1) / 8;
                 int nfu = 0;
@@ -350,6 +362,7 @@ __device__ __noinline__ void chol_tile_block(const double* __restrict__ gsrc, st
                                 mi, ni, 0, 16, -1.0, true);
                     }
                 __syncthreads();
+                chol_mark(4 + 3 * pnl, trace);
             }
         }
         // R out
@@ -358,6 +371,7 @@ __device__ __noinline__ void chol_tile_block(const double* __restrict__ gsrc, st
             r[i + static_cast<std::int64_t>(j) * ldr] = i <= j ? W[i * C::LD + j] : 0.0;
         }
         __syncthreads();
+        chol_mark(23, trace);
         // in-place inversion, block column by block column
         for (int jb = 0; jb < C::P; ++jb) {
             const int cj = 16 * jb;
@@ -381,6 +395,7 @@ __device__ __noinline__ void chol_tile_block(const double* __restrict__ gsrc, st
                 W[(cj + i) * C::LD + cj + k] = Dj[i * C::TLD + k];
             }
             __syncthreads();
+            chol_mark(24 + jb, trace);
         }
         for (int idx = tid; idx < b * b; idx += nthr) {
             const int i = idx % b, j = idx / b;
@@ -407,6 +422,7 @@ __device__ __noinline__ void chol_tile_block(const double* __restrict__ gsrc, st
         }
     }
     __syncthreads();
+    chol_mark(31, trace);
 }
 
 template <int BP>
@@ -750,6 +766,17 @@ __device__ __forceinline__ void panel_trmm(const double* ys, const double* rs, d
         }
 }
 
+// Phase timestamps of the last panel launch (CTA 0, %globaltimer ns): read by
+// qbfac_gpu_test_panel_trace for the per-phase breakdown in profiles/.
+__device__ unsigned long long g_panel_trace[kPanelTraceSlots];
+__device__ __forceinline__ void panel_mark(int slot) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_panel_trace[slot] = t;
+    }
+}
+
 template <int BP>
 __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArgs p) {
     using C = PanelCfg<BP>;
@@ -838,17 +865,23 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
         cp_async_wait<0>();
     };
     // ---- phase A: Gram of Y
+    panel_mark(0);
     zero_acc();
     sub_loop(p.y, p.ldy, [&](double* cur, std::int64_t) {
         if (mma_warp) panel_gram<BP>(cur, acc, fm, fn);
     });
+    panel_mark(1);
     if (mma_warp) write_part();
     grid_barrier(p.gbar, G);
+    panel_mark(2);
     reduce_parts();
     grid_barrier(p.gbar, G);
+    panel_mark(3);
     static_assert(CholCfg<BP>::SMEM <= C::SMEM, "chol workspace");
     if (cta == 0) chol_tile_block<BP>(p.g, kSmallMax, p.b, p.ra, p.rainv, kSmallMax, p.st0, psm);
+    panel_mark(4);
     grid_barrier(p.gbar, G);
+    panel_mark(5);
     // A near-orthonormal panel (Gram within 1e-8 of I: every re-orthogonalisation) needs one
     // pass: Q = Y Ra^{-1} is orthonormal to O(u) already, so phase B writes Q and the second
     // Gram / Cholesky / product are skipped (Rb = I, its status reports a clean identity).
@@ -883,6 +916,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
                 p.st1->gram_dev = 0.0;
             }
         }
+        panel_mark(11);
         return;
     }
     // ---- phase B: T1 = Y Ra^{-1} (written out) and the Gram of T1
@@ -907,12 +941,16 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
         __syncthreads();
         if (mma_warp) panel_gram<BP>(cur, acc, fm, fn);
     });
+    panel_mark(6);
     if (mma_warp) write_part();
     grid_barrier(p.gbar, G);
     reduce_parts();
     grid_barrier(p.gbar, G);
-    if (cta == 0) chol_tile_block<BP>(p.g, kSmallMax, p.b, p.rb, p.rbinv, kSmallMax, p.st1, psm);
+    panel_mark(7);
+    if (cta == 0) chol_tile_block<BP>(p.g, kSmallMax, p.b, p.rb, p.rbinv, kSmallMax, p.st1, psm, false);
+    panel_mark(8);
     grid_barrier(p.gbar, G);
+    panel_mark(9);
     // ---- phase D: Q = T1 Rb^{-1}
     stage_r(p.rbinv);
     sub_loop(p.t1, p.b, [&](double* cur, std::int64_t r0) {
@@ -929,6 +967,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
                 }
         }
     });
+    panel_mark(10);
 }
 
 // ---- one-sided Jacobi SVD of a small square matrix (qb_to_svd) ---------
@@ -1362,6 +1401,11 @@ void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t
         case 96: launch_cholqr2_panel<96>(st, a, cap); break;
         default: launch_cholqr2_panel<112>(st, a, cap); break;
     }
+}
+
+void panel_trace(unsigned long long* out) {
+    QB_CUDA(cudaMemcpyFromSymbol(out, g_panel_trace, sizeof(unsigned long long) * kPanelTraceSlots));
+    QB_CUDA(cudaMemcpyFromSymbol(out + kPanelTraceSlots, g_chol_trace, sizeof(long long) * 32));
 }
 
 int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, int max_sweeps) {
