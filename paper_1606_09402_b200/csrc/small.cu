@@ -670,42 +670,46 @@ struct PanelCfg {
     static constexpr int SMEM = (STAGES * SUB + BP) * LD * 8;
 };
 
-// Asynchronous copy of one sub-tile into ys (zero-filled outside rows x b): 16-byte
-// cp.async chunks when every row start is 16-byte aligned and b is even, 8-byte ones
-// otherwise. Commits one group.
-template <int BP>
-__device__ __forceinline__ void panel_stage_async(double* ys, const double* __restrict__ src, std::int64_t ld,
-                                                  std::int64_t r0, std::int64_t rows, int b, bool vec2) {
-    using C = PanelCfg<BP>;
-    if (vec2) {
-        for (int idx = threadIdx.x; idx < C::SUB * BP / 2; idx += blockDim.x) {
-            const int r = idx / (BP / 2), c = 2 * (idx - r * (BP / 2));
-            const std::int64_t gr = r0 + r;
-            const bool ok = gr < rows && c < b;
-            const double* s = ok ? src + gr * ld + c : src;
-            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(ys + r * C::LD + c));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(s), "r"(ok ? 16 : 0) : "memory");
-        }
-    } else {
-        for (int idx = threadIdx.x; idx < C::SUB * BP; idx += blockDim.x) {
-            const int r = idx / BP, c = idx - r * BP;
-            const std::int64_t gr = r0 + r;
-            const bool ok = gr < rows && c < b;
-            const double* s = ok ? src + gr * ld + c : src;
-            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(ys + r * C::LD + c));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(s), "r"(ok ? 8 : 0) : "memory");
-        }
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
+// Panel sub-tile ring: the producer warp moves each sub-tile row (b contiguous doubles) with a
+// TMA bulk copy (cp.async.bulk ... mbarrier::complete_tx, SASS UBLKCP) into the padded
+// shared layout; full/empty mbarrier pairs replace the CTA-wide barriers of a cp.async ring.
+__device__ __forceinline__ unsigned sm_addr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void pb_init(std::uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(count));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void pb_arrive(std::uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sm_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void pb_arrive_tx(std::uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void pb_wait(std::uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "PB_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra PB_WAIT_%=;\n"
+        "}\n" ::"r"(sm_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void pb_bulk(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(sm_addr(dst)),
+        "l"(src), "r"(bytes), "r"(sm_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void pb_fence_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// named barrier over the 8 DMMA (consumer) warps only
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 
-// acc += Ys^T Ys on this warp's upper fragments (KSG interleaved chains along the rows)
-template <int BP>
-__device__ __forceinline__ void panel_gram(const double* ys, double (&acc)[PanelCfg<BP>::MAXG][PanelCfg<BP>::KSG][4],
-                                           const int (&fm)[PanelCfg<BP>::MAXG], const int (&fn)[PanelCfg<BP>::MAXG]) {
+// acc += Ys^T Ys on this warp's first NV upper fragments (KSG interleaved chains along the
+// rows). NV is the warp's count of valid fragments, dispatched at compile time: a predicated-off
+// DMMA still occupies the FP64 tensor pipe, so invalid fragments must not be issued at all.
+template <int BP, int NV>
+__device__ __forceinline__ void panel_gram_n(const double* ys, double (&acc)[PanelCfg<BP>::MAXG][PanelCfg<BP>::KSG][4],
+                                             const int (&fm)[PanelCfg<BP>::MAXG], const int (&fn)[PanelCfg<BP>::MAXG]) {
     using C = PanelCfg<BP>;
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll 2
@@ -714,16 +718,24 @@ __device__ __forceinline__ void panel_gram(const double* ys, double (&acc)[Panel
         for (int c = 0; c < C::KSG; ++c) {
             const double* row = ys + (kk + 4 * c + t) * C::LD;  // A = Ys^T: a(m, k) = Ys(k, m)
 #pragma unroll
-            for (int f = 0; f < C::MAXG; ++f) {
-                if (fm[f] < 0) continue;
+            for (int f = 0; f < NV; ++f)
                 dmma_16x8x4(acc[f][c], row[16 * fm[f] + g], row[16 * fm[f] + g + 8], row[8 * fn[f] + g]);
-            }
         }
     }
 }
+template <int BP, int NV = PanelCfg<BP>::MAXG>
+__device__ __forceinline__ void panel_gram(const double* ys, double (&acc)[PanelCfg<BP>::MAXG][PanelCfg<BP>::KSG][4],
+                                           const int (&fm)[PanelCfg<BP>::MAXG], const int (&fn)[PanelCfg<BP>::MAXG],
+                                           int nvf) {
+    if constexpr (NV > 0) {
+        if (nvf == NV) panel_gram_n<BP, NV>(ys, acc, fm, fn);
+        else panel_gram<BP, NV - 1>(ys, acc, fm, fn, nvf);
+    }
+}
 
-// out fragments = Ys (SUB x BP) * Rs (BP x BP, upper), mi = warp % MI, ni = warp / MI + NG j
-// (KST interleaved chains along k, summed at the end)
+// out fragments = Ys (SUB x BP) * Rs (BP x BP, upper), mi = warp % MI, ni = warp / MI + NG j.
+// Fragment by fragment with the exact triangular k range (k < 8 ni + 8): no predicated-off
+// DMMAs; two interleaved chains along k, summed at the end.
 template <int BP>
 __device__ __forceinline__ void panel_trmm(const double* ys, const double* rs, double (&out)[PanelCfg<BP>::MAXT][4],
                                            int b) {
@@ -731,39 +743,27 @@ __device__ __forceinline__ void panel_trmm(const double* ys, const double* rs, d
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int mi = warp % C::MI, h = warp / C::MI;
     const int nb8 = (b + 7) >> 3, kmax = (b + 3) & ~3;
-    double acc[C::MAXT][C::KST][4];
+    const double* a0p = ys + (16 * mi + g) * C::LD + t;
+    const double* a1p = a0p + 8 * C::LD;
 #pragma unroll
-    for (int j = 0; j < C::MAXT; ++j)
+    for (int j = 0; j < C::MAXT; ++j) {
+        const int ni = h + C::NG * j;
 #pragma unroll
-        for (int c = 0; c < C::KST; ++c)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[j][c][e] = 0.0;
-#pragma unroll 2
-    for (int k0 = 0; k0 < kmax; k0 += 4 * C::KST) {
-#pragma unroll
-        for (int c = 0; c < C::KST; ++c) {
-            const int kk = k0 + 4 * c;
-            if (kk >= kmax) continue;
-            const double a0 = ys[(16 * mi + g) * C::LD + kk + t];
-            const double a1 = ys[(16 * mi + g + 8) * C::LD + kk + t];
-#pragma unroll
-            for (int j = 0; j < C::MAXT; ++j) {
-                const int ni = h + C::NG * j;
-                // R^{-1} upper: column block ni needs k < 8 ni + 8; blocks past b are zero
-                if (ni >= nb8 || kk >= 8 * ni + 8) continue;
-                dmma_16x8x4(acc[j][c], a0, a1, rs[(kk + t) * C::LD + 8 * ni + g]);
-            }
+        for (int e = 0; e < 4; ++e) out[j][e] = 0.0;
+        if (ni >= nb8) continue;  // warp-uniform
+        // 8 ni + 8 is a multiple of 8: two chains of k4 steps, at most one odd step at kmax
+        const int kend = min(kmax, 8 * ni + 8);
+        const double* bp = rs + t * C::LD + 8 * ni + g;
+        double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
+        int kk = 0;
+        for (; kk + 8 <= kend; kk += 8) {
+            dmma_16x8x4(acc0, a0p[kk], a1p[kk], bp[kk * C::LD]);
+            dmma_16x8x4(acc1, a0p[kk + 4], a1p[kk + 4], bp[(kk + 4) * C::LD]);
         }
+        if (kk < kend) dmma_16x8x4(acc0, a0p[kk], a1p[kk], bp[kk * C::LD]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) out[j][e] = acc0[e] + acc1[e];
     }
-#pragma unroll
-    for (int j = 0; j < C::MAXT; ++j)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            double v = acc[j][0][e];
-#pragma unroll
-            for (int c = 1; c < C::KST; ++c) v += acc[j][c][e];
-            out[j][e] = v;
-        }
 }
 
 // Phase timestamps of the last panel launch (CTA 0, %globaltimer ns): read by
@@ -783,9 +783,26 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
     extern __shared__ __align__(16) double psm[];
     double* ys2 = psm;                              // STAGES sub-tile buffers (SUB x LD)
     double* rs = psm + C::STAGES * C::SUB * C::LD;  // BP x LD triangular factor
+    __shared__ __align__(8) std::uint64_t full[C::STAGES], empty[C::STAGES];
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const bool mma_warp = warp < 8;
+    if (tid == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            pb_init(&full[s], 1);
+            pb_init(&empty[s], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    // The bulk copies fill columns [0, b) only. Columns [b, kmax) enter the triangular products
+    // (times zero rows of R^{-1}) and must hold zeros; columns past kmax only reach discarded
+    // Gram entries.
+    const int kpad = ((p.b + 3) & ~3) - p.b;
+    auto zero_pad = [&]() {
+        for (int idx = tid; idx < C::STAGES * C::SUB * kpad; idx += blockDim.x)
+            ys2[(idx / kpad) * C::LD + p.b + idx % kpad] = 0.0;
+    };
+    zero_pad();
     // this warp's upper Gram fragments
     int fm[C::MAXG], fn[C::MAXG];
 #pragma unroll
@@ -802,6 +819,9 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
         fm[f] = mi;
         fn[f] = 2 * mi + e;
     }
+    int nvf = 0;  // valid fragments form a prefix
+#pragma unroll
+    for (int f = 0; f < C::MAXG; ++f) nvf += fm[f] >= 0 ? 1 : 0;
     double acc[C::MAXG][C::KSG][4];
     auto zero_acc = [&]() {
 #pragma unroll
@@ -842,33 +862,59 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
             rs[k * C::LD + n] = (k < p.b && n < p.b && k <= n) ? __ldcg(rinv + k + n * kSmallMax) : 0.0;
         }
     };
-    // sub-tile loop with STAGES-1 sub-tile copies in flight (one cp.async group per
-    // sub-tile, empty groups past the end keep the group count uniform)
+    // sub-tile loop: warp 8 produces (TMA bulk row copies, or generic copies when rows are not
+    // 16-byte aligned), warps 0-7 consume; the ring position persists across the phases.
+    int ring_stage = 0;
+    unsigned ring_phase = 0;
     auto sub_loop = [&](const double* src, std::int64_t ld, auto&& body) {
-        const bool vec2 = (ld % 2 == 0) && (p.b % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(src) & 15) == 0);
-        auto buf = [&](int i) { return ys2 + (i % C::STAGES) * C::SUB * C::LD; };
-        auto issue = [&](int i) {
-            const int sub = cta + i * G;
-            if (sub < p.nsub) panel_stage_async<BP>(buf(i), src, ld, static_cast<std::int64_t>(sub) * C::SUB, p.rows, p.b, vec2);
-            else cp_async_commit();
-        };
-#pragma unroll
-        for (int i = 0; i < C::STAGES - 1; ++i) issue(i);
-        int i = 0;
-        for (int sub = cta; sub < p.nsub; sub += G, ++i) {
-            issue(i + C::STAGES - 1);
-            cp_async_wait<C::STAGES - 1>();
-            __syncthreads();
-            body(buf(i), static_cast<std::int64_t>(sub) * C::SUB);
-            __syncthreads();
+        const bool bulk = (ld % 2 == 0) && (p.b % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(src) & 15) == 0);
+        if (cta == 0) zero_pad();  // the Cholesky used the ring as its workspace
+        pb_fence_async();  // generic shared writes of the previous phase before async-proxy copies
+        __syncthreads();
+        if (!mma_warp) {
+            for (int sub = cta; sub < p.nsub; sub += G) {
+                pb_wait(&empty[ring_stage], ring_phase ^ 1);
+                double* buf = ys2 + ring_stage * C::SUB * C::LD;
+                const std::int64_t r0 = static_cast<std::int64_t>(sub) * C::SUB;
+                const int nr = static_cast<int>(min(static_cast<std::int64_t>(C::SUB), p.rows - r0));
+                if (bulk) {
+                    if (nr < C::SUB) {  // rows past the end: zero (stale data of an earlier sub-tile)
+                        for (int idx = lane; idx < (C::SUB - nr) * BP; idx += 32)
+                            buf[(nr + idx / BP) * C::LD + idx % BP] = 0.0;
+                        pb_fence_async();
+                    }
+                    __syncwarp();
+                    if (lane == 0) pb_arrive_tx(&full[ring_stage], static_cast<unsigned>(nr * p.b * 8));
+                    __syncwarp();
+                    for (int r = lane; r < nr; r += 32)
+                        pb_bulk(buf + r * C::LD, src + (r0 + r) * ld, static_cast<unsigned>(p.b * 8), &full[ring_stage]);
+                } else {
+                    for (int idx = lane; idx < C::SUB * BP; idx += 32) {
+                        const int r = idx / BP, c = idx - r * BP;
+                        buf[r * C::LD + c] = (r < nr && c < p.b) ? src[(r0 + r) * ld + c] : 0.0;
+                    }
+                    __syncwarp();
+                    if (lane == 0) pb_arrive(&full[ring_stage]);
+                }
+                if (++ring_stage == C::STAGES) { ring_stage = 0; ring_phase ^= 1; }
+            }
+        } else {
+            for (int sub = cta; sub < p.nsub; sub += G) {
+                pb_wait(&full[ring_stage], ring_phase);
+                body(ys2 + ring_stage * C::SUB * C::LD, static_cast<std::int64_t>(sub) * C::SUB);
+                pb_fence_async();  // phase B writes T into the buffer before the next bulk copy lands there
+                __syncwarp();
+                if (lane == 0) pb_arrive(&empty[ring_stage]);
+                if (++ring_stage == C::STAGES) { ring_stage = 0; ring_phase ^= 1; }
+            }
         }
-        cp_async_wait<0>();
+        __syncthreads();
     };
     // ---- phase A: Gram of Y
     panel_mark(0);
     zero_acc();
     sub_loop(p.y, p.ldy, [&](double* cur, std::int64_t) {
-        if (mma_warp) panel_gram<BP>(cur, acc, fm, fn);
+        if (mma_warp) panel_gram<BP>(cur, acc, fm, fn, nvf);
     });
     panel_mark(1);
     if (mma_warp) write_part();
@@ -925,7 +971,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
     sub_loop(p.y, p.ldy, [&](double* cur, std::int64_t r0) {
         double tacc[C::MAXT][4];
         if (mma_warp) panel_trmm<BP>(cur, rs, tacc, p.b);
-        __syncthreads();
+        consumer_sync();
         if (mma_warp) {
             const int mi = warp % C::MI, h = warp / C::MI;
 #pragma unroll
@@ -938,8 +984,8 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
                     if (r0 + row < p.rows && col < p.b) p.t1[(r0 + row) * p.b + col] = tacc[j][e];
                 }
         }
-        __syncthreads();
-        if (mma_warp) panel_gram<BP>(cur, acc, fm, fn);
+        consumer_sync();
+        if (mma_warp) panel_gram<BP>(cur, acc, fm, fn, nvf);
     });
     panel_mark(6);
     if (mma_warp) write_part();

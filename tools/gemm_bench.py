@@ -35,6 +35,10 @@ def main():
         ("Bt*M 5e4x500x50", 50000, 50, 500, 1, 1, 1),
         ("Y*Rinv 1e5x50x50", 100000, 50, 50, 1, 0, 1),
         ("gram Y^T Y 1e5x50", 50, 50, 100000, 0, 1, 0),
+        ("Q*M 1e6x500x100", 1000000, 100, 500, 1, 1, 1),
+        ("Q^T*Y 1e6x500x100", 500, 100, 1000000, 0, 1, 1),
+        ("Bt^T*Om 5e5x500x100", 500, 100, 500000, 0, 1, 1),
+        ("Bt*M 5e5x500x100", 500000, 100, 500, 1, 1, 1),
     ]
     res = {}
     for name, M, N, K, ar, br, cr in shapes:
