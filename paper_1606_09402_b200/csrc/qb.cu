@@ -102,7 +102,10 @@ Matrix::~Matrix() {
     }
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    if (a && owns_a) cudaFree(a);
+    if (a && owns_a) {
+        if (pooled_a) cudaFreeAsync(a, ctx->st);
+        else cudaFree(a);
+    }
     if (rp) cudaFree(rp);
     if (ci) cudaFree(ci);
     if (v) cudaFree(v);
@@ -128,7 +131,9 @@ std::unique_ptr<Matrix> make_dense(Context& c, std::int64_t m_global, std::int64
     mat->m_global = m_global;
     mat->row0 = row0;
     mat->lda = std::max<std::int64_t>(8, round_up(m, 8));
-    QB_CUDA(cudaMalloc(&mat->a, sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1)));
+    // stream-ordered pool (retained across calls): no cudaMalloc/cudaFree of the whole matrix per upload
+    QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mat->a), sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1), c.st));
+    mat->pooled_a = true;
     if (mat->lda != m) QB_CUDA(cudaMemsetAsync(mat->a, 0, sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1), c.st));
     if (m > 0 && n > 0)
         QB_CUDA(cudaMemcpy2DAsync(mat->a, mat->lda * sizeof(double), a, lda * sizeof(double), m * sizeof(double), n,
@@ -153,7 +158,9 @@ std::unique_ptr<Matrix> make_dense_async(Context& c, std::int64_t m, std::int64_
     mat->n = n;
     mat->m_global = m;
     mat->lda = std::max<std::int64_t>(8, round_up(m, 8));
-    QB_CUDA(cudaMalloc(&mat->a, sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1)));
+    QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mat->a), sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1),
+                            c.st_copy));
+    mat->pooled_a = true;
     if (mat->lda != m) {
         QB_CUDA(cudaMemsetAsync(mat->a, 0, sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1), c.st_copy));
     }

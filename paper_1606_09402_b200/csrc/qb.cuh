@@ -82,6 +82,7 @@ struct Matrix {
     double* a = nullptr;
     std::int64_t lda = 0;
     bool owns_a = true;
+    bool pooled_a = false;  // `a` from the stream-ordered pool (freed with cudaFreeAsync on ctx->st)
     // CSR + device-built transposed CSR
     std::int64_t nnz = 0;
     std::int64_t* rp = nullptr;

@@ -107,10 +107,21 @@ __global__ void sumsq_stage1(const double* __restrict__ p, std::int64_t outer, s
         const std::int64_t i0 = (u % pieces_per_seg) * piece;
         const std::int64_t i1 = min(inner, i0 + piece);
         const double* seg = p + s * ld;
-        for (std::int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-            const double v = seg[i];
-            acc = fma(v, v, acc);
+        // 8 independent loads in flight per thread (a single dependent chain ran at ~2.3 TB/s)
+        double a8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        std::int64_t i = i0 + threadIdx.x;
+        for (; i + 7 * static_cast<std::int64_t>(blockDim.x) < i1; i += 8 * static_cast<std::int64_t>(blockDim.x)) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = __ldg(seg + i + q * static_cast<std::int64_t>(blockDim.x));
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a8[q] = fma(v[q], v[q], a8[q]);
         }
+        for (; i < i1; i += blockDim.x) {
+            const double v = seg[i];
+            a8[0] = fma(v, v, a8[0]);
+        }
+        acc += ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
     }
     const double s = block_sum<kRedThreads>(acc, sh);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
@@ -130,12 +141,20 @@ __global__ void colsumsq_stage1(MatView v, std::int64_t chunk, double* __restric
     const std::int64_t r0 = blockIdx.x * chunk;
     const std::int64_t r1 = min(v.rows, r0 + chunk);
     for (std::int64_t j = threadIdx.x; j < v.cols; j += blockDim.x) {
-        double acc = 0.0;
-        for (std::int64_t i = r0; i < r1; ++i) {
-            const double x = *v.at(i, j);
-            acc = fma(x, x, acc);
+        double a8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // 8 rows in flight per thread
+        std::int64_t i = r0;
+        for (; i + 8 <= r1; i += 8) {
+            double x[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) x[q] = *v.at(i + q, j);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a8[q] = fma(x[q], x[q], a8[q]);
         }
-        partial[blockIdx.x * v.cols + j] = acc;
+        for (; i < r1; ++i) {
+            const double x = *v.at(i, j);
+            a8[0] = fma(x, x, a8[0]);
+        }
+        partial[blockIdx.x * v.cols + j] = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
     }
 }
 
