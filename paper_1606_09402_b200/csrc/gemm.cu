@@ -418,6 +418,11 @@ bool aligned16(const MatView& v) {
 
 }  // namespace
 
+void make_tensor_map_rows(void* map, const double* base, std::int64_t rows, int w, std::int64_t ld) {
+    // one row of w doubles per box (tile::gather4 requires box height 1)
+    make_tmap(reinterpret_cast<CUtensorMap*>(map), base, w, rows, ld, w, 1);
+}
+
 int gemm_num_sms() {
     static int sms = [] {
         int dev = 0, n = 148;
