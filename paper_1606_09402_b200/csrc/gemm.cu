@@ -449,9 +449,12 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     Family fam;
     int bm, bn, bk;
     // wide widths: 128-column tiles unless 80-column tiles pad less (e.g. l = 400: 4 x 128 = 512
-    // vs 5 x 80 = 400)
+    // vs 5 x 80 = 400; l = 2000: 2048 vs 2000)
     // (A column-major only: the A^T passes measured faster on 128-wide tiles)
-    const bool use80 = N >= 96 && 10 * round_up(N, 80) < 9 * round_up(N, 128);
+    // (N = 2000: 25 x 80 columns, no padding, measured 0.8-5 % faster than 16 x 128 on the
+    // cfg2 passes, Gram and X R^-1)
+    // (not for upper-triangular outputs: the 128 x 80 tiles straddling the diagonal waste more)
+    const bool use80 = N >= 96 && round_up(N, 80) < round_up(N, 128) && !(flags & kGemmUpperC);
     if (use80) { fam = Family::kWide80; bm = 128; bn = 80; bk = 32; }
     else if (N >= 96) { fam = Family::kWide; bm = 128; bn = 128; bk = QB_WIDE_BK; }
     else if (N > 48 && N <= 56) { fam = Family::kSkinny56; bm = 128; bn = 56; bk = 32; }

@@ -14,9 +14,6 @@
 // result is bitwise reproducible.
 
 #include "sparse.cuh"
-#include "gemm.cuh"
-
-#include <cuda.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -177,8 +174,8 @@ __device__ __forceinline__ void store_row2(double* __restrict__ yr, int w, int l
     }
 }
 
-template <int NQ2>
-__global__ void __launch_bounds__(256, 4)
+template <int NQ2, int MINB = 4>
+__global__ void __launch_bounds__(256, MINB)
 csr_spmm_kernel2(std::int64_t rows, const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
                  const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx,
                  double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, bool y_vec) {
@@ -208,290 +205,6 @@ csr_spmm_kernel2(std::int64_t rows, const std::int64_t* __restrict__ rp, const s
                 }
         }
     }
-}
-
-// Row-block CSR pass (irregular / power-law rows): a warp takes 32 consecutive rows and
-// streams their nonzeros as ONE sequence — 32 (col, val) pairs per coalesced load, 4 X-row
-// gathers in flight per step regardless of row boundaries — and flushes a row's sum to Y
-// when the sequence moves past it. Short rows (config 5: median length 10) no longer pay a
-// per-row rp -> (col, val) -> gather load chain plus a serial tail. A row's nonzeros are
-// summed in order by one chain (deterministic). Rows longer than kHeavyRow are skipped
-// (segment kernels + combine); empty rows get y = beta * y.
-template <int NQ2>
-__device__ __forceinline__ void flush_row2(double* __restrict__ yr, int w, int lane, const double2 (&acc)[NQ2],
-                                           double alpha, double beta, bool y_vec) {
-    if (y_vec) {
-        store_row2<NQ2>(yr, w, lane, acc, alpha, beta);
-        return;
-    }
-#pragma unroll
-    for (int q = 0; q < NQ2; ++q)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int col = 2 * (lane + 32 * q) + h;
-            if (col < w) {
-                const double r = alpha * (h ? acc[q].y : acc[q].x);
-                yr[col] = beta == 0.0 ? r : r + beta * yr[col];
-            }
-        }
-}
-
-template <int NQ2>
-__global__ void __launch_bounds__(256)
-csr_spmm_rowblock_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
-                         const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx,
-                         double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, bool y_vec) {
-    constexpr unsigned kAll = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const std::int64_t nblk = (rows + 31) >> 5;
-    const double2* x2 = reinterpret_cast<const double2*>(x);
-    const std::int64_t ldx2 = ldx >> 1;
-    for (std::int64_t blk = warp; blk < nblk; blk += nwarps) {
-        const std::int64_t i0 = blk << 5;
-        const int R = static_cast<int>(min(static_cast<std::int64_t>(32), rows - i0));
-        const bool in = lane < R;
-        const std::int64_t my_start = in ? __ldg(rp + i0 + lane) : 0;
-        const std::int64_t my_end = in ? __ldg(rp + i0 + lane + 1) : 0;
-        const std::int64_t len = my_end - my_start;
-        const unsigned heavy = __ballot_sync(kAll, in && len > kHeavyRow);
-        const unsigned empty = __ballot_sync(kAll, in && len == 0);
-        const std::int64_t blk_end = __shfl_sync(kAll, my_end, R - 1);
-        std::int64_t e = __shfl_sync(kAll, my_start, 0);
-        int cur = -1;
-        double2 acc[NQ2];
-#pragma unroll
-        for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
-        while (e < blk_end) {
-            // the next heavy row at or after e bounds this chunk (or is skipped if it starts at e)
-            const unsigned hv = heavy & __ballot_sync(kAll, in && my_start >= e);
-            std::int64_t stop = blk_end;
-            if (hv) {
-                const int hr = __ffs(hv) - 1;
-                stop = __shfl_sync(kAll, my_start, hr);
-                if (stop == e) {
-                    e = __shfl_sync(kAll, my_end, hr);
-                    continue;
-                }
-            }
-            const int cnt = static_cast<int>(min(static_cast<std::int64_t>(32), stop - e));
-            std::int32_t my_c = 0;
-            double my_v = 0.0;
-            if (lane < cnt) {
-                my_c = __ldg(ci + e + lane);
-                my_v = __ldg(v + e + lane);
-            }
-            for (int j = 0; j < cnt; j += 4) {
-                double2 g[4][NQ2];
-                double vv[4];
-                int rr[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int jj = j + q;
-                    const bool ok = jj < cnt;
-                    const std::int64_t c = __shfl_sync(kAll, my_c, jj & 31);
-                    vv[q] = __shfl_sync(kAll, my_v, jj & 31);
-                    rr[q] = __popc(__ballot_sync(kAll, in && my_start <= e + jj)) - 1;
-                    const double2* xr = x2 + c * ldx2;
-#pragma unroll
-                    for (int p = 0; p < NQ2; ++p) {
-                        const int pc = lane + 32 * p;
-                        g[q][p] = (ok && 2 * pc < w) ? __ldg(xr + pc) : make_double2(0.0, 0.0);
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (j + q >= cnt) break;
-                    if (rr[q] != cur) {
-                        if (cur >= 0) flush_row2<NQ2>(y + (i0 + cur) * ldy, w, lane, acc, alpha, beta, y_vec);
-                        cur = rr[q];
-#pragma unroll
-                        for (int p = 0; p < NQ2; ++p) acc[p] = make_double2(0.0, 0.0);
-                    }
-#pragma unroll
-                    for (int p = 0; p < NQ2; ++p) {
-                        acc[p].x = fma(vv[q], g[q][p].x, acc[p].x);
-                        acc[p].y = fma(vv[q], g[q][p].y, acc[p].y);
-                    }
-                }
-            }
-            e += cnt;
-        }
-        if (cur >= 0) flush_row2<NQ2>(y + (i0 + cur) * ldy, w, lane, acc, alpha, beta, y_vec);
-        // empty rows: y = alpha * 0 + beta * y
-        unsigned em = empty;
-        while (em) {
-            const int r = __ffs(em) - 1;
-            em &= em - 1;
-            double* yr = y + (i0 + r) * ldy;
-            for (int col = lane; col < w; col += 32) yr[col] = beta == 0.0 ? 0.0 : beta * yr[col];
-        }
-    }
-}
-
-// TMA-gather CSR pass: every warp streams the nonzeros of its 32-row blocks in chunks of
-// 32; the X rows of a chunk are fetched by tile::gather4 TMA instructions (one lane per 4
-// rows, SASS UTMALDG.GATHER4) into the warp's shared ring (2 chunks: one landing while the
-// other is consumed), so the gathers cost no registers and ~26 KB per warp are in flight.
-// Row sums are accumulated in nonzero order by one chain and flushed when the sequence
-// moves to the next row (deterministic). Heavy rows are skipped (segment kernels), empty
-// rows get y = beta * y. Needs w even, ldx even and a 16-byte aligned X.
-__device__ __forceinline__ void tg_wait(std::uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "TG_WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra TG_WAIT_%=;\n"
-        "}\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
-        "r"(parity)
-        : "memory");
-}
-
-template <int NQ2>
-__global__ void __launch_bounds__(256, 1)
-csr_spmm_gather_kernel(const __grid_constant__ CUtensorMap xmap, std::int64_t rows, const std::int64_t* __restrict__ rp,
-                       const std::int32_t* __restrict__ ci, const double* __restrict__ v, double* __restrict__ y,
-                       std::int64_t ldy, int w, double alpha, double beta, bool y_vec) {
-    constexpr unsigned kAll = 0xffffffffu;
-    extern __shared__ __align__(128) double gsm[];
-    __shared__ __align__(8) std::uint64_t bars[8][2];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    // a gather4 lands 4 rows at a 128-byte aligned shared address: groups of 4 rows are padded
-    const int gstride = (4 * w + 15) & ~15;  // doubles per group of 4 rows
-    const int sstride = 8 * gstride;         // doubles per slot (32 rows)
-    double* ring = gsm + static_cast<std::size_t>(wib) * 2 * sstride;
-    std::uint64_t* bar = bars[wib];
-    if (lane == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(&bar[0]))));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(&bar[1]))));
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncwarp();
-    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const std::int64_t nblk = (rows + 31) >> 5;
-    const unsigned row_bytes = static_cast<unsigned>(w) * 8u;
-    unsigned par = 0;     // parity bit per ring slot
-    int slot = 0;         // slot the next chunk lands in
-    // the chunk in flight (issued, not yet consumed)
-    bool pend = false;
-    int p_cnt = 0;
-    double p_v = 0.0;
-    std::int64_t p_row = 0;
-    // the row being accumulated
-    std::int64_t cur = -1;
-    double2 acc[NQ2];
-#pragma unroll
-    for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
-
-    int p_slot = 0;
-    auto consume = [&]() {
-        const int s = p_slot;
-        tg_wait(&bar[s], (par >> s) & 1u);
-        par ^= 1u << s;
-        const double* base = ring + static_cast<std::size_t>(s) * sstride;
-        for (int j = 0; j < p_cnt; ++j) {
-            const std::int64_t r = __shfl_sync(kAll, p_row, j);
-            const double a = __shfl_sync(kAll, p_v, j);
-            if (r != cur) {
-                if (cur >= 0) flush_row2<NQ2>(y + cur * ldy, w, lane, acc, alpha, beta, y_vec);
-                cur = r;
-#pragma unroll
-                for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
-            }
-            const double2* xr = reinterpret_cast<const double2*>(base + (j >> 2) * gstride + (j & 3) * w);
-#pragma unroll
-            for (int q = 0; q < NQ2; ++q) {
-                const int pc = lane + 32 * q;
-                if (2 * pc < w) {
-                    const double2 g = xr[pc];
-                    acc[q].x = fma(a, g.x, acc[q].x);
-                    acc[q].y = fma(a, g.y, acc[q].y);
-                }
-            }
-        }
-        __syncwarp();  // the slot is free for the next issue
-        pend = false;
-    };
-
-    for (std::int64_t blk = warp; blk < nblk; blk += nwarps) {
-        const std::int64_t i0 = blk << 5;
-        const int R = static_cast<int>(min(static_cast<std::int64_t>(32), rows - i0));
-        const bool in = lane < R;
-        const std::int64_t my_start = in ? __ldg(rp + i0 + lane) : 0;
-        const std::int64_t my_end = in ? __ldg(rp + i0 + lane + 1) : 0;
-        const std::int64_t len = my_end - my_start;
-        const unsigned heavy = __ballot_sync(kAll, in && len > kHeavyRow);
-        unsigned em = __ballot_sync(kAll, in && len == 0);
-        while (em) {  // empty rows: y = alpha * 0 + beta * y
-            const int r = __ffs(em) - 1;
-            em &= em - 1;
-            double* yr = y + (i0 + r) * ldy;
-            for (int col = lane; col < w; col += 32) yr[col] = beta == 0.0 ? 0.0 : beta * yr[col];
-        }
-        const std::int64_t blk_end = __shfl_sync(kAll, my_end, R - 1);
-        std::int64_t e = __shfl_sync(kAll, my_start, 0);
-        while (e < blk_end) {
-            const unsigned hv = heavy & __ballot_sync(kAll, in && my_start >= e);
-            std::int64_t stop = blk_end;
-            if (hv) {
-                const int hr = __ffs(hv) - 1;
-                stop = __shfl_sync(kAll, my_start, hr);
-                if (stop == e) {
-                    e = __shfl_sync(kAll, my_end, hr);
-                    continue;
-                }
-            }
-            const int cnt = static_cast<int>(min(static_cast<std::int64_t>(32), stop - e));
-            std::int32_t my_c = 0;
-            double my_v = 0.0;
-            if (lane < cnt) {
-                my_c = __ldg(ci + e + lane);
-                my_v = __ldg(v + e + lane);
-            }
-            // row of nonzero e + lane: the last row of the block whose start is <= it
-            int my_r = -1;
-            for (int k = 0; k < R; ++k) my_r += (__shfl_sync(kAll, my_start, k) <= e + lane) ? 1 : 0;
-            // issue this chunk's gathers into `slot` (free: its previous chunk was consumed)
-            const int ng = (cnt + 3) >> 2;
-            int c4[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int src = min(4 * lane + q, cnt - 1);
-                c4[q] = __shfl_sync(kAll, my_c, src & 31);
-            }
-            double* dst = ring + static_cast<std::size_t>(slot) * sstride;
-            if (lane == 0) {
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
-                                 static_cast<unsigned>(__cvta_generic_to_shared(&bar[slot]))),
-                             "r"(static_cast<unsigned>(ng) * 4u * row_bytes)
-                             : "memory");
-            }
-            __syncwarp();
-            if (lane < ng) {
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-                    " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(
-                        static_cast<unsigned>(__cvta_generic_to_shared(dst + static_cast<std::size_t>(lane) * gstride))),
-                    "l"(reinterpret_cast<std::uint64_t>(&xmap)), "r"(0), "r"(c4[0]), "r"(c4[1]), "r"(c4[2]), "r"(c4[3]),
-                    "r"(static_cast<unsigned>(__cvta_generic_to_shared(&bar[slot])))
-                    : "memory");
-            }
-            const int issued = slot;
-            slot ^= 1;
-            if (pend) consume();
-            pend = true;
-            p_slot = issued;
-            p_cnt = cnt;
-            p_v = my_v;
-            p_row = i0 + my_r;
-            e += cnt;
-        }
-    }
-    if (pend) consume();
-    if (cur >= 0) flush_row2<NQ2>(y + cur * ldy, w, lane, acc, alpha, beta, y_vec);
 }
 
 template <int NQ2>
@@ -723,61 +436,16 @@ void free_heavy_plan(HeavyPlan& p) {
 }
 
 namespace {
-template <int NQ2>
+template <int NQ2, int MINB = 4>
 void spmm_launch2(cudaStream_t st, const CsrView& a, const double* x, std::int64_t ldx, double* y, std::int64_t ldy,
                   int w, double alpha, double beta, int sms, double* partial) {
     const int threads = 256;
     const int blocks = static_cast<int>(std::max<std::int64_t>(
         1, std::min<std::int64_t>(ceil_div(a.rows * 32, threads), 16L * sms)));
     const bool y_vec = (ldy % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(y) & 15) == 0);
-    csr_spmm_kernel2<NQ2><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, y_vec);
+    csr_spmm_kernel2<NQ2, MINB><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, y_vec);
     QB_LAUNCH_CHECK();
     if (a.heavy.nseg > 0) {
-        const int sb = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(a.heavy.nseg * 32, threads), 16L * sms)));
-        csr_segment_kernel2<NQ2><<<sb, threads, 0, st>>>(a.heavy.nseg, a.heavy.seg, a.ci, a.v, x, ldx, w, partial);
-        QB_LAUNCH_CHECK();
-        csr_heavy_combine_kernel<<<static_cast<int>(std::min<std::int64_t>(a.heavy.nrows, 65535)), 128, 0, st>>>(
-            a.heavy.nrows, a.heavy.rows, partial, y, ldy, w, alpha, beta);
-        QB_LAUNCH_CHECK();
-    }
-}
-
-template <int NQ2>
-void spmm_launch_rowblock(cudaStream_t st, const CsrView& a, const double* x, std::int64_t ldx, double* y,
-                          std::int64_t ldy, int w, double alpha, double beta, int sms, double* partial) {
-    const int threads = 256;
-    const std::int64_t nblk = ceil_div(a.rows, 32);
-    const int blocks = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(nblk * 32, threads), 16L * sms)));
-    const bool y_vec = (ldy % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(y) & 15) == 0);
-    csr_spmm_rowblock_kernel<NQ2><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta,
-                                                              y_vec);
-    QB_LAUNCH_CHECK();
-    if (a.heavy.nseg > 0) {
-        const int sb = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(a.heavy.nseg * 32, threads), 16L * sms)));
-        csr_segment_kernel2<NQ2><<<sb, threads, 0, st>>>(a.heavy.nseg, a.heavy.seg, a.ci, a.v, x, ldx, w, partial);
-        QB_LAUNCH_CHECK();
-        csr_heavy_combine_kernel<<<static_cast<int>(std::min<std::int64_t>(a.heavy.nrows, 65535)), 128, 0, st>>>(
-            a.heavy.nrows, a.heavy.rows, partial, y, ldy, w, alpha, beta);
-        QB_LAUNCH_CHECK();
-    }
-}
-
-template <int NQ2>
-void spmm_launch_gather(cudaStream_t st, const CsrView& a, const double* x, std::int64_t ldx, std::int64_t xrows,
-                        double* y, std::int64_t ldy, int w, double alpha, double beta, int sms, double* partial) {
-    alignas(64) CUtensorMap map;
-    make_tensor_map_rows(&map, x, std::max<std::int64_t>(xrows, 1), w, ldx);
-    // warps per CTA: the two-chunk ring (2 x 32 rows x w doubles per warp) within ~200 KB
-    const int per_warp = 2 * 8 * ((4 * w + 15) & ~15) * 8;
-    const int nw = std::max(1, std::min(8, (200 * 1024) / per_warp));
-    const int smem = nw * per_warp;
-    auto kern = csr_spmm_gather_kernel<NQ2>;
-    QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const bool y_vec = (ldy % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(y) & 15) == 0);
-    kern<<<sms, nw * 32, smem, st>>>(map, a.rows, a.rp, a.ci, a.v, y, ldy, w, alpha, beta, y_vec);
-    QB_LAUNCH_CHECK();
-    if (a.heavy.nseg > 0) {
-        const int threads = 256;
         const int sb = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(a.heavy.nseg * 32, threads), 16L * sms)));
         csr_segment_kernel2<NQ2><<<sb, threads, 0, st>>>(a.heavy.nseg, a.heavy.seg, a.ci, a.v, x, ldx, w, partial);
         QB_LAUNCH_CHECK();
@@ -813,18 +481,6 @@ void csr_spmm(cudaStream_t st, const CsrView& a, const double* x, std::int64_t l
     const bool x_vec = (ldx % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(x) & 15) == 0) && (ldx >= w + (w & 1));
     // 16-byte gathers measured faster for 32 < w <= 64 only (config 3: +10-16 %); wider blocks
     // (config 5, w = 100) lose occupancy to the larger register footprint
-    static const int rowblock = [] {
-        const char* e = std::getenv("QBFAC_SPMM_ROWBLOCK");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (rowblock == 2 && x_vec && w % 2 == 0 && w <= 128 && a.cols > 0) {
-        if (w <= 64) return spmm_launch_gather<1>(st, a, x, ldx, a.cols, y, ldy, w, alpha, beta, sms, partial);
-        return spmm_launch_gather<2>(st, a, x, ldx, a.cols, y, ldy, w, alpha, beta, sms, partial);
-    }
-    if (rowblock == 1 && x_vec && w <= 128) {
-        if (w <= 64) return spmm_launch_rowblock<1>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
-        return spmm_launch_rowblock<2>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
-    }
     if (x_vec && w > 32 && w <= 64) return spmm_launch2<1>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
     if (w <= 32) return spmm_launch<1>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
     if (w <= 64) return spmm_launch<2>(st, a, x, ldx, y, ldy, w, alpha, beta, sms, partial);
