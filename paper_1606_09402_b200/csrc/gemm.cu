@@ -302,7 +302,8 @@ void make_tmap(CUtensorMap* map, const double* base, std::int64_t inner, std::in
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int NP>
 void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc, bool c_row, int M,
-               int N, int K, int splits, int klen, double alpha, double beta, double* partial, int flags) {
+               int N, int K, int splits, int klen, double alpha, double beta, double* partial, int flags,
+               Workspace* tws) {
     using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
     auto kern = dgemm_ws_kernel<BM, BN, BK, WM, WN, STAGES, AR, BR, NP>;
     constexpr int smem = T::SMEM_BYTES + 2 * STAGES * 8;
@@ -321,23 +322,51 @@ void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, s
     if (AR) make_tmap(&p.tmA, a.p, K, M, a.ld, T::LDA, BM);               // A(i,k) at A + i*lda + k
     if (BR && BN < 64) make_tmap(&p.tmB, b.p, N, K, b.ld, T::LDB, BK);    // B(k,j) at B + k*ldb + j
     if (!BR) make_tmap(&p.tmB, b.p, K, N, b.ld, T::LDB, BN);              // B(k,j) at B + k + j*ldb
-    const std::int64_t items = static_cast<std::int64_t>(p.tiles) * splits;
-    const int grid = static_cast<int>(std::min<std::int64_t>(items, static_cast<std::int64_t>(per_sm) * gemm_num_sms()));
+    std::int64_t items = static_cast<std::int64_t>(p.tiles) * splits;
+    const int gmax = per_sm * gemm_num_sms();
+    // Last-wave balancing: when the whole tiles leave a partial last wave (e.g. 1575 tiles on
+    // 148 CTAs: 10 waves + 95 tiles), the tail tiles are cut along K into s pieces so the tail
+    // takes ceil(tail*s/G)/s of a wave instead of one; pieces write partial tiles and the
+    // last-arriving piece sums them in piece order (deterministic) and runs the epilogue.
+    p.full_items = p.tiles;
+    p.tail_s = 0;
+    if (splits == 1 && !partial && tws && !(flags & (kGemmUpperC | kGemmTriB)) && p.tiles > gmax) {
+        const int tail = p.tiles % gmax;
+        double best = 1.0;
+        int best_s = 1;
+        for (int s = 2; s <= 16 && K / s >= 8 * BK; ++s) {
+            const double cost = static_cast<double>((tail * s + gmax - 1) / gmax) * (1.0 / s + 0.02);
+            if (cost < best - 0.05) { best = cost; best_s = s; }
+        }
+        if (tail > 0 && best_s > 1) {
+            p.full_items = p.tiles - tail;
+            p.tail_s = best_s;
+            p.tail_klen = static_cast<int>(round_up(ceil_div(K, best_s), BK));
+            const std::size_t part = static_cast<std::size_t>(tail) * best_s * BM * BN;
+            double* w = tws->get(part + (tail + 7) / 8 + 8);
+            p.tail_part = w;
+            p.tail_cnt = reinterpret_cast<unsigned*>(w + part);
+            QB_CUDA(cudaMemsetAsync(p.tail_cnt, 0, sizeof(unsigned) * tail, st));
+            items = p.full_items + static_cast<std::int64_t>(tail) * best_s;
+        }
+    }
+    const int grid = static_cast<int>(std::min<std::int64_t>(items, gmax));
     kern<<<grid, (WM * WN + NP) * 32, smem, st>>>(p);
     QB_LAUNCH_CHECK();
 }
 
 template <bool AR, bool BR>
 bool dispatch_ws(int fam, cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc, bool c_row,
-                 int M, int N, int K, int splits, int klen, double alpha, double beta, double* partial, int flags) {
+                 int M, int N, int K, int splits, int klen, double alpha, double beta, double* partial, int flags,
+                 Workspace* tws) {
     // one producer warp when both operands move by bulk TMA, two when cp.async chunks are involved
     constexpr int NP = (!AR && BR) ? 1 : 2;
-    if (fam == 0) launch_ws<128, 128, 32, 2, 4, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
-    else if (fam == 1) launch_ws<128, 64, 32, 4, 2, 4, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
-    else if (fam == 3) launch_ws<128, 56, 32, 8, 1, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
-    else if (fam == 4) launch_ws<128, 80, 32, 4, 2, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
-    else if (fam == 5) launch_ws<128, 112, 32, 4, 2, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
-    else launch_ws<64, 32, 32, 2, 2, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags);
+    if (fam == 0) launch_ws<128, 128, 32, 2, 4, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
+    else if (fam == 1) launch_ws<128, 64, 32, 4, 2, 4, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
+    else if (fam == 3) launch_ws<128, 56, 32, 8, 1, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
+    else if (fam == 4) launch_ws<128, 80, 32, 4, 2, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
+    else if (fam == 5) launch_ws<128, 112, 32, 4, 2, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
+    else launch_ws<64, 32, 32, 2, 2, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
     return true;
 }
 
@@ -497,11 +526,11 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
                           : fam == Family::kSkinny56 ? (a.rowmajor ? 3 : 1) : fam == Family::kSkinny ? 1 : 2;
         {
             if (a.rowmajor) {
-                if (b.rowmajor) dispatch_ws<true, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);
-                else dispatch_ws<true, false>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);
+                if (b.rowmajor) dispatch_ws<true, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags, &ws);
+                else dispatch_ws<true, false>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags, &ws);
             } else {
-                if (b.rowmajor) dispatch_ws<false, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);
-                else dispatch_ws<false, false>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags);
+                if (b.rowmajor) dispatch_ws<false, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags, &ws);
+                else dispatch_ws<false, false>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags, &ws);
             }
         }
     } else {

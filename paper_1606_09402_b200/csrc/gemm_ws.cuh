@@ -154,7 +154,16 @@ struct WsArgs {
     int tiles;  // output tiles per k-split (kGemmUpperC: only those on/above the diagonal)
     double alpha, beta;
     double* partial;
+    // last-wave balancing (launch_ws): items >= full_items are K-pieces of the tail tiles
+    int full_items, tail_s, tail_klen;
+    double* tail_part;    // (tail tiles x tail_s) partial tiles, fragment order
+    unsigned* tail_cnt;   // arrivals per tail tile (zeroed per launch)
 };
+
+// Work item -> tile and K range; tail_j >= 0 marks a K-piece of a tail tile.
+template <int BM, int BN>
+__device__ __forceinline__ void ws_item(const WsArgs& p, int it, int& mt, int& nt, int& kz, int& k_begin, int& k_end,
+                                        int& tail_j);
 
 // Work item -> (m tile, n tile, k split), n-fastest. For kGemmUpperC only the tiles
 // reaching the diagonal or above are enumerated (row mt starts at n tile mt*BM/BN),
@@ -183,6 +192,24 @@ __device__ __forceinline__ void ws_decode_item(const WsArgs& p, int it, int& mt,
     nt = (mt * BM) / BN + t;
 }
 
+template <int BM, int BN>
+__device__ __forceinline__ void ws_item(const WsArgs& p, int it, int& mt, int& nt, int& kz, int& k_begin, int& k_end,
+                                        int& tail_j) {
+    tail_j = -1;
+    if (p.tail_s && it >= p.full_items) {
+        const int j = it - p.full_items;
+        ws_decode_item<BM, BN>(p, p.full_items + j / p.tail_s, mt, nt, kz);
+        k_begin = (j % p.tail_s) * p.tail_klen;
+        k_end = min(p.K, k_begin + p.tail_klen);
+        tail_j = j;
+        return;
+    }
+    ws_decode_item<BM, BN>(p, it, mt, nt, kz);
+    k_begin = kz * p.k_split_len;
+    k_end = min(p.K, k_begin + p.k_split_len);
+    if (p.flags & kGemmTriB) k_end = min(k_end, nt * BN + BN);
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int NP>
 __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const __grid_constant__ WsArgs p) {
     using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
@@ -202,7 +229,8 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    const int items = p.tiles * p.splits;
+    const int items = p.tail_s ? p.full_items + (p.tiles - p.full_items) * p.tail_s : p.tiles * p.splits;
+    __shared__ int s_last;
     if (warp >= NC) {
         // ===== producer warps =====
         const int pt = threadIdx.x - NC * 32;  // producer thread index
@@ -210,12 +238,9 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
         int stage = 0;
         unsigned phase = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
-            int mt, nt, kz;
-            ws_decode_item<BM, BN>(p, it, mt, nt, kz);
+            int mt, nt, kz, k_begin, k_end, tail_j;
+            ws_item<BM, BN>(p, it, mt, nt, kz, k_begin, k_end, tail_j);
             const int m0 = mt * BM, n0 = nt * BN;
-            const int k_begin = kz * p.k_split_len;
-            int k_end = min(p.K, k_begin + p.k_split_len);
-            if (p.flags & kGemmTriB) k_end = min(k_end, n0 + BN);
             const int ntiles = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
             for (int kt = 0; kt < ntiles; ++kt) {
                 mbar_wait(&empty[stage], phase ^ 1);
@@ -283,12 +308,9 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
     int stage = 0;
     unsigned phase = 0;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        int mt, nt, kz;
-        ws_decode_item<BM, BN>(p, it, mt, nt, kz);
+        int mt, nt, kz, k_begin, k_end, tail_j;
+        ws_item<BM, BN>(p, it, mt, nt, kz, k_begin, k_end, tail_j);
         const int m0 = mt * BM, n0 = nt * BN;
-        const int k_begin = kz * p.k_split_len;
-        int k_end = min(p.K, k_begin + p.k_split_len);
-        if (p.flags & kGemmTriB) k_end = min(k_end, n0 + BN);
         const int ntiles = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
         double acc[T::MI][T::NI][4];
 #pragma unroll
@@ -352,6 +374,37 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (tail_j >= 0) {
+            // K-piece of a tail tile: publish the partial; the last piece to arrive sums all
+            // pieces in piece order and falls through to the epilogue
+            const int tt = tail_j / p.tail_s, piece = tail_j % p.tail_s;
+            constexpr int FR = T::MI * T::NI * 4 * 32;  // doubles per warp
+            double* mine = p.tail_part + (static_cast<std::size_t>(tt) * p.tail_s + piece) * (NC * FR) + warp * FR;
+#pragma unroll
+            for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) __stcg(mine + ((i * T::NI + j) * 4 + r) * 32 + lane, acc[i][j][r]);
+            __threadfence();
+            asm volatile("bar.sync 2, %0;\n" ::"n"(NC * 32) : "memory");
+            if (threadIdx.x == 0) s_last = atomicAdd(p.tail_cnt + tt, 1u) == static_cast<unsigned>(p.tail_s - 1);
+            asm volatile("bar.sync 2, %0;\n" ::"n"(NC * 32) : "memory");
+            if (!s_last) continue;
+            __threadfence();
+            const double* all = p.tail_part + static_cast<std::size_t>(tt) * p.tail_s * (NC * FR) + warp * FR;
+#pragma unroll
+            for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        double v = 0.0;
+                        for (int q = 0; q < p.tail_s; ++q)
+                            v += __ldcg(all + static_cast<std::size_t>(q) * (NC * FR) + ((i * T::NI + j) * 4 + r) * 32 + lane);
+                        acc[i][j][r] = v;
+                    }
         }
         // epilogue (registers -> global); the producer is already prefetching the next item
 #pragma unroll
