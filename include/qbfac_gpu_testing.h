@@ -11,6 +11,7 @@
  *   qbfac_gpu_test_householder  the Householder panel QR (orth_qr, qr.hpp:15-18)
  *   qbfac_gpu_test_orth_wide the power step's orth() of a wide sketch (CholQR2 or BCGS2)
  *   qbfac_gpu_test_colsumsq  per-column sums of squares (the indicator's row norms)
+ *   qbfac_gpu_test_chol_wide_trace  per-step stamps of the wide Cholesky
  *   qbfac_gpu_test_panel_trace  per-phase %globaltimer stamps (ns) of the last CholQR2 panel launch
  *   qbfac_gpu_test_csr_spmm  CSR pass Y = alpha A X + beta Y on device arrays
  *                            (replaces csr_gemm_n, kernels_drivers.cpp:67-79)
@@ -40,6 +41,9 @@ int qbfac_gpu_test_cholqr2(qbfac_gpu_ctx* ctx, const double* y, int64_t rows, in
    6 phase B done, 7 Gram B reduced, 8/9 chol B done / published, 10 end (two-pass), 11 end (one pass);
    then 32 clock64 stamps of the last in-CTA Cholesky (out must hold 44 values) */
 int qbfac_gpu_test_panel_trace(qbfac_gpu_ctx* ctx, unsigned long long* out);
+/* 64 x 4 %globaltimer stamps (ns) per step k of the last chol_wide launch (CTA 0): step start, phase 2
+   done, phase 3 done (incl. the next diagonal Cholesky on CTA 0), step end */
+int qbfac_gpu_test_chol_wide_trace(qbfac_gpu_ctx* ctx, unsigned long long* out);
 int qbfac_gpu_test_chol_wide(qbfac_gpu_ctx* ctx, double* g, int l, double* r, double* rinv, int* breakdown);
 /* Householder QR of a column-major m x b panel in place (Q overwrites y); R col-major ld b. */
 int qbfac_gpu_test_householder(qbfac_gpu_ctx* ctx, double* y, int64_t m, int b, int64_t ld, double* r);

@@ -512,6 +512,13 @@ int qbfac_gpu_test_cholqr2(qbfac_gpu_ctx* ctx, const double* y, int64_t rows, in
     });
 }
 
+int qbfac_gpu_test_chol_wide_trace(qbfac_gpu_ctx* ctx, unsigned long long* out) {
+    return guard(ctx, [&] {
+        QB_CUDA(cudaStreamSynchronize(ctx->c->st));
+        qbgpu::chol_wide_trace(out);
+    });
+}
+
 int qbfac_gpu_test_panel_trace(qbfac_gpu_ctx* ctx, unsigned long long* out) {
     return guard(ctx, [&] {
         QB_CUDA(cudaStreamSynchronize(ctx->c->st));

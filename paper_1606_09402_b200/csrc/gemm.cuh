@@ -90,7 +90,8 @@ int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, 
 // q <- t1 rb^{-1}; statuses of both Choleskies in st0 / st1. q may alias y. Small
 // matrices are column-major with ld kSmallMax. gbar: two zero-initialised words per
 // context (grid barrier).
-void panel_trace(unsigned long long* out);  // phase timestamps of the last panel launch
+void panel_trace(unsigned long long* out);
+void chol_wide_trace(unsigned long long* out);  // 64 x 4 step stamps of the last chol_wide launch  // phase timestamps of the last panel launch
 void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t rows, int b, std::int64_t ldy,
                    double* t1, double* q, std::int64_t ldq, double* g, double* ra, double* rainv, double* rb,
                    double* rbinv, SmallStatus* st0, SmallStatus* st1, unsigned* gbar);

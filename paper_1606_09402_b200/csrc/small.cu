@@ -565,6 +565,17 @@ struct CholWideArgs {
     SmallStatus* stats;
 };
 
+// per-step %globaltimer stamps of CTA 0 (qbfac_gpu_test_chol_wide_trace): [k][0] step start,
+// [k][1] phase 2 done, [k][2] phase 3 (CTA 0: W_{k+1,k+1} + its Cholesky) done, [k][3] step end
+__device__ unsigned long long g_cw_trace[64][4];
+__device__ __forceinline__ void cw_mark(int k, int slot) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && k < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_cw_trace[k][slot] = t;
+    }
+}
+
 __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs p) {
     extern __shared__ __align__(16) double cw_smem[];
     cg::grid_group grid = cg::this_grid();
@@ -580,6 +591,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
     if (cta == 0) chol_tile_block<64>(W(0, 0), p.ldw, sz(0), R(0, 0), F(0, 0), p.ldr, p.stats, cw_smem);
     grid.sync();
     for (int k = 0; k < nt; ++k) {
+        cw_mark(k, 0);
         const int bk = sz(k);
         const int n = nt - k - 1;
         // phase 2: items 1..n left (j = k + e), n+1..n+k right (p = e - n - 1)
@@ -594,6 +606,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
                 cw_tile_gemm(cw_smem, F(pp, k), 1, p.ldr, F(k, k), 1, p.ldr, F(pp, k), p.ldr, sz(pp), bk, bk, 1.0, 0.0);
             }
         }
+        cw_mark(k, 1);
         grid.sync();
         if (n == 0) break;
         // phase 3: item 0 = (k+1, k+1); then the other left tiles, then the right tiles
@@ -617,7 +630,9 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
                 chol_tile_block<64>(W(k + 1, k + 1), p.ldw, sz(k + 1), R(k + 1, k + 1), F(k + 1, k + 1), p.ldr,
                                     p.stats + k + 1, cw_smem);
         }
+        cw_mark(k, 2);
         grid.sync();
+        cw_mark(k, 3);
     }
 }
 
@@ -1466,6 +1481,10 @@ void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t
         case 96: launch_cholqr2_panel<96>(st, a, cap); break;
         default: launch_cholqr2_panel<112>(st, a, cap); break;
     }
+}
+
+void chol_wide_trace(unsigned long long* out) {
+    QB_CUDA(cudaMemcpyFromSymbol(out, g_cw_trace, sizeof(unsigned long long) * 64 * 4));
 }
 
 void panel_trace(unsigned long long* out) {

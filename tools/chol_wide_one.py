@@ -33,3 +33,15 @@ for i in range(reps):
     print(f"l={l} chol_wide {e0.elapsed_time(e1):.3f} ms (incl. memsets + status read)")
 rr = r.cpu().numpy().T
 print("resid", np.linalg.norm(rr.T @ rr - g0.cpu().numpy()) / np.linalg.norm(g0.cpu().numpy()))
+# per-step breakdown of the last launch (CTA 0 %globaltimer stamps)
+L.qbfac_gpu_test_chol_wide_trace.argtypes = [C.c_void_p, C.c_void_p]
+tr = np.zeros((64, 4), dtype=np.uint64)
+assert L.qbfac_gpu_test_chol_wide_trace(ctx.handle, tr.ctypes.data) == 0
+t = tr.astype(np.int64)
+nt = (l + 63) // 64
+ph2 = [(t[k, 1] - t[k, 0]) / 1e3 for k in range(nt)]
+ph3 = [(t[k, 2] - t[k, 1]) / 1e3 for k in range(nt - 1)]
+syn = [(t[k, 3] - t[k, 2]) / 1e3 for k in range(nt - 1)]
+print(f"steps {nt}: phase2 sum {sum(ph2):.1f} us (first {ph2[0]:.1f}), phase3(CTA0) sum {sum(ph3):.1f} us "
+      f"(first {ph3[0]:.1f}, last {ph3[-1]:.1f}), wait-for-grid sum {sum(syn):.1f} us, "
+      f"total {(t[nt - 1, 1] - t[0, 0]) / 1e3:.1f} us")
