@@ -152,6 +152,35 @@ def test_gemm_deterministic(ctx):
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 
+@pytest.mark.parametrize("m,n,k", [(8000, 2000, 2000), (20000, 400, 3000), (30000, 100, 1024)])
+@pytest.mark.parametrize("a_row,b_row,c_row", [(0, 1, 1), (1, 1, 1)])
+def test_gemm_last_wave_balanced(ctx, m, n, k, a_row, b_row, c_row):
+    """Shapes whose whole tiles leave a partial last wave (128x80 / 128x112 tiles on 148 SMs): the
+    tail tiles run as K-pieces reduced in piece order by the last-arriving piece (gemm_ws.cuh);
+    result within the GEMM tolerance and bitwise reproducible."""
+    import torch
+    L = _lib()
+    rs = np.random.default_rng(m + n + k)
+    a = rs.standard_normal((m, k))
+    b = rs.standard_normal((k, n))
+    c0 = rs.standard_normal((m, n))
+    ad, lda = _store(a, a_row)
+    bd, ldb = _store(b, b_row)
+    outs = []
+    for _ in range(2):
+        cd, ldc = _store(c0, c_row)
+        torch.cuda.synchronize()
+        st = L.qbfac_gpu_test_gemm(ctx.handle, 1.25, _ptr(ad), m, k, lda, a_row, _ptr(bd), n, ldb, b_row, -0.5,
+                                   _ptr(cd), ldc, c_row)
+        assert st == 0, L.qbfac_gpu_last_error(ctx.handle)
+        outs.append(_load(cd, (m, n), c_row))
+    assert np.array_equal(outs[0], outs[1])
+    ref = 1.25 * (a @ b) - 0.5 * c0
+    scale = 1.25 * (np.abs(a) @ np.abs(b)) + np.abs(0.5 * c0)
+    err = np.max(np.abs(outs[0] - ref) / scale)
+    assert err < 1e-13 * max(1.0, np.sqrt(k) / 8), err
+
+
 # ---- small dense kernels --------------------------------------------------------------------
 @pytest.mark.parametrize("b", [1, 5, 20, 50, 100, 112])
 def test_chol_small(ctx, b):
