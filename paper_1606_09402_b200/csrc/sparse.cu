@@ -178,13 +178,14 @@ template <int NQ2, int MINB = 4>
 __global__ void __launch_bounds__(256, MINB)
 csr_spmm_kernel2(std::int64_t rows, const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
                  const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx,
-                 double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, bool y_vec) {
+                 double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, bool y_vec,
+                 std::int64_t heavy_thr) {
     const int lane = threadIdx.x & 31;
     const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
     for (std::int64_t i = warp; i < rows; i += nwarps) {
         const std::int64_t e0 = rp[i], e1 = rp[i + 1];
-        if (e1 - e0 > kHeavyRow) continue;  // heavy rows: segment kernels
+        if (e1 - e0 > heavy_thr) continue;  // heavy rows: segment kernels
         double2 acc[NQ2];
 #pragma unroll
         for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
@@ -272,7 +273,7 @@ template <int NQ>
 __global__ void __launch_bounds__(256)
 csr_spmm_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
                 const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx,
-                double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta) {
+                double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, std::int64_t heavy_thr) {
     const int lane = threadIdx.x & 31;
     const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -281,7 +282,7 @@ csr_spmm_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const st
 #pragma unroll
         for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
         const std::int64_t e0 = rp[i], e1 = rp[i + 1];
-        if (e1 - e0 > kHeavyRow) continue;  // heavy rows: segment kernels
+        if (e1 - e0 > heavy_thr) continue;  // heavy rows: segment kernels
         row_dot<NQ>(ci, v, x, ldx, w, e0, e1, lane, acc);
         double* yr = y + i * ldy;
 #pragma unroll
@@ -395,22 +396,33 @@ __global__ void validate_kernel(std::int64_t m, std::int64_t n, std::int64_t nnz
 
 }  // namespace
 
+std::int64_t heavy_row_threshold() {
+    static const std::int64_t t = [] {
+        const char* e = std::getenv("QBFAC_HEAVY_ROW");
+        const long long v = e ? std::atoll(e) : 0;
+        return v > 0 ? static_cast<std::int64_t>(v) : kHeavyRow;
+    }();
+    return t;
+}
+
 HeavyPlan make_heavy_plan(const std::int64_t* rp, std::int64_t rows, cudaStream_t st) {
+    const std::int64_t thr = heavy_row_threshold();
     std::vector<std::int64_t> sr, slo, shi, hr, hs0, hns;
     for (std::int64_t i = 0; i < rows; ++i) {
         const std::int64_t len = rp[i + 1] - rp[i];
-        if (len <= kHeavyRow) continue;
+        if (len <= thr) continue;
         hr.push_back(i);
         hs0.push_back(static_cast<std::int64_t>(sr.size()));
         std::int64_t cnt = 0;
-        for (std::int64_t e = rp[i]; e < rp[i + 1]; e += kHeavyRow, ++cnt) {
+        for (std::int64_t e = rp[i]; e < rp[i + 1]; e += thr, ++cnt) {
             sr.push_back(i);
             slo.push_back(e);
-            shi.push_back(std::min(rp[i + 1], e + kHeavyRow));
+            shi.push_back(std::min(rp[i + 1], e + thr));
         }
         hns.push_back(cnt);
     }
     HeavyPlan p;
+    p.thr = thr;
     p.nseg = static_cast<std::int64_t>(sr.size());
     p.nrows = static_cast<std::int64_t>(hr.size());
     if (p.nseg == 0) return p;
@@ -443,7 +455,7 @@ void spmm_launch2(cudaStream_t st, const CsrView& a, const double* x, std::int64
     const int blocks = static_cast<int>(std::max<std::int64_t>(
         1, std::min<std::int64_t>(ceil_div(a.rows * 32, threads), 16L * sms)));
     const bool y_vec = (ldy % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(y) & 15) == 0);
-    csr_spmm_kernel2<NQ2, MINB><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, y_vec);
+    csr_spmm_kernel2<NQ2, MINB><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, y_vec, a.heavy.thr);
     QB_LAUNCH_CHECK();
     if (a.heavy.nseg > 0) {
         const int sb = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(a.heavy.nseg * 32, threads), 16L * sms)));
@@ -461,7 +473,7 @@ void spmm_launch(cudaStream_t st, const CsrView& a, const double* x, std::int64_
     const int threads = 256;
     const int blocks = static_cast<int>(std::max<std::int64_t>(
         1, std::min<std::int64_t>(ceil_div(a.rows * 32, threads), 16L * sms)));
-    csr_spmm_kernel<NQ><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta);
+    csr_spmm_kernel<NQ><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, a.heavy.thr);
     QB_LAUNCH_CHECK();
     if (a.heavy.nseg > 0) {
         const int sb = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(a.heavy.nseg * 32, threads), 16L * sms)));

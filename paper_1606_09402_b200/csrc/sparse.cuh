@@ -11,11 +11,16 @@ namespace qbgpu {
 
 // Rows longer than kHeavyRow nonzeros (Zipf-like dense rows, popular columns in the
 // transposed CSR) are cut into segments of at most kHeavyRow entries that separate
-// warps process; their partial rows are then summed in segment order.
-constexpr std::int64_t kHeavyRow = 4096;
+// warps process; their partial rows are then summed in segment order. A warp walks its row
+// 4 gathers per step, so one long row on one warp is a serial tail: config 5's passes went
+// 15.7 / 15.1 ms -> 12.2 / 11.9 ms when the threshold dropped from 4096 to 256
+// (tools/spmm_bench.py sweep 4096/1024/512/256/128/64; 128 was 2 % faster on config 5 but
+// segmented config 3's ~100-entry transposed columns, +10 %).
+constexpr std::int64_t kHeavyRow = 256;
 
 struct HeavyPlan {
     std::int64_t nseg = 0, nrows = 0;
+    std::int64_t thr = kHeavyRow;     // rows longer than thr are segmented (segments of thr entries)
     std::int64_t* seg = nullptr;      // device: 3 x nseg (row, lo, hi), segments of a row contiguous
     std::int64_t* rows = nullptr;     // device: 3 x nrows (row, first segment, segment count)
 };
@@ -30,6 +35,8 @@ struct CsrView {
 
 // Build the heavy-row plan from a host copy of row_ptr (device arrays allocated here).
 HeavyPlan make_heavy_plan(const std::int64_t* rp_host, std::int64_t rows, cudaStream_t st);
+// Segment length / heavy-row threshold (QBFAC_HEAVY_ROW overrides kHeavyRow).
+std::int64_t heavy_row_threshold();
 void free_heavy_plan(HeavyPlan& p);
 
 // Y(rows x w, row-major ldy) = alpha * A X + beta * Y, X (cols x w, row-major ldx).
