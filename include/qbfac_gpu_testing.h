@@ -11,6 +11,7 @@
  *   qbfac_gpu_test_householder  the Householder panel QR (orth_qr, qr.hpp:15-18)
  *   qbfac_gpu_test_orth_wide the power step's orth() of a wide sketch (CholQR2 or BCGS2)
  *   qbfac_gpu_test_colsumsq  per-column sums of squares (the indicator's row norms)
+ *   qbfac_gpu_test_create_local_group  in-process rank group on one GPU (sharded-engine tests)
  *   qbfac_gpu_test_chol_wide_trace  per-step stamps of the wide Cholesky
  *   qbfac_gpu_test_panel_trace  per-phase %globaltimer stamps (ns) of the last CholQR2 panel launch
  *   qbfac_gpu_test_csr_spmm  CSR pass Y = alpha A X + beta Y on device arrays
@@ -41,6 +42,11 @@ int qbfac_gpu_test_cholqr2(qbfac_gpu_ctx* ctx, const double* y, int64_t rows, in
    6 phase B done, 7 Gram B reduced, 8/9 chol B done / published, 10 end (two-pass), 11 end (one pass);
    then 32 clock64 stamps of the last in-CTA Cholesky (out must hold 44 values) */
 int qbfac_gpu_test_panel_trace(qbfac_gpu_ctx* ctx, unsigned long long* out);
+/* `world` contexts on ONE device forming an in-process rank group: the row-sharded engine's
+   allreduces meet at a host barrier and rank 0 sums the buffers in rank order. Each rank must be
+   driven by its own host thread (qbfac_gpu_run blocks in the collectives). Test harness for the
+   NCCL path's arithmetic on a single GPU; outs[world] receives the contexts. */
+int qbfac_gpu_test_create_local_group(int device, int world, qbfac_gpu_ctx** outs);
 /* 64 x 4 %globaltimer stamps (ns) per step k of the last chol_wide launch (CTA 0): step start, phase 2
    done, phase 3 done (incl. the next diagonal Cholesky on CTA 0), step end */
 int qbfac_gpu_test_chol_wide_trace(qbfac_gpu_ctx* ctx, unsigned long long* out);

@@ -512,6 +512,22 @@ int qbfac_gpu_test_cholqr2(qbfac_gpu_ctx* ctx, const double* y, int64_t rows, in
     });
 }
 
+int qbfac_gpu_test_create_local_group(int device, int world, qbfac_gpu_ctx** outs) {
+    if (!outs || world < 2) return QBFAC_ERROR;
+    for (int r = 0; r < world; ++r) outs[r] = nullptr;
+    std::vector<std::unique_ptr<qbfac_gpu_ctx>> hs;
+    int st = guard(nullptr, [&] {
+        auto g = std::make_shared<qbgpu::LocalGroup>(world);
+        for (int r = 0; r < world; ++r) {
+            hs.push_back(std::make_unique<qbfac_gpu_ctx>());
+            hs.back()->c = std::make_unique<qbgpu::Context>(device, r, world, nullptr, g);
+        }
+    });
+    if (st == QBFAC_OK)
+        for (int r = 0; r < world; ++r) outs[r] = hs[static_cast<std::size_t>(r)].release();
+    return st;
+}
+
 int qbfac_gpu_test_chol_wide_trace(qbfac_gpu_ctx* ctx, unsigned long long* out) {
     return guard(ctx, [&] {
         QB_CUDA(cudaStreamSynchronize(ctx->c->st));

@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -55,6 +56,34 @@ void check(ncclResult_t r, const char* what) {
 
 }  // namespace
 
+LocalGroup::~LocalGroup() {
+    if (sum) cudaFree(sum);
+}
+
+void LocalGroup::barrier() {
+    std::unique_lock<std::mutex> l(mu);
+    const unsigned g = gen;
+    if (++arrived == world) {
+        arrived = 0;
+        ++gen;
+        cv.notify_all();
+    } else {
+        cv.wait(l, [&] { return gen != g; });
+    }
+}
+
+namespace {
+__global__ void local_add_kernel(double* __restrict__ d, const double* __restrict__ s, std::size_t n) {
+    for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+        d[i] += s[i];
+}
+}  // namespace
+
+Comm::Comm(int rank, int world, std::shared_ptr<LocalGroup> group) : rank_(rank), world_(world), local_(std::move(group)) {
+    if (!local_ || world != local_->world || rank < 0 || rank >= world) throw QbError(kDimensionError, "bad local group");
+}
+
 Comm::Comm(int rank, int world, const void* unique_id128) : rank_(rank), world_(world) {
     if (world < 1 || rank < 0 || rank >= world) throw QbError(kDimensionError, "bad rank/world");
     if (world == 1) return;
@@ -71,6 +100,29 @@ Comm::~Comm() {
 }
 
 void Comm::allreduce_sum(double* p, std::size_t count, cudaStream_t st) {
+    if (local_) {
+        LocalGroup& g = *local_;
+        QB_CUDA(cudaStreamSynchronize(st));
+        g.ptrs[static_cast<std::size_t>(rank_)] = p;
+        g.barrier();
+        if (rank_ == 0 && count) {
+            if (g.cap < count) {
+                if (g.sum) QB_CUDA(cudaFree(g.sum));
+                QB_CUDA(cudaMalloc(&g.sum, count * sizeof(double)));
+                g.cap = count;
+            }
+            QB_CUDA(cudaMemcpyAsync(g.sum, g.ptrs[0], count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            for (int r = 1; r < world_; ++r)
+                local_add_kernel<<<static_cast<unsigned>(std::min<std::size_t>((count + 255) / 256, 1024)), 256, 0, st>>>(
+                    g.sum, g.ptrs[static_cast<std::size_t>(r)], count);
+            QB_CUDA(cudaStreamSynchronize(st));
+        }
+        g.barrier();
+        if (count) QB_CUDA(cudaMemcpyAsync(p, g.sum, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        QB_CUDA(cudaStreamSynchronize(st));
+        g.barrier();
+        return;
+    }
     if (world_ == 1 || count == 0) return;
     check(api().all_reduce(p, p, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), st),
           "ncclAllReduce");

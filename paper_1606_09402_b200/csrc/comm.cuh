@@ -5,14 +5,37 @@
 
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstddef>
 #include <cstdint>
+#include <memory>
+#include <mutex>
+#include <vector>
 
 namespace qbgpu {
+
+// In-process rank group on ONE device (test harness for the row-sharded engine): every rank is a
+// Context driven by its own host thread; allreduce_sum synchronizes the rank's stream, meets the
+// others at a host barrier, and rank 0 sums the buffers in rank order (deterministic, the same
+// order NCCL's ring would not guarantee). Kernels never wait on each other — only host threads do.
+struct LocalGroup {
+    explicit LocalGroup(int w) : world(w), ptrs(static_cast<std::size_t>(w), nullptr) {}
+    ~LocalGroup();
+    void barrier();
+    int world;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    unsigned gen = 0;
+    std::vector<double*> ptrs;
+    double* sum = nullptr;
+    std::size_t cap = 0;
+};
 
 class Comm {
 public:
     Comm(int rank, int world, const void* unique_id128);
+    Comm(int rank, int world, std::shared_ptr<LocalGroup> group);  // in-process loopback (tests)
     ~Comm();
     Comm(const Comm&) = delete;
     Comm& operator=(const Comm&) = delete;
@@ -27,6 +50,7 @@ public:
 private:
     int rank_, world_;
     void* comm_ = nullptr;
+    std::shared_ptr<LocalGroup> local_;
 };
 
 }  // namespace qbgpu

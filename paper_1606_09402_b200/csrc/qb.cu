@@ -44,7 +44,8 @@ enum SmallSlot { kG = 0, kRa, kRainv, kRb, kRbinv, kR1, kR1inv, kR2, kR2inv, kR,
 }  // namespace
 
 // ---------------------------------------------------------------------------------
-Context::Context(int dev, int rank_, int world_, const void* nccl_id) : device(dev), rank(rank_), world(world_) {
+Context::Context(int dev, int rank_, int world_, const void* nccl_id, std::shared_ptr<LocalGroup> local)
+    : device(dev), rank(rank_), world(world_) {
     QB_CUDA(cudaSetDevice(dev));
     cudaDeviceProp prop{};
     QB_CUDA(cudaGetDeviceProperties(&prop, dev));
@@ -70,7 +71,7 @@ Context::Context(int dev, int rank_, int world_, const void* nccl_id) : device(d
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     rng.device();
-    if (world > 1) comm = std::make_unique<Comm>(rank, world, nccl_id);
+    if (world > 1) comm = local ? std::make_unique<Comm>(rank, world, std::move(local)) : std::make_unique<Comm>(rank, world, nccl_id);
 }
 
 Context::~Context() {

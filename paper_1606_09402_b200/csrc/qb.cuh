@@ -65,7 +65,8 @@ struct Context {
     IndicatorOut* h_ind = nullptr;
     double* h_scalar = nullptr;
 
-    explicit Context(int dev, int rank_ = 0, int world_ = 1, const void* nccl_id = nullptr);
+    explicit Context(int dev, int rank_ = 0, int world_ = 1, const void* nccl_id = nullptr,
+                     std::shared_ptr<LocalGroup> local = nullptr);
     ~Context();
     void allreduce(double* p, std::size_t count) {
         if (comm) comm->allreduce_sum(p, count, st);

@@ -1,0 +1,110 @@
+"""Row-sharded engine on one GPU: `world` contexts form an in-process rank
+group (qbfac_gpu_test_create_local_group), each driven by its own host thread; the engine's
+collectives — the n x w allreduce after every A^T pass, the b x b / k x b Gram allreduces and
+||A||^2 — meet at a host barrier and are summed in rank order. Every rank must reproduce the
+unsharded factorization: same rank, passes and termination, bitwise-identical replicated B across
+ranks, σ(B) and ||A - QB|| of the stacked row shards of Q against the single-context run."""
+import ctypes as C
+import threading
+
+import numpy as np
+import pytest
+
+from paper_1606_09402_b200 import dist, matgen, qbfac
+
+pytestmark = pytest.mark.gpu
+
+
+def _local_group(world):
+    L = qbfac.lib()
+    L.qbfac_gpu_test_create_local_group.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+    arr = (C.c_void_p * world)()
+    st = L.qbfac_gpu_test_create_local_group(0, world, arr)
+    assert st == 0, L.qbfac_gpu_last_error(None).decode()
+    ctxs = []
+    for r in range(world):
+        c = qbfac.Context.__new__(qbfac.Context)
+        c._h = C.c_void_p(arr[r])
+        c.device, c.rank, c.world = 0, r, world
+        ctxs.append(c)
+    return ctxs
+
+
+def _run_ranks(handles, **kw):
+    out, errs = [None] * len(handles), []
+
+    def work(r):
+        try:
+            res = qbfac.run_device(handles[r], **kw)
+            out[r] = (res.rank, int(res.info.passes), int(res.info.terminated_by), float(res.info.error_indicator),
+                      res.q(), res.b())
+            res.free()
+        except Exception as ex:  # pragma: no cover - surfaced below
+            errs.append(repr(ex))
+
+    ths = [threading.Thread(target=work, args=(r,)) for r in range(len(handles))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=300)
+    assert not errs, errs
+    return out
+
+
+def _single(h, **kw):
+    res = qbfac.run_device(h, **kw)
+    o = (res.rank, int(res.info.passes), int(res.info.terminated_by), float(res.info.error_indicator), res.q(), res.b())
+    res.free()
+    return o
+
+
+def _check(a_dense, ref, shards, sig_tol):
+    rank, passes, term, e, q, b = ref
+    for r, s in enumerate(shards):
+        assert s[0] == rank and s[1] == passes and s[2] == term, (r, s[:3], ref[:3])
+        assert np.array_equal(s[5], shards[0][5]), "replicated B differs across ranks"
+    qs = np.vstack([s[4] for s in shards])
+    bs = shards[0][5]
+    sg = np.linalg.svd(bs, compute_uv=False)
+    sr = np.linalg.svd(b, compute_uv=False)
+    assert np.max(np.abs(sg - sr) / sr) < sig_tol
+    err_s = np.linalg.norm(a_dense - qs @ bs)
+    err_r = np.linalg.norm(a_dense - q @ b)
+    assert abs(err_s - err_r) <= 1e-8 * np.linalg.norm(a_dense) + 1e-6 * err_r
+    if e >= 0:
+        assert abs(shards[0][3] - e) <= 1e-10 * e + 1e-13 * np.linalg.norm(a_dense) ** 2
+    assert np.linalg.norm(qs.T @ qs - np.eye(qs.shape[1])) < 1e-10
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("alg,kw", [(0, dict(b=10, power=1, max_rank=200)),
+                                    (1, dict(b=10, power=1, max_rank=200, l_budget=120)),
+                                    (3, dict(mode=0, b=16, k=60, s=0))])
+def test_sharded_dense_matches_single(world, alg, kw):
+    a = matgen.synthesize(901, 300, matgen.spectrum("exp_decay", 300, tau=12.0), 21)
+    eps = 1e-3 * np.linalg.norm(a)
+    run = dict(alg=alg, eps_abs=eps, seed=7, **kw)
+    ref = _single(qbfac.MatrixHandle.dense(a, qbfac.default_context()), **run)
+    ctxs = _local_group(world)
+    plan = dist.plan_dense_rows(a.shape[0], world)
+    hs = [qbfac.MatrixHandle.dense_shard(dist.shard_dense(a, r0, rows), a.shape[0], r0, ctxs[g])
+          for g, (r0, rows) in enumerate(plan)]
+    shards = _run_ranks(hs, **run)
+    _check(a, ref, shards, 1e-10 if alg == 0 else 1e-8)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_csr_ei_matches_single(world):
+    csr = matgen.csr_uniform(1200, 500, 13, seed=11)
+    a = matgen.csr_to_dense(csr)
+    eps = 0.6 * np.linalg.norm(a)
+    run = dict(alg=0, b=20, power=1, max_rank=120, eps_abs=eps, seed=3)
+    ref = _single(qbfac.MatrixHandle.csr(*csr, ctx=qbfac.default_context()), **run)
+    ctxs = _local_group(world)
+    plan = dist.plan_csr_rows(csr[2], world)
+    hs = []
+    for g, (r0, rows) in enumerate(plan):
+        loc = dist.shard_csr(csr, r0, rows)
+        hs.append(qbfac.MatrixHandle.csr_shard(csr[0], r0, csr[1], loc[2], loc[3], loc[4], ctxs[g]))
+    shards = _run_ranks(hs, **run)
+    _check(a, ref, shards, 1e-10)
