@@ -881,13 +881,24 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
         }
     };
     // fixed-order sum of the CTA partials into the b x b Gram slot (upper triangle)
+    // one warp per Gram entry: lanes load partials lane, lane+32, ... (all in flight at once) and
+    // a fixed shuffle tree sums them (deterministic); a thread per entry walking all G partials
+    // serially cost 6-10 us per reduction
     auto reduce_parts = [&]() {
-        for (int e = cta * blockDim.x + tid; e < BP * BP; e += G * blockDim.x) {
+        const int nwg = (G * blockDim.x) >> 5;
+        for (int e = (cta * blockDim.x + tid) >> 5; e < BP * BP; e += nwg) {
             const int i = e % BP, j = e / BP;
-            if (i > j || j >= p.b) continue;
-            double s = 0.0;
-            for (int c = 0; c < G; ++c) s += __ldcg(p.part + static_cast<std::size_t>(c) * BP * BP + e);
-            p.g[i + j * kSmallMax] = s;
+            if (i > j || j >= p.b) continue;  // warp-uniform
+            double v[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                const int c = lane + 32 * q;
+                v[q] = c < G ? __ldcg(p.part + static_cast<std::size_t>(c) * BP * BP + e) : 0.0;
+            }
+            double s = ((v[0] + v[1]) + (v[2] + v[3])) + v[4];
+            for (int c = lane + 160; c < G; c += 32) s += __ldcg(p.part + static_cast<std::size_t>(c) * BP * BP + e);
+            s = warp_sum(s);
+            if (lane == 0) p.g[i + j * kSmallMax] = s;
         }
     };
     auto stage_r = [&](const double* rinv) {
