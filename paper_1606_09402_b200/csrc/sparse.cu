@@ -179,11 +179,25 @@ __global__ void __launch_bounds__(256, MINB)
 csr_spmm_kernel2(std::int64_t rows, const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
                  const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx,
                  double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, bool y_vec,
-                 std::int64_t heavy_thr) {
+                 std::int64_t heavy_thr, std::int64_t nseg, const std::int64_t* __restrict__ seg,
+                 double* __restrict__ partial) {
     const int lane = threadIdx.x & 31;
     const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (std::int64_t i = warp; i < rows; i += nwarps) {
+    for (std::int64_t s = warp; s < nseg; s += nwarps) {  // heavy-row segments first (see csr_spmm_kernel)
+        double2 acc[NQ2];
+#pragma unroll
+        for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
+        row_dot2<NQ2>(ci, v, x, ldx, w, seg[nseg + s], seg[2 * nseg + s], lane, acc);
+#pragma unroll
+        for (int q = 0; q < NQ2; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int col = 2 * (lane + 32 * q) + h;
+                if (col < w) partial[s * w + col] = h ? acc[q].y : acc[q].x;
+            }
+    }
+    for (std::int64_t i = (warp + nwarps - nseg % nwarps) % nwarps; i < rows; i += nwarps) {
         const std::int64_t e0 = rp[i], e1 = rp[i + 1];
         if (e1 - e0 > heavy_thr) continue;  // heavy rows: segment kernels
         double2 acc[NQ2];
@@ -208,50 +222,7 @@ csr_spmm_kernel2(std::int64_t rows, const std::int64_t* __restrict__ rp, const s
     }
 }
 
-template <int NQ2>
-__global__ void __launch_bounds__(256)
-csr_segment_kernel2(std::int64_t nseg, const std::int64_t* __restrict__ seg, const std::int32_t* __restrict__ ci,
-                    const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx, int w,
-                    double* __restrict__ partial) {
-    const int lane = threadIdx.x & 31;
-    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (std::int64_t s = warp; s < nseg; s += nwarps) {
-        double2 acc[NQ2];
-#pragma unroll
-        for (int q = 0; q < NQ2; ++q) acc[q] = make_double2(0.0, 0.0);
-        row_dot2<NQ2>(ci, v, x, ldx, w, seg[nseg + s], seg[2 * nseg + s], lane, acc);
-#pragma unroll
-        for (int q = 0; q < NQ2; ++q)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int col = 2 * (lane + 32 * q) + h;
-                if (col < w) partial[s * w + col] = h ? acc[q].y : acc[q].x;
-            }
-    }
-}
 
-// Heavy-row segments: warp per segment, partial row into partial[seg * w + col].
-template <int NQ>
-__global__ void __launch_bounds__(256)
-csr_segment_kernel(std::int64_t nseg, const std::int64_t* __restrict__ seg, const std::int32_t* __restrict__ ci,
-                   const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx, int w,
-                   double* __restrict__ partial) {
-    const int lane = threadIdx.x & 31;
-    const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (std::int64_t s = warp; s < nseg; s += nwarps) {
-        double acc[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-        row_dot<NQ>(ci, v, x, ldx, w, seg[nseg + s], seg[2 * nseg + s], lane, acc);
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const int col = lane + 32 * q;
-            if (col < w) partial[s * w + col] = acc[q];
-        }
-    }
-}
 
 // Heavy rows: y[row] = alpha * sum over its segments (in order) + beta * y[row].
 __global__ void csr_heavy_combine_kernel(std::int64_t nrows, const std::int64_t* __restrict__ hr,
@@ -273,11 +244,25 @@ template <int NQ>
 __global__ void __launch_bounds__(256)
 csr_spmm_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
                 const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx,
-                double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, std::int64_t heavy_thr) {
+                double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, std::int64_t heavy_thr,
+                std::int64_t nseg, const std::int64_t* __restrict__ seg, double* __restrict__ partial) {
     const int lane = threadIdx.x & 31;
     const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (std::int64_t i = warp; i < rows; i += nwarps) {
+    // heavy-row segments first (uniform 256-entry work), then the light rows fill the tail; one
+    // launch, so warps that draw short rows move on instead of idling behind a second kernel
+    for (std::int64_t s = warp; s < nseg; s += nwarps) {
+        double acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+        row_dot<NQ>(ci, v, x, ldx, w, seg[nseg + s], seg[2 * nseg + s], lane, acc);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int col = lane + 32 * q;
+            if (col < w) partial[s * w + col] = acc[q];
+        }
+    }
+    for (std::int64_t i = (warp + nwarps - nseg % nwarps) % nwarps; i < rows; i += nwarps) {
         double acc[NQ];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
@@ -453,14 +438,12 @@ void spmm_launch2(cudaStream_t st, const CsrView& a, const double* x, std::int64
                   int w, double alpha, double beta, int sms, double* partial) {
     const int threads = 256;
     const int blocks = static_cast<int>(std::max<std::int64_t>(
-        1, std::min<std::int64_t>(ceil_div(a.rows * 32, threads), 16L * sms)));
+        1, std::min<std::int64_t>(ceil_div((a.rows + a.heavy.nseg) * 32, threads), 16L * sms)));
     const bool y_vec = (ldy % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(y) & 15) == 0);
-    csr_spmm_kernel2<NQ2, MINB><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, y_vec, a.heavy.thr);
+    csr_spmm_kernel2<NQ2, MINB><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, y_vec,
+                                                            a.heavy.thr, a.heavy.nseg, a.heavy.seg, partial);
     QB_LAUNCH_CHECK();
     if (a.heavy.nseg > 0) {
-        const int sb = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(a.heavy.nseg * 32, threads), 16L * sms)));
-        csr_segment_kernel2<NQ2><<<sb, threads, 0, st>>>(a.heavy.nseg, a.heavy.seg, a.ci, a.v, x, ldx, w, partial);
-        QB_LAUNCH_CHECK();
         csr_heavy_combine_kernel<<<static_cast<int>(std::min<std::int64_t>(a.heavy.nrows, 65535)), 128, 0, st>>>(
             a.heavy.nrows, a.heavy.rows, partial, y, ldy, w, alpha, beta);
         QB_LAUNCH_CHECK();
@@ -472,13 +455,11 @@ void spmm_launch(cudaStream_t st, const CsrView& a, const double* x, std::int64_
                  int w, double alpha, double beta, int sms, double* partial) {
     const int threads = 256;
     const int blocks = static_cast<int>(std::max<std::int64_t>(
-        1, std::min<std::int64_t>(ceil_div(a.rows * 32, threads), 16L * sms)));
-    csr_spmm_kernel<NQ><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, a.heavy.thr);
+        1, std::min<std::int64_t>(ceil_div((a.rows + a.heavy.nseg) * 32, threads), 16L * sms)));
+    csr_spmm_kernel<NQ><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, a.heavy.thr,
+                                                    a.heavy.nseg, a.heavy.seg, partial);
     QB_LAUNCH_CHECK();
     if (a.heavy.nseg > 0) {
-        const int sb = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(ceil_div(a.heavy.nseg * 32, threads), 16L * sms)));
-        csr_segment_kernel<NQ><<<sb, threads, 0, st>>>(a.heavy.nseg, a.heavy.seg, a.ci, a.v, x, ldx, w, partial);
-        QB_LAUNCH_CHECK();
         csr_heavy_combine_kernel<<<static_cast<int>(std::min<std::int64_t>(a.heavy.nrows, 65535)), 128, 0, st>>>(
             a.heavy.nrows, a.heavy.rows, partial, y, ldy, w, alpha, beta);
         QB_LAUNCH_CHECK();
