@@ -335,7 +335,7 @@ def main():
             "gpu_launches": int(launches * args.steps),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "dgemm_kernel (DMMA) G = A*Omega, 8000x8000x2000",
+                         "kernel": "dgemm_ws_kernel<128,80,32> (DMMA, TMA bulk + mbarrier ring) G = A*Omega, 8000x8000x2000",
                          "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run (FP64 tensor)",
                          "pass_ms": t_pass * 1e3},
             "cpu_baseline": cpu,

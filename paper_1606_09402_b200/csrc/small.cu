@@ -312,6 +312,10 @@ __device__ __forceinline__ void chol_tile_block(const double* __restrict__ gsrc,
             rinv[i + static_cast<std::int64_t>(j) * ldr] = iv;
         }
     } else {
+        // not unrolled: one copy of the (fully unrolled) 16 x 16 elimination serves every panel, so
+        // the instruction stream stays cache-resident (unrolled copies missed the instruction
+        // cache on every call inside chol_wide: 27k clk for the first panel, 44 us per 64 x 64)
+#pragma unroll 1
         for (int pnl = 0; pnl < C::P; ++pnl) {
             const int c0 = 16 * pnl, c1 = c0 + 16;
             double* Dv = Dall + pnl * 16 * C::TLD;
@@ -392,6 +396,7 @@ __device__ __forceinline__ void chol_tile_block(const double* __restrict__ gsrc,
         __syncthreads();
         chol_mark(23, trace);
         // in-place inversion, block column by block column
+#pragma unroll 1
         for (int jb = 0; jb < C::P; ++jb) {
             const int cj = 16 * jb;
             const double* Dj = Dall + jb * 16 * C::TLD;
