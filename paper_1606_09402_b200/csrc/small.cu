@@ -471,6 +471,14 @@ chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double*
 // F (in `rinv`, zero-initialised) ends as R^{-1}: the right half of the elimination of
 // [W | I] kept transposed (F_kk = R_kk^{-1} from phase 1). Two grid barriers per step
 // instead of ~5 dependent launches per 64-column panel.
+// chol_wide's diagonal factorization as an out-of-line call: its own register allocation instead
+// of sharing chol_wide_kernel's (the inlined copy spilled and ran ~2x slower than standalone)
+__device__ __noinline__ void chol_tile_block64_call(const double* __restrict__ g, std::int64_t ldg, int b,
+                                                    double* __restrict__ r, double* __restrict__ rinv, std::int64_t ldr,
+                                                    SmallStatus* status, double* sm) {
+    chol_tile_block<64>(g, ldg, b, r, rinv, ldr, status, sm);
+}
+
 constexpr int kCwNb = 64;
 constexpr int kCwLd = 68;   // padded shared stride (= 4 mod 16 doubles: conflict-free fragments)
 constexpr int kCwSmemBytes = 2 * kCwNb * kCwLd * 8;
@@ -593,7 +601,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
     // item e >= 1 of a phase -> CTA 1 + (e-1) % (G-1); item 0 (phase 3: W_{k+1,k+1}) -> CTA 0
     const int e_first = G == 1 ? 1 : cta, e_step = G == 1 ? 1 : G - 1;
     static_assert(CholCfg<64>::SMEM <= kCwSmemBytes, "chol workspace");
-    if (cta == 0) chol_tile_block<64>(W(0, 0), p.ldw, sz(0), R(0, 0), F(0, 0), p.ldr, p.stats, cw_smem);
+    if (cta == 0) chol_tile_block64_call(W(0, 0), p.ldw, sz(0), R(0, 0), F(0, 0), p.ldr, p.stats, cw_smem);
     grid.sync();
     for (int k = 0; k < nt; ++k) {
         cw_mark(k, 0);
@@ -632,8 +640,8 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
                 cw_tile_gemm(cw_smem, F(pp, k), 1, p.ldr, R(k, i), 1, p.ldr, F(pp, i), p.ldr, sz(pp), sz(i), bk, -1.0, 1.0);
             }
             if (e == 0)
-                chol_tile_block<64>(W(k + 1, k + 1), p.ldw, sz(k + 1), R(k + 1, k + 1), F(k + 1, k + 1), p.ldr,
-                                    p.stats + k + 1, cw_smem);
+                chol_tile_block64_call(W(k + 1, k + 1), p.ldw, sz(k + 1), R(k + 1, k + 1), F(k + 1, k + 1), p.ldr,
+                                       p.stats + k + 1, cw_smem);
         }
         cw_mark(k, 2);
         grid.sync();
