@@ -473,10 +473,16 @@ chol_small_kernel(const double* __restrict__ g, std::int64_t ldg, int b, double*
 // instead of ~5 dependent launches per 64-column panel.
 // chol_wide's diagonal factorization as an out-of-line call: its own register allocation instead
 // of sharing chol_wide_kernel's (the inlined copy spilled and ran ~2x slower than standalone)
-__device__ __noinline__ void chol_tile_block64_call(const double* __restrict__ g, std::int64_t ldg, int b,
-                                                    double* __restrict__ r, double* __restrict__ rinv, std::int64_t ldr,
-                                                    SmallStatus* status, double* sm) {
-    chol_tile_block<64>(g, ldg, b, r, rinv, ldr, status, sm);
+template <int BP>
+__device__ __noinline__ void chol_tile_block_call(const double* __restrict__ g, std::int64_t ldg, int b,
+                                                  double* __restrict__ r, double* __restrict__ rinv, std::int64_t ldr,
+                                                  SmallStatus* status, double* sm, bool trace = true) {
+    chol_tile_block<BP>(g, ldg, b, r, rinv, ldr, status, sm, trace);
+}
+__device__ __forceinline__ void chol_tile_block64_call(const double* __restrict__ g, std::int64_t ldg, int b,
+                                                       double* __restrict__ r, double* __restrict__ rinv,
+                                                       std::int64_t ldr, SmallStatus* status, double* sm) {
+    chol_tile_block_call<64>(g, ldg, b, r, rinv, ldr, status, sm);
 }
 
 constexpr int kCwNb = 64;
