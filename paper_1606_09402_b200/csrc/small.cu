@@ -127,6 +127,30 @@ __global__ void sumsq_stage1(const double* __restrict__ p, std::int64_t outer, s
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
+// Contiguous operand (ld == inner): a flat grid-stride sweep with 16-byte loads, 4 in flight per
+// thread (the segment/piece walk above reached only ~2.7 TB/s on the 512 MB config-2 matrix).
+__global__ void __launch_bounds__(kRedThreads) sumsq_flat_stage1(const double2* __restrict__ p, std::int64_t n2,
+                                                                  double* __restrict__ partial) {
+    __shared__ double sh[32];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+        const double2 v0 = __ldg(p + i), v1 = __ldg(p + i + stride), v2 = __ldg(p + i + 2 * stride),
+                      v3 = __ldg(p + i + 3 * stride);
+        a0 = fma(v0.x, v0.x, fma(v0.y, v0.y, a0));
+        a1 = fma(v1.x, v1.x, fma(v1.y, v1.y, a1));
+        a2 = fma(v2.x, v2.x, fma(v2.y, v2.y, a2));
+        a3 = fma(v3.x, v3.x, fma(v3.y, v3.y, a3));
+    }
+    for (; i < n2; i += stride) {
+        const double2 v = __ldg(p + i);
+        a0 = fma(v.x, v.x, fma(v.y, v.y, a0));
+    }
+    const double s = block_sum<kRedThreads>((a0 + a1) + (a2 + a3), sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
 __global__ void sumsq_stage2(const double* __restrict__ partial, int n, double* out) {
     __shared__ double sh[32];
     double acc = 0.0;
@@ -1402,7 +1426,11 @@ void sum_squares(cudaStream_t st, Workspace& ws, const MatView& v, double* out) 
     const int nblk = static_cast<int>(std::min<std::int64_t>(
         std::max<std::int64_t>(1, ceil_div(outer * inner, 8 * kRedThreads)), 4L * gemm_num_sms()));
     double* part = ws.get(static_cast<std::size_t>(nblk));
-    sumsq_stage1<<<nblk, kRedThreads, 0, st>>>(v.p, outer, inner, v.ld, part);
+    const std::int64_t total = outer * inner;
+    if (v.ld == inner && total % 2 == 0 && (reinterpret_cast<std::uintptr_t>(v.p) & 15) == 0 && total >= 65536)
+        sumsq_flat_stage1<<<nblk, kRedThreads, 0, st>>>(reinterpret_cast<const double2*>(v.p), total / 2, part);
+    else
+        sumsq_stage1<<<nblk, kRedThreads, 0, st>>>(v.p, outer, inner, v.ld, part);
     QB_LAUNCH_CHECK();
     sumsq_stage2<<<1, kRedThreads, 0, st>>>(part, nblk, out);
     QB_LAUNCH_CHECK();
