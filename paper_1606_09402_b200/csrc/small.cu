@@ -182,17 +182,16 @@ __global__ void colsumsq_stage1(MatView v, std::int64_t chunk, double* __restric
     }
 }
 
-// One warp per column: lanes take partials lane, lane+32, ... in order, then a fixed
-// shuffle tree (deterministic).
-__global__ void colsumsq_stage2(const double* __restrict__ partial, int nblk, std::int64_t cols,
-                                double* __restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const std::int64_t j = blockIdx.x * static_cast<std::int64_t>(blockDim.x / 32) + (threadIdx.x >> 5);
-    if (j >= cols) return;
+// One CTA per column: threads take partials tid, tid+256, ... (all loads in flight), then the
+// fixed block tree (deterministic).
+__global__ void __launch_bounds__(kRedThreads) colsumsq_stage2(const double* __restrict__ partial, int nblk,
+                                                               std::int64_t cols, double* __restrict__ out) {
+    __shared__ double sh[32];
+    const std::int64_t j = blockIdx.x;
     double s = 0.0;
-    for (int c = lane; c < nblk; c += 32) s += partial[c * cols + j];
-    s = warp_sum(s);
-    if (lane == 0) out[j] = s;
+    for (int c = threadIdx.x; c < nblk; c += kRedThreads) s += partial[c * cols + j];
+    s = block_sum<kRedThreads>(s, sh);
+    if (threadIdx.x == 0) out[j] = s;
 }
 
 constexpr int kCholThreads = 288;  // 9 warps: 8 DMMA warps + 1
@@ -1447,14 +1446,16 @@ void column_sumsq(cudaStream_t st, Workspace& ws, const MatView& v, double* out)
         QB_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * v.cols, st));
         return;
     }
-    const std::int64_t target = 2L * gemm_num_sms();
-    const std::int64_t chunk = std::max<std::int64_t>(64, ceil_div(v.rows, target));
+    // many short row chunks: each thread walks only ~16-32 rows (8 loads in flight), the fixed-order
+    // stage-2 warp sums the chunk partials (was 2 x SMs chunks: 27 us for a 5e4 x 50 block)
+    const std::int64_t target = 16L * gemm_num_sms();
+    const std::int64_t chunk = std::max<std::int64_t>(16, ceil_div(v.rows, target));
     const int nblk = static_cast<int>(ceil_div(v.rows, chunk));
     double* part = ws.get(static_cast<std::size_t>(nblk) * v.cols);
     const int thr = static_cast<int>(std::min<std::int64_t>(256, round_up(v.cols, 32)));
     colsumsq_stage1<<<nblk, thr, 0, st>>>(v, chunk, part);
     QB_LAUNCH_CHECK();
-    colsumsq_stage2<<<static_cast<int>(ceil_div(v.cols, 4)), 128, 0, st>>>(part, nblk, v.cols, out);
+    colsumsq_stage2<<<static_cast<int>(v.cols), kRedThreads, 0, st>>>(part, nblk, v.cols, out);
     QB_LAUNCH_CHECK();
 }
 
