@@ -5,7 +5,7 @@ timeout 200 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 300 python bench.py > $O/bench.log 2>&1
 timeout 300 python bench.py --impl reference > $O/bench_ref.log 2>&1
 timeout 900 python tools/run_configs.py --configs 1,3,4,5 > $O/run_configs.log 2>&1
-for c in 1 2 3; do
+for c in 1 2 3 4; do
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg$c.csv python tools/profile_run.py --config $c > $O/l$c.log 2>&1
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg5.csv python tools/profile_run.py --config 5 > $O/l5.log 2>&1
