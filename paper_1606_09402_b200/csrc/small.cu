@@ -1199,18 +1199,39 @@ __global__ void __launch_bounds__(1024) trmm_upper_kernel(TrmmPair prm, int n, s
     double* sa = sm;              // sa[i * lds + p] = A(i, p)
     double* sb = sm + n * lds;    // sb[j * lds + p] = B(p, j)
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    // staged with explicit zeros outside the triangles, so the product can run over the full p
+    // range: adding exact zeros in the same ascending-p order leaves every sum bit-identical to the
+    // triangular loop, and each thread's 16 outputs become 16 independent FMA chains
     for (int j = ty; j < n; j += 32)
         for (int i = tx; i < n; i += 32) {
-            sa[i * lds + j] = a[i + j * ld];
-            sb[j * lds + i] = bm[i + j * ld];
+            sa[i * lds + j] = j >= i ? a[i + j * ld] : 0.0;
+            sb[j * lds + i] = i <= j ? bm[i + j * ld] : 0.0;
         }
     __syncthreads();
-    for (int j = ty; j < n; j += 32)
-        for (int i = tx; i < n; i += 32) {
-            double s = 0.0;
-            if (i <= j)
-                for (int p = i; p <= j; ++p) s = fma(sa[i * lds + p], sb[j * lds + p], s);
-            c[i + j * ld] = s;
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+    for (int p = 0; p < n; ++p) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = tx + 32 * u, j = ty + 32 * u;
+            av[u] = i < n ? sa[i * lds + p] : 0.0;
+            bv[u] = j < n ? sb[j * lds + p] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int i = tx + 32 * u, j = ty + 32 * v;
+            if (i < n && j < n) c[i + j * ld] = i <= j ? acc[u][v] : 0.0;
         }
 }
 
