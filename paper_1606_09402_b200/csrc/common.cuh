@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
+#include <utility>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -74,5 +76,34 @@ struct MatView {
     MatView cols_range(std::int64_t c0, std::int64_t nc) const { return block(0, c0, rows, nc); }
     MatView rows_range(std::int64_t r0, std::int64_t nr) const { return block(r0, 0, nr, cols); }
 };
+
+// Programmatic dependent launch (PDL): GEMM and split-K-reduce launches may start while the
+// previous kernel on the stream drains; they execute griddepcontrol.wait before touching memory,
+// and each GEMM CTA signals launch_dependents once its last work item is done.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("QBFAC_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    QB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 }  // namespace qbgpu

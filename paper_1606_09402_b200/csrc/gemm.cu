@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <utility>
 
 #ifndef QB_WIDE_BK
 #define QB_WIDE_BK 32
@@ -243,9 +244,11 @@ dgemm_kernel(const double* __restrict__ A, std::int64_t lda, const double* __res
 
 // Deterministic split-K reduction: a CTA owns 32 consecutive outputs (lanes); warp g
 // sums splits g, g+8, ... in order, then warp 0 adds the 8 group sums in order.
+
 __global__ void __launch_bounds__(256)
 splitk_reduce_kernel(const double* __restrict__ partial, int splits, int M, int N, double alpha, double beta,
                      double* __restrict__ C, std::int64_t ldc, int c_row, int flags, int bm, int bn) {
+    pdl_wait();
     __shared__ double sh[8][33];
     const std::int64_t total = static_cast<std::int64_t>(M) * N;
     const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
@@ -351,7 +354,7 @@ void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, s
         }
     }
     const int grid = static_cast<int>(std::min<std::int64_t>(items, gmax));
-    kern<<<grid, (WM * WN + NP) * 32, smem, st>>>(p);
+    launch_pdl(kern, dim3(grid), dim3((WM * WN + NP) * 32), smem, st, p);
     QB_LAUNCH_CHECK();
 }
 
@@ -558,8 +561,9 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     }
     if (splits > 1) {
         const std::int64_t total = M * N;
-        splitk_reduce_kernel<<<static_cast<unsigned>(ceil_div(total, 32)), 256, 0, st>>>(
-            partial, splits, (int)M, (int)N, alpha, beta, c.p, c.ld, c.rowmajor ? 1 : 0, flags, bm, bn);
+        launch_pdl(splitk_reduce_kernel, dim3(static_cast<unsigned>(ceil_div(total, 32))), dim3(256), 0, st,
+                   static_cast<const double*>(partial), static_cast<int>(splits), static_cast<int>(M), static_cast<int>(N),
+                   alpha, beta, c.p, static_cast<std::int64_t>(c.ld), c.rowmajor ? 1 : 0, flags, bm, bn);
         QB_LAUNCH_CHECK();
     }
 }

@@ -214,6 +214,7 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, 
 __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const __grid_constant__ WsArgs p) {
     using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
     constexpr int NC = WM * WN;  // consumer warps
+    pdl_wait();  // launched with programmatic stream serialization: wait for the previous kernel's memory
     extern __shared__ __align__(128) double smem[];
     double* sA = smem;
     double* sB = smem + STAGES * T::A_STAGE;
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
+        pdl_trigger();
         return;
     }
     // ===== consumers =====

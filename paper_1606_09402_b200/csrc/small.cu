@@ -162,6 +162,7 @@ __global__ void sumsq_stage2(const double* __restrict__ partial, int n, double* 
 // Per-column sums of squares. CTA c owns rows [c*chunk, (c+1)*chunk); thread j owns
 // columns j, j+blockDim, ...
 __global__ void colsumsq_stage1(MatView v, std::int64_t chunk, double* __restrict__ partial) {
+    pdl_wait();
     const std::int64_t r0 = blockIdx.x * chunk;
     const std::int64_t r1 = min(v.rows, r0 + chunk);
     for (std::int64_t j = threadIdx.x; j < v.cols; j += blockDim.x) {
@@ -186,6 +187,7 @@ __global__ void colsumsq_stage1(MatView v, std::int64_t chunk, double* __restric
 // fixed block tree (deterministic).
 __global__ void __launch_bounds__(kRedThreads) colsumsq_stage2(const double* __restrict__ partial, int nblk,
                                                                std::int64_t cols, double* __restrict__ out) {
+    pdl_wait();
     __shared__ double sh[32];
     const std::int64_t j = blockIdx.x;
     double s = 0.0;
@@ -1253,6 +1255,7 @@ __global__ void tri_inverse_kernel(const double* __restrict__ r, double* __restr
 
 __global__ void indicator_kernel(double* e_dev, const double* __restrict__ norms, int b, double eps2,
                                  int check, IndicatorOut* out) {
+    pdl_wait();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double e = *e_dev;
     int keep = b, met = 0;
@@ -1474,9 +1477,10 @@ void column_sumsq(cudaStream_t st, Workspace& ws, const MatView& v, double* out)
     const int nblk = static_cast<int>(ceil_div(v.rows, chunk));
     double* part = ws.get(static_cast<std::size_t>(nblk) * v.cols);
     const int thr = static_cast<int>(std::min<std::int64_t>(256, round_up(v.cols, 32)));
-    colsumsq_stage1<<<nblk, thr, 0, st>>>(v, chunk, part);
+    launch_pdl(colsumsq_stage1, dim3(nblk), dim3(thr), 0, st, v, chunk, part);
     QB_LAUNCH_CHECK();
-    colsumsq_stage2<<<static_cast<int>(v.cols), kRedThreads, 0, st>>>(part, nblk, v.cols, out);
+    launch_pdl(colsumsq_stage2, dim3(static_cast<unsigned>(v.cols)), dim3(kRedThreads), 0, st,
+               static_cast<const double*>(part), nblk, static_cast<std::int64_t>(v.cols), out);
     QB_LAUNCH_CHECK();
 }
 
@@ -1619,7 +1623,7 @@ void tri_inverse_small(cudaStream_t st, const double* r, double* rinv, int n, st
 
 void indicator_step(cudaStream_t st, double* e_dev, const double* norms, int b, double eps2, int check,
                     IndicatorOut* out) {
-    indicator_kernel<<<1, 32, 0, st>>>(e_dev, norms, b, eps2, check, out);
+    launch_pdl(indicator_kernel, dim3(1), dim3(32), 0, st, e_dev, norms, b, eps2, check, out);
     QB_LAUNCH_CHECK();
 }
 

@@ -181,6 +181,7 @@ csr_spmm_kernel2(std::int64_t rows, const std::int64_t* __restrict__ rp, const s
                  double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, bool y_vec,
                  std::int64_t heavy_thr, std::int64_t nseg, const std::int64_t* __restrict__ seg,
                  double* __restrict__ partial) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -246,6 +247,7 @@ csr_spmm_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const st
                 const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx,
                 double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, std::int64_t heavy_thr,
                 std::int64_t nseg, const std::int64_t* __restrict__ seg, double* __restrict__ partial) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -440,8 +442,8 @@ void spmm_launch2(cudaStream_t st, const CsrView& a, const double* x, std::int64
     const int blocks = static_cast<int>(std::max<std::int64_t>(
         1, std::min<std::int64_t>(ceil_div((a.rows + a.heavy.nseg) * 32, threads), 16L * sms)));
     const bool y_vec = (ldy % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(y) & 15) == 0);
-    csr_spmm_kernel2<NQ2, MINB><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, y_vec,
-                                                            a.heavy.thr, a.heavy.nseg, a.heavy.seg, partial);
+    launch_pdl(csr_spmm_kernel2<NQ2, MINB>, dim3(blocks), dim3(threads), 0, st, a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w,
+               alpha, beta, y_vec, a.heavy.thr, a.heavy.nseg, static_cast<const std::int64_t*>(a.heavy.seg), partial);
     QB_LAUNCH_CHECK();
     if (a.heavy.nseg > 0) {
         csr_heavy_combine_kernel<<<static_cast<int>(std::min<std::int64_t>(a.heavy.nrows, 65535)), 128, 0, st>>>(
@@ -456,8 +458,8 @@ void spmm_launch(cudaStream_t st, const CsrView& a, const double* x, std::int64_
     const int threads = 256;
     const int blocks = static_cast<int>(std::max<std::int64_t>(
         1, std::min<std::int64_t>(ceil_div((a.rows + a.heavy.nseg) * 32, threads), 16L * sms)));
-    csr_spmm_kernel<NQ><<<blocks, threads, 0, st>>>(a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha, beta, a.heavy.thr,
-                                                    a.heavy.nseg, a.heavy.seg, partial);
+    launch_pdl(csr_spmm_kernel<NQ>, dim3(blocks), dim3(threads), 0, st, a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha,
+               beta, a.heavy.thr, a.heavy.nseg, static_cast<const std::int64_t*>(a.heavy.seg), partial);
     QB_LAUNCH_CHECK();
     if (a.heavy.nseg > 0) {
         csr_heavy_combine_kernel<<<static_cast<int>(std::min<std::int64_t>(a.heavy.nrows, 65535)), 128, 0, st>>>(
