@@ -843,9 +843,12 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
     const std::int64_t ldom = even(nb_batch * bmax);
     DBuf om(static_cast<std::size_t>(n) * ldom, c.st);
     std::int64_t batch_first = -1, batch_cols = 0;  // draw offset (in blocks) and width of the current batch
-    DBuf y(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * bpad, c.st);
+    // Y and Z rows padded to a multiple of 4 doubles: every CSR gather of one of their rows then
+    // starts on a 32-byte L2 sector (w = 50: 13 sectors per row instead of 13.5 on average)
+    const std::int64_t lyz = round_up(bpad, 4);
+    DBuf y(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * lyz, c.st);
     DBuf tmp(static_cast<std::size_t>(std::max<std::int64_t>(std::max<std::int64_t>(m, n), 1)) * bpad, c.st);
-    DBuf z(p.power > 0 ? static_cast<std::size_t>(n) * bpad : 0, c.st);
+    DBuf z(p.power > 0 ? static_cast<std::size_t>(n) * lyz : 0, c.st);
     DBuf mbuf(static_cast<std::size_t>(std::max<std::int64_t>(cap, 1)) * bpad, c.st);
     double e_host = norm_a_sq;
     while (true) {
@@ -862,7 +865,7 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             gaussian_fill(c.st, c.rng, p.seed, p.stream, static_cast<std::uint64_t>(g_used), all);  // step 4
         }
         MatView omv{om.p + (jblk - batch_first) * bmax, n, bi, ldom, true};
-        MatView yv{y.p, m, bi, bi, true};
+        MatView yv{y.p, m, bi, lyz, true};
         MatView mv{mbuf.p, s.k, bi, bi, true};
         int d = 0, keep = 0;
         bool met = false;
@@ -880,7 +883,7 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             // per-block power iteration with deflation at every application
             for (std::int64_t it = 0; it < p.power; ++it) {
                 eng.orth_block(yv, yv, kR1, kR1inv, sharded, tmp, false);
-                MatView zv{z.p, n, bi, bi, true};
+                MatView zv{z.p, n, bi, lyz, true};
                 eng.apply_t(yv, zv); a.passes += 1;
                 if (s.k > 0) {
                     eng.gemm(1.0, s.qk().t(), yv, 0.0, mv);
