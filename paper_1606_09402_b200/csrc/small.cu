@@ -857,6 +857,7 @@ __device__ __forceinline__ void panel_mark(int slot) {
 
 template <int BP>
 __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArgs p) {
+    pdl_wait();
     using C = PanelCfg<BP>;
     extern __shared__ __align__(16) double psm[];
     double* ys2 = psm;                              // STAGES sub-tile buffers (SUB x LD)
@@ -1541,8 +1542,21 @@ void launch_cholqr2_panel(cudaStream_t st, PanelArgs& a, int grid_cap) {
         if (per_sm < 1) throw QbError(kError, "cholqr2_panel: kernel does not fit on an SM");
     }
     const int grid = std::max(1, std::min(std::min(a.nsub, grid_cap), per_sm * gemm_num_sms()));
-    void* args[] = {&a};
-    QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, kCholThreads, args, C::SMEM, st));
+    // cooperative + programmatic stream serialization: the panel's CTAs may become resident while the
+    // previous kernel drains (the kernel waits on griddepcontrol before touching memory)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kCholThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    QB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     QB_LAUNCH_CHECK();
 }
 
