@@ -823,24 +823,40 @@ __device__ __forceinline__ void panel_trmm(const double* ys, const double* rs, d
     const int nb8 = (b + 7) >> 3, kmax = (b + 3) & ~3;
     const double* a0p = ys + (16 * mi + g) * C::LD + t;
     const double* a1p = a0p + 8 * C::LD;
+    // fragments in pairs (n-blocks h + NG j and h + NG (j+1)): over the shorter triangular k range
+    // both share the A-fragment loads (4 shared loads per 2 DMMAs instead of 6), the longer one
+    // then continues alone; every accumulation runs in ascending k (deterministic)
 #pragma unroll
-    for (int j = 0; j < C::MAXT; ++j) {
-        const int ni = h + C::NG * j;
+    for (int jp = 0; jp < C::MAXT; jp += 2) {
+        const int ni0 = h + C::NG * jp, ni1 = h + C::NG * (jp + 1);
+        const bool v1 = (jp + 1 < C::MAXT) && ni1 < nb8;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) out[j][e] = 0.0;
-        if (ni >= nb8) continue;  // warp-uniform
-        // 8 ni + 8 is a multiple of 8: two chains of k4 steps, at most one odd step at kmax
-        const int kend = min(kmax, 8 * ni + 8);
-        const double* bp = rs + t * C::LD + 8 * ni + g;
-        double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
-        int kk = 0;
-        for (; kk + 8 <= kend; kk += 8) {
-            dmma_16x8x4(acc0, a0p[kk], a1p[kk], bp[kk * C::LD]);
-            dmma_16x8x4(acc1, a0p[kk + 4], a1p[kk + 4], bp[(kk + 4) * C::LD]);
+        for (int e = 0; e < 4; ++e) {
+            out[jp][e] = 0.0;
+            if (jp + 1 < C::MAXT) out[jp + 1][e] = 0.0;
         }
-        if (kk < kend) dmma_16x8x4(acc0, a0p[kk], a1p[kk], bp[kk * C::LD]);
+        if (ni0 >= nb8) continue;  // warp-uniform; ni1 > ni0 is then invalid too
+        const int kend0 = min(kmax, 8 * ni0 + 8);
+        const double* bp0 = rs + t * C::LD + 8 * ni0 + g;
+        double acc0[4] = {0.0, 0.0, 0.0, 0.0};
+        if (v1) {
+            const int kend1 = min(kmax, 8 * ni1 + 8);
+            const double* bp1 = rs + t * C::LD + 8 * ni1 + g;
+            double acc1[4] = {0.0, 0.0, 0.0, 0.0};
+            int kk = 0;
+            for (; kk < kend0; kk += 4) {
+                const double x0 = a0p[kk], x1 = a1p[kk];
+                dmma_16x8x4(acc0, x0, x1, bp0[kk * C::LD]);
+                dmma_16x8x4(acc1, x0, x1, bp1[kk * C::LD]);
+            }
+            for (; kk < kend1; kk += 4) dmma_16x8x4(acc1, a0p[kk], a1p[kk], bp1[kk * C::LD]);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) out[j][e] = acc0[e] + acc1[e];
+            for (int e = 0; e < 4; ++e) out[jp + 1][e] = acc1[e];
+        } else {
+            for (int kk = 0; kk < kend0; kk += 4) dmma_16x8x4(acc0, a0p[kk], a1p[kk], bp0[kk * C::LD]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) out[jp][e] = acc0[e];
     }
 }
 
