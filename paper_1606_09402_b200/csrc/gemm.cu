@@ -450,6 +450,11 @@ bool aligned16(const MatView& v) {
 
 }  // namespace
 
+void make_tensor_map_2d(void* map, const double* base, std::int64_t inner, std::int64_t outer, std::int64_t ld,
+                        int box0, int box1) {
+    make_tmap(reinterpret_cast<CUtensorMap*>(map), base, inner, outer, ld, box0, box1);
+}
+
 void make_tensor_map_rows(void* map, const double* base, std::int64_t rows, int w, std::int64_t ld) {
     // one row of w doubles per box (tile::gather4 requires box height 1)
     make_tmap(reinterpret_cast<CUtensorMap*>(map), base, w, rows, ld, w, 1);

@@ -38,6 +38,10 @@ int gemm_num_sms();
 // 2-D tensor map over a row-major rows x w FP64 matrix (leading dimension ld), box = one row
 // (for TMA tile::gather4); `map` points to a 64-byte aligned CUtensorMap.
 void make_tensor_map_rows(void* map, const double* base, std::int64_t rows, int w, std::int64_t ld);
+// 2-D tensor map over a row-major outer x inner FP64 matrix (row stride ld), box box0 x box1 elements;
+// elements outside the matrix are zero-filled by the TMA unit.
+void make_tensor_map_2d(void* map, const double* base, std::int64_t inner, std::int64_t outer, std::int64_t ld,
+                        int box0, int box1);
 
 // C = alpha * A * B + beta * C, all FP64 views in device memory (any layouts).
 // beta == 0 never reads C. Deterministic (fixed split-K reduction order).

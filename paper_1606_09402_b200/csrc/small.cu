@@ -10,6 +10,7 @@
 // are bitwise reproducible.
 
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -716,6 +717,9 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
 }
 
 struct PanelArgs {
+    CUtensorMap tm_y;   // Y as rows x b (row stride ldy), box {BP + 4, SUB}: one TMA per sub-tile
+    CUtensorMap tm_t1;  // T1 as rows x b (row stride b)
+    int use_tm_y, use_tm_t1;
     const double* y;
     std::int64_t ldy;
     double* t1;  // rows x b, ld b
@@ -872,10 +876,10 @@ __device__ __forceinline__ void panel_mark(int slot) {
 }
 
 template <int BP>
-__global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArgs p) {
+__global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __grid_constant__ PanelArgs p) {
     pdl_wait();
     using C = PanelCfg<BP>;
-    extern __shared__ __align__(16) double psm[];
+    extern __shared__ __align__(128) double psm[];
     double* ys2 = psm;                              // STAGES sub-tile buffers (SUB x LD)
     double* rs = psm + C::STAGES * C::SUB * C::LD;  // BP x LD triangular factor
     __shared__ __align__(8) std::uint64_t full[C::STAGES], empty[C::STAGES];
@@ -972,7 +976,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
     // 16-byte aligned), warps 0-7 consume; the ring position persists across the phases.
     int ring_stage = 0;
     unsigned ring_phase = 0;
-    auto sub_loop = [&](const double* src, std::int64_t ld, auto&& body) {
+    auto sub_loop = [&](const double* src, std::int64_t ld, const CUtensorMap* tm, auto&& body) {
         const bool bulk = (ld % 2 == 0) && (p.b % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(src) & 15) == 0);
         if (cta == 0) zero_pad();  // the Cholesky used the ring as its workspace
         pb_fence_async();  // generic shared writes of the previous phase before async-proxy copies
@@ -983,7 +987,20 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
                 double* buf = ys2 + ring_stage * C::SUB * C::LD;
                 const std::int64_t r0 = static_cast<std::int64_t>(sub) * C::SUB;
                 const int nr = static_cast<int>(min(static_cast<std::int64_t>(C::SUB), p.rows - r0));
-                if (bulk) {
+                if (tm) {
+                    // one 2-D tensor TMA lands the padded sub-tile; columns >= b and rows past the
+                    // end are zero-filled by the TMA unit (the full box counts toward the tx bytes)
+                    if (lane == 0) {
+                        pb_arrive_tx(&full[ring_stage], static_cast<unsigned>(C::SUB * C::LD * 8));
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+                                sm_addr(buf)),
+                            "l"(reinterpret_cast<std::uint64_t>(tm)), "r"(0), "r"(static_cast<int>(r0)),
+                            "r"(sm_addr(&full[ring_stage]))
+                            : "memory");
+                    }
+                    __syncwarp();
+                } else if (bulk) {
                     if (nr < C::SUB) {  // rows past the end: zero (stale data of an earlier sub-tile)
                         for (int idx = lane; idx < (C::SUB - nr) * BP; idx += 32)
                             buf[(nr + idx / BP) * C::LD + idx % BP] = 0.0;
@@ -1019,7 +1036,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
     // ---- phase A: Gram of Y
     panel_mark(0);
     zero_acc();
-    sub_loop(p.y, p.ldy, [&](double* cur, std::int64_t) {
+    sub_loop(p.y, p.ldy, p.use_tm_y ? &p.tm_y : nullptr, [&](double* cur, std::int64_t) {
         if (mma_warp) panel_gram<BP>(cur, acc, fm, fn, nvf);
     });
     panel_mark(1);
@@ -1040,7 +1057,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
     const bool one_pass = __ldcg(&p.st0->gram_dev) <= kFirstOrderDev && __ldcg(&p.st0->breakdown) == 0;
     if (one_pass) {
         stage_r(p.rainv);
-        sub_loop(p.y, p.ldy, [&](double* cur, std::int64_t r0) {
+        sub_loop(p.y, p.ldy, p.use_tm_y ? &p.tm_y : nullptr, [&](double* cur, std::int64_t r0) {
             if (mma_warp) {
                 double tacc[C::MAXT][4];
                 panel_trmm<BP>(cur, rs, tacc, p.b);
@@ -1074,7 +1091,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
     // ---- phase B: T1 = Y Ra^{-1} (written out) and the Gram of T1
     stage_r(p.rainv);
     zero_acc();
-    sub_loop(p.y, p.ldy, [&](double* cur, std::int64_t r0) {
+    sub_loop(p.y, p.ldy, p.use_tm_y ? &p.tm_y : nullptr, [&](double* cur, std::int64_t r0) {
         double tacc[C::MAXT][4];
         if (mma_warp) panel_trmm<BP>(cur, rs, tacc, p.b);
         consumer_sync();
@@ -1105,7 +1122,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(PanelArg
     panel_mark(9);
     // ---- phase D: Q = T1 Rb^{-1}
     stage_r(p.rbinv);
-    sub_loop(p.t1, p.b, [&](double* cur, std::int64_t r0) {
+    sub_loop(p.t1, p.b, p.use_tm_t1 ? &p.tm_t1 : nullptr, [&](double* cur, std::int64_t r0) {
         if (mma_warp) {
             double tacc[C::MAXT][4];
             panel_trmm<BP>(cur, rs, tacc, p.b);
@@ -1558,6 +1575,23 @@ void launch_cholqr2_panel(cudaStream_t st, PanelArgs& a, int grid_cap) {
         if (per_sm < 1) throw QbError(kError, "cholqr2_panel: kernel does not fit on an SM");
     }
     const int grid = std::max(1, std::min(std::min(a.nsub, grid_cap), per_sm * gemm_num_sms()));
+    static const bool tm_on = [] {
+        const char* e = std::getenv("QBFAC_PANEL_TM");
+        return !(e && e[0] == '0');
+    }();
+    a.use_tm_y = a.use_tm_t1 = 0;
+    // tensor-map sub-tiles measured faster for BP <= 64 (1e5 x 50: Gram 26.6 -> 15.9 us) and slower
+    // for the 32-row sub-tiles of BP >= 96 (2e6 x 100: 4.13 -> 4.33 ms), which keep the row copies
+    if (tm_on && BP <= 64 && a.rows > 0) {
+        if (a.ldy % 2 == 0 && (reinterpret_cast<std::uintptr_t>(a.y) & 15) == 0) {
+            make_tensor_map_2d(&a.tm_y, a.y, a.b, a.rows, a.ldy, C::LD, C::SUB);
+            a.use_tm_y = 1;
+        }
+        if (a.b % 2 == 0 && (reinterpret_cast<std::uintptr_t>(a.t1) & 15) == 0) {
+            make_tensor_map_2d(&a.tm_t1, a.t1, a.b, a.rows, a.b, C::LD, C::SUB);
+            a.use_tm_t1 = 1;
+        }
+    }
     // cooperative + programmatic stream serialization: the panel's CTAs may become resident while the
     // previous kernel drains (the kernel waits on griddepcontrol before touching memory)
     cudaLaunchConfig_t cfg = {};
