@@ -1580,9 +1580,9 @@ void launch_cholqr2_panel(cudaStream_t st, PanelArgs& a, int grid_cap) {
         return !(e && e[0] == '0');
     }();
     a.use_tm_y = a.use_tm_t1 = 0;
-    // tensor-map sub-tiles measured faster for BP <= 64 (1e5 x 50: Gram 26.6 -> 15.9 us) and slower
-    // for the 32-row sub-tiles of BP >= 96 (2e6 x 100: 4.13 -> 4.33 ms), which keep the row copies
-    if (tm_on && BP <= 64 && a.rows > 0) {
+    // tensor-map sub-tiles (same-box A/B against the bulk row copies): 1e5 x 50 Gram 26.6 -> 15.9 us,
+    // 2e6 x 100 panel 4.41 -> 4.33 ms
+    if (tm_on && a.rows > 0) {
         if (a.ldy % 2 == 0 && (reinterpret_cast<std::uintptr_t>(a.y) & 15) == 0) {
             make_tensor_map_2d(&a.tm_y, a.y, a.b, a.rows, a.ldy, C::LD, C::SUB);
             a.use_tm_y = 1;
