@@ -50,6 +50,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 }
 
 __global__ void scale_kernel(MatView c, double beta) {
+    pdl_wait();
     const std::int64_t total = c.rows * c.cols;
     for (std::int64_t idx = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
          idx < total; idx += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
@@ -62,6 +63,7 @@ __global__ void scale_kernel(MatView c, double beta) {
 }
 
 __global__ void copy_kernel(MatView s, MatView d) {
+    pdl_wait();
     const std::int64_t total = s.rows * s.cols;
     for (std::int64_t idx = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
          idx < total; idx += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
@@ -73,6 +75,7 @@ __global__ void copy_kernel(MatView s, MatView d) {
 }
 
 __global__ void add_kernel(MatView s, MatView d, double alpha) {
+    pdl_wait();
     const std::int64_t total = s.rows * s.cols;
     for (std::int64_t idx = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
          idx < total; idx += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
@@ -1225,6 +1228,7 @@ struct TrmmPair {
 };
 
 __global__ void __launch_bounds__(1024) trmm_upper_kernel(TrmmPair prm, int n, std::int64_t ld) {
+    pdl_wait();
     extern __shared__ double sm[];
     const int z = blockIdx.x;
     const double* __restrict__ a = prm.a[z];
@@ -1449,21 +1453,21 @@ int grid_for(std::int64_t total, int threads) {
 
 void scale_matrix(cudaStream_t st, const MatView& c, double beta) {
     if (c.rows * c.cols == 0) return;
-    scale_kernel<<<grid_for(c.rows * c.cols, 256), 256, 0, st>>>(c, beta);
+    launch_pdl(scale_kernel, dim3(grid_for(c.rows * c.cols, 256)), dim3(256), 0, st, c, beta);
     QB_LAUNCH_CHECK();
 }
 
 void copy_matrix(cudaStream_t st, const MatView& s, const MatView& d) {
     if (s.rows != d.rows || s.cols != d.cols) throw QbError(kDimensionError, "copy_matrix: shape");
     if (s.rows * s.cols == 0) return;
-    copy_kernel<<<grid_for(s.rows * s.cols, 256), 256, 0, st>>>(s, d);
+    launch_pdl(copy_kernel, dim3(grid_for(s.rows * s.cols, 256)), dim3(256), 0, st, s, d);
     QB_LAUNCH_CHECK();
 }
 
 void add_matrix(cudaStream_t st, const MatView& s, const MatView& d, double alpha) {
     if (s.rows != d.rows || s.cols != d.cols) throw QbError(kDimensionError, "add_matrix: shape");
     if (s.rows * s.cols == 0) return;
-    add_kernel<<<grid_for(s.rows * s.cols, 256), 256, 0, st>>>(s, d, alpha);
+    launch_pdl(add_kernel, dim3(grid_for(s.rows * s.cols, 256)), dim3(256), 0, st, s, d, alpha);
     QB_LAUNCH_CHECK();
 }
 
@@ -1676,7 +1680,7 @@ void trmm_upper_pair(cudaStream_t st, const double* a0, const double* b0, double
     }
     TrmmPair p{{a0, a1}, {b0, b1}, {c0, c1}};
     const int smem = 2 * n * (n + 1) * static_cast<int>(sizeof(double));
-    trmm_upper_kernel<<<c1 ? 2 : 1, 1024, smem, st>>>(p, n, ld);
+    launch_pdl(trmm_upper_kernel, dim3(c1 ? 2 : 1), dim3(1024), static_cast<std::size_t>(smem), st, p, n, ld);
     QB_LAUNCH_CHECK();
 }
 
