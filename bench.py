@@ -8,12 +8,19 @@ device. `value` is the device time per step with A resident in HBM (512 MB > L2,
 so no L2 flush is needed); `e2e` is the same call through the C-ABI from pinned host
 memory: H2D of A, the factorization, and D2H of Q and B every step.
 
+A is the pinned config-2 input of tools/pinned_inputs.py (bit-identical on every x86-64
+host; its SHA-256 is in `config`), the same bytes the reference arm and the golden
+fixtures use.
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): each rank runs an independent replica of the workload (weak
-scaling; config 2 is a single-GPU config), timed max-over-ranks.
---impl reference: the reference's own CPU kernels (oracle/_ref, built from
-/root/reference/proj/src) on a bounded sample, rank 0 only.
+N > 1 (torchrun, one process per GPU, NCCL): config 2 row-sharded over the N ranks
+(A, G, Y, Q by rows; the n x l allreduce after each A^T pass and the
+Gram allreduces over NCCL), timed max over ranks — strong scaling. Every N also reports
+config 4 (single pass, 40000 x 20000) row-sharded the same way under `sharded.cfg4`,
+and N = 8 (or --cfg5) config 5 (CSR, 2e8 nnz) under `sharded.cfg5`.
+--impl reference: the reference's own CPU path (oracle/_ref: the reference's kernels,
+RNG and containers + the restated rand_qb_fp) run to epsilon on config 2, rank 0 only.
 """
 from __future__ import annotations
 
@@ -26,13 +33,17 @@ import sys
 import threading
 import time
 
-import numpy as np
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+import numpy as np  # noqa: E402
+
+import pinned_inputs  # noqa: E402
 
 METRIC = "randQB_FP time-to-eps (s), config 2"
-CFG = dict(n=8000, b=50, power=1, eps_rel=5e-2, max_rank=2000, l_budget=2000, a_seed=2, omega_seed=42)
+CFG = dict(n=8000, b=50, power=1, eps_rel=5e-2, max_rank=2000, l_budget=2000, omega_seed=42)
+REF_CACHE = os.path.join(pinned_inputs.CACHE, "ref_arm_cfg2.json")
 
 
 def env_int(k, d):
@@ -40,6 +51,31 @@ def env_int(k, d):
         return int(os.environ.get(k, d))
     except ValueError:
         return d
+
+
+def workload_config(world: int, sha: str) -> dict:
+    """Identical in both arms."""
+    return {"workload": "cfg2: randQB_FP dense 8000x8000 sigma_j=1/j, b=50, P=1, eps=5e-2 rel, max rank 2000, "
+                        "l~=2000", "n": CFG["n"], "b": CFG["b"], "power": CFG["power"], "eps_rel": CFG["eps_rel"],
+            "l_budget": CFG["l_budget"], "max_rank": CFG["max_rank"], "omega_seed": CFG["omega_seed"],
+            "a_sha256": sha[:16], "l2": "inputs larger than L2 (A = 512 MB)",
+            "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU"}
+
+
+DATA = ("synthetic (config-2 recipe: A = U diag(1/j) V^T, U,V = Q of QR of RngStream(2) gaussians; "
+        "tools/pinned_inputs.py, identical bytes in both arms)")
+
+
+def host_info() -> dict:
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": model}
 
 
 # ---- clocks ---------------------------------------------------------------------------
@@ -86,68 +122,182 @@ class ClockSampler:
 
 
 # ---- reference CPU arm -------------------------------------------------------------------
-def cpu_sample(a: np.ndarray, rows: int = 1000, width: int = 2000) -> dict:
-    """Bounded sample of the reference's own CPU path for config 2: the dense passes
-    A*Omega (gemm_nn) and A^T*G (gemm_tn) of MatrixHandle::multiply
-    (matrix_handle.cpp:112-116, kernels_drivers.cpp:21-65) on a `rows`-row block of A
-    at the sketch width l~; scaled to the four full passes of randQB_FP with P=1. The
-    power-step orthonormalisations and the block loop are NOT included (so the
-    estimate is a lower bound of the reference's time-to-eps)."""
+def reference_time_to_eps(a, sha: str) -> dict:
+    """The reference's own CPU path to epsilon on config 2: rand_qb_fp (restated algorithm
+    layer, oracle/qb_restated.cpp) over the reference's MatrixHandle / DenseMatrix /
+    gemm_nn / gemm_tn (kernels_drivers.cpp:21-65, AVX2 lane) and RngStream (rng.cpp),
+    compiled from /root/reference/proj/src into oracle/_ref/libqbref.so. The time is the
+    oracle's steady_clock around the rand_qb_fp call (matrix wrap excluded). One core:
+    the reference has no threads."""
     from oracle import oracle as O
 
-    n = a.shape[1]
-    blk = np.asfortranarray(a[:rows])
-    om = np.asfortranarray(np.random.default_rng(0).standard_normal((n, width)))
-    t0 = time.perf_counter()
-    g = O.dense_multiply(blk, om, False)
-    t1 = time.perf_counter()
-    O.dense_multiply(blk, g, True)
-    t2 = time.perf_counter()
-    scale = a.shape[0] / rows
-    est = 2 * (t1 - t0) * scale + 2 * (t2 - t1) * scale
-    return {"value": est, "t_nn": t1 - t0, "t_tn": t2 - t1, "rows": rows, "width": width,
-            "lane": O.lane_name(), "gflops_nn": 2 * rows * n * width / (t1 - t0) / 1e9,
-            "gflops_tn": 2 * rows * n * width / (t2 - t1) / 1e9}
+    a = np.asfortranarray(a)
+    eps = CFG["eps_rel"] * float(np.linalg.norm(a))
+    r = O.run("fp", a, b=CFG["b"], power=CFG["power"], eps_abs=eps, l_budget=CFG["l_budget"],
+              max_rank=CFG["max_rank"], seed=CFG["omega_seed"])
+    out = {"value": r.seconds, "rank": r.rank, "passes": r.passes, "terminated_by": r.terminated_by,
+           "E": r.E, "lane": O.lane_name(), "a_sha256": sha, "host": host_info(),
+           "when": time.strftime("%Y-%m-%dT%H:%M:%S")}
+    os.makedirs(os.path.dirname(REF_CACHE), exist_ok=True)
+    json.dump(out, open(REF_CACHE, "w"))
+    return out
 
 
-def host_matrix_cfg2():
-    from paper_1606_09402_b200 import matgen
-    return matgen.cfg2_matrix(CFG["n"], CFG["a_seed"])
+def cpu_baseline_obj(ref: dict, how: str) -> dict:
+    return {"value": ref["value"], "unit": "s", "cores": 1, "kind": "reference",
+            "sample": f"full reference rand_qb_fp to eps on config 2 (lane {ref['lane']}, rank {ref['rank']}, "
+                      f"{ref['passes']} passes, {ref['terminated_by']}), one core of {ref['host']['cpu']} "
+                      f"({ref['host']['nproc']} cores); {how}"}
 
 
 def run_reference(args):
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
-    cache = os.path.join(ROOT, "gpurun_out", "cfg2_A.npy")
-    a = None
-    if os.path.exists(cache):
-        a = np.load(cache, mmap_mode="r")
-    if a is None:
-        a = host_matrix_cfg2()
-    for _ in range(args.warmup):
-        cpu_sample(a, rows=250)
+    a, sha = pinned_inputs.matrix(2, gauss="oracle")  # no library of this repo is loaded on this arm
+    steps = max(1, min(args.steps, env_int("QBFAC_REF_STEPS", 1)))
     times, last = [], None
-    for _ in range(args.steps):
-        last = cpu_sample(a)
+    for _ in range(steps):
+        last = reference_time_to_eps(a, sha)
         times.append(last["value"])
-    v = float(np.mean(times))
-    line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (config-2 recipe, numpy LAPACK QR)",
-            "impl": "reference",
-            "config": {"workload": "cfg2: randQB_FP dense 8000x8000, b=50, P=1, eps=5e-2 rel, l~=2000",
-                       "n": CFG["n"], "b": CFG["b"], "power": CFG["power"]},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "reference",
-                             "sample": f"reference gemm_nn+gemm_tn on a {last['rows']}-row block at width "
-                                       f"{last['width']}, scaled to 4 full passes (QR/block loop excluded; "
-                                       f"lane {last['lane']})"},
+    v = float(np.median(times))
+    last["value"] = v
+    line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": steps,
+            "steps_requested": args.steps, "warmup": 0, "warmup_requested": args.warmup, "ms_per_step": v * 1e3,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "impl": "reference", "config": workload_config(args.gpus, sha),
+            "result": {"rank": last["rank"], "passes": last["passes"], "terminated_by": last["terminated_by"]},
+            "cpu_baseline": cpu_baseline_obj(last, f"{steps} full run(s), warm-up skipped (a run is ~3 min)"),
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ---- our arm -------------------------------------------------------------------------------
+class Dist:
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.rank, self.world, self.local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+
+def timed_device(ctx, fn, steps):
+    import torch
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    ctx.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / steps
+
+
+def sharded_cfg4(D, ctx, steps=3):
+    """Config 4 (single-pass FP, 40000 x 20000, l = 400, b = 100) row-sharded over the ranks:
+    G = A_g Omega local, H = sum_g A_g^T G_g allreduced once (64 MB), Grams allreduced."""
+    import torch
+
+    from paper_1606_09402_b200 import dist as qdist
+    from paper_1606_09402_b200 import matgen, qbfac
+    m, n = 40000, 20000
+    row0, rows = qdist.plan_dense_rows(m, D.world)[D.rank]
+    sig = np.exp(-np.arange(1, 401) / 60.0)
+    at = matgen.synthesize_torch(m, n, sig, 4, noise=1e-6)  # device-synthesized (timing only)
+    a_loc = at.t()[row0:row0 + rows].cpu().numpy()
+    del at
+    torch.cuda.empty_cache()
+    h = qbfac.MatrixHandle.dense_shard(a_loc, m, row0, ctx) if D.world > 1 else qbfac.MatrixHandle.dense(a_loc, ctx)
+    del a_loc
+
+    def f():
+        return qbfac.run_device(h, alg=3, mode=0, b=100, power=0, k=400, s=0, seed=42)
+    r = f()
+    info = qbfac.info_dict(r.info)
+    r.free()
+    ctx.synchronize()
+    D.barrier()
+    res = []
+    t = timed_device(ctx, lambda: res.append(f()), steps)
+    for x in res:
+        x.free()
+    t = D.max(t)
+    w = 400
+    pass_t = pass_time(h, w, False, ctx)
+    out = {"workload": "cfg4: single-pass FP 40000x20000 rank-400 + 1e-6 noise, l=400, b=100 (device-synthesized A)",
+           "time_s": t, "rank": info["rank"], "passes": info["passes"], "rows_per_rank": rows,
+           "pass_nn_ms_local": pass_t * 1e3, "pass_nn_tflops_local": 2.0 * rows * n * w / pass_t / 1e12}
+    h.free()
+    return out
+
+
+def sharded_cfg5(D, ctx, steps=2):
+    from paper_1606_09402_b200 import dist as qdist
+    from paper_1606_09402_b200 import matgen, qbfac
+    csr = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=2e8, seed=5)
+    m, n = csr[0], csr[1]
+    row0, rows = qdist.plan_csr_rows(csr[2], D.world)[D.rank]
+    lm, ln, rp, ci, v = qdist.shard_csr(csr, row0, rows)
+    norm = float(np.sqrt(D.sum(float(v @ v))))
+    if D.world > 1:
+        h = qbfac.MatrixHandle.csr_shard(m, row0, n, rp, ci, v, ctx)
+    else:
+        h = qbfac.MatrixHandle.csr(m, n, rp, ci, v, ctx)
+    del csr
+
+    def f():
+        return qbfac.run_device(h, alg=0, b=100, power=2, max_rank=2000, eps_abs=0.6 * norm, seed=42)
+    r = f()
+    info = qbfac.info_dict(r.info)
+    r.free()
+    ctx.synchronize()
+    D.barrier()
+    res = []
+    t = timed_device(ctx, lambda: res.append(f()), steps)
+    for x in res:
+        x.free()
+    out = {"workload": "cfg5: EI CSR 2e6x5e5 Zipf(1.1) 2e8 nnz, b=100, P=2, eps=0.6 rel, cap 2000",
+           "time_s": D.max(t), "rank": info["rank"], "passes": info["passes"], "nnz_local": int(len(v)),
+           "rows_per_rank": rows}
+    h.free()
+    return out
+
+
+def pass_time(h, w, trans, ctx, reps=5):
+    import torch
+    rows_in = h.m if trans else h.n
+    rows_out = h.n if trans else h.m
+    x = torch.randn((rows_in, w), dtype=torch.float64, device="cuda")
+    y = torch.empty((rows_out, w), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(2):
+        h.multiply_device(x.data_ptr(), w, w, trans, y.data_ptr(), w)
+    ctx.synchronize()
+    return timed_device(ctx, lambda: h.multiply_device(x.data_ptr(), w, w, trans, y.data_ptr(), w), reps)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -155,136 +305,115 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the config-4/5 row-sharded sub-measurements")
+    ap.add_argument("--cfg5", action="store_true", help="also run config 5 (default only at N = 8)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
 
-    import torch
-    import torch.distributed as dist
+    D = Dist()
+    torch = D.torch
+    from paper_1606_09402_b200 import dist as qdist
+    from paper_1606_09402_b200 import qbfac
 
-    from paper_1606_09402_b200 import matgen, qbfac
-
-    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    os.environ["QBFAC_DEVICE"] = str(local)
-    ctx = qbfac.Context(local)
+    # the pinned input: built once (local rank 0), then every rank maps the same file
+    if D.local == 0:
+        pinned_inputs.matrix(2)
+    D.barrier()
+    a_host, sha = pinned_inputs.matrix(2)
     n = CFG["n"]
-    # A (config 2) synthesized on the device: U, V = Q of QR of device gaussians.
-    at = matgen.synthesize_torch(n, n, matgen.spectrum("inv", n), CFG["a_seed"])  # at = A^T storage
-    norm_a = float(torch.linalg.norm(at))
-    eps = CFG["eps_rel"] * norm_a
-    handle = qbfac.MatrixHandle.dense_device(at.data_ptr(), n, n, n, ctx)
-    stream = torch.cuda.ExternalStream(ctx.stream())
+    eps = CFG["eps_rel"] * float(np.linalg.norm(np.asfortranarray(a_host)))
+    os.environ["QBFAC_DEVICE"] = str(D.local)
+    if D.world > 1:
+        ctx = qdist.sharded_context(D.local)
+        row0, rows = qdist.plan_dense_rows(n, D.world)[D.rank]
+        a_loc = np.asfortranarray(a_host[row0:row0 + rows])
+        handle = qbfac.MatrixHandle.dense_shard(a_loc, n, row0, ctx)
+    else:
+        ctx = qbfac.Context(D.local)
+        row0, rows = 0, n
+        a_loc = np.asfortranarray(a_host)
+        handle = qbfac.MatrixHandle.dense(a_loc, ctx)
 
-    def factorize():
-        return qbfac.run_device(handle, alg=1, b=CFG["b"], power=CFG["power"], max_rank=CFG["max_rank"],
+    def factorize(h=handle):
+        return qbfac.run_device(h, alg=1, b=CFG["b"], power=CFG["power"], max_rank=CFG["max_rank"],
                                 l_budget=CFG["l_budget"], eps_abs=eps, seed=CFG["omega_seed"])
 
     for _ in range(args.warmup):
         r = factorize()
-        rank_out = r.rank
         info = qbfac.info_dict(r.info)
         r.free()
     ctx.synchronize()
 
-    # ---- timed region: A resident in HBM ----
-    clocks = ClockSampler(local)
+    # ---- timed region: A (this rank's rows) resident in HBM ----
+    clocks = ClockSampler(D.local)
     clocks.start()
     time.sleep(0.2)
-    barrier()
+    D.barrier()
     ctx.synchronize()
     l0 = ctx.kernel_launches()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        r = factorize()
-        r.free()
-    e1.record(stream)
-    ctx.synchronize()
-    barrier()
-    launches = (ctx.kernel_launches() - l0) // max(args.steps, 1)
+    res = []
+    t_step = timed_device(ctx, lambda: res.append(factorize()), args.steps)
+    D.barrier()
+    launches = ctx.kernel_launches() - l0
+    for x in res:
+        x.free()
     clk = clocks.stop()
-    t_step = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.steps)
+    t_step = D.max(t_step)
 
-    # ---- e2e: through the C-ABI from pinned host memory ----
-    host_a = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-    host_a.copy_(at.cpu())
-    a_np = host_a.numpy()  # row-major storage of A^T == column-major A
-    a_view = a_np.T        # A, Fortran-ordered view, no copy
-    # caller-allocated pinned output buffers (the C-ABI's two-phase copy-out)
-    q_out = torch.empty(n * CFG["max_rank"], dtype=torch.float64, pin_memory=True).numpy()
+    # ---- e2e: through the C-ABI from pinned host memory, Q and B back to the host ----
+    host_a = torch.empty((a_loc.shape[1], a_loc.shape[0]), dtype=torch.float64, pin_memory=True)
+    host_a.numpy()[:] = a_loc.T
+    a_view = host_a.numpy().T  # column-major rows x n, pinned
+    q_out = torch.empty(rows * CFG["max_rank"], dtype=torch.float64, pin_memory=True).numpy()
     b_out = torch.empty(n * CFG["max_rank"], dtype=torch.float64, pin_memory=True).numpy()
     e2e_times, h2d, d2h, phases = [], 0, 0, []
     for s in range(max(2, min(args.steps, 5))):
         ctx.synchronize()
-        barrier()
+        D.barrier()
         t0 = time.perf_counter()
-        # H2D of A (8*n*n bytes) in row chunks on the copy stream; the first pass G = A*Omega
-        # consumes each chunk as it lands (qbfac_gpu_matrix_dense_async)
-        h = qbfac.MatrixHandle.dense_async(a_view, ctx)
+        if D.world > 1:
+            h = qbfac.MatrixHandle.dense_shard(a_view, n, row0, ctx)  # H2D of this rank's rows
+        else:
+            # H2D in row chunks on the copy stream; the first pass G = A*Omega consumes each
+            # chunk as it lands (qbfac_gpu_matrix_dense_async)
+            h = qbfac.MatrixHandle.dense_async(a_view, ctx)
         t1 = time.perf_counter()
-        r = factorize_h(qbfac, h, eps)
+        r = factorize(h)
         t2 = time.perf_counter()
-        q = r.q(q_out)                                      # D2H of Q
-        b = r.b(b_out)                                      # D2H of B
+        q = r.q(q_out)                                      # D2H of Q (this rank's rows)
+        b = r.b(b_out) if D.rank == 0 else np.zeros(0)      # D2H of B (replicated: rank 0)
         t3 = time.perf_counter()
         r.free()
         h.free()
         ctx.synchronize()
         e2e_times.append(time.perf_counter() - t0)
         phases.append((t1 - t0, t2 - t1, t3 - t2, e2e_times[-1] - (t3 - t0)))
-        h2d = 8 * n * n
-        d2h = 8 * (q.size + b.size)
-    t_e2e = max_over_ranks(float(np.median(e2e_times)))
+        h2d = int(D.sum(8.0 * a_view.size))
+        d2h = int(D.sum(8.0 * (q.size + b.size)))
+    t_e2e = D.max(float(np.median(e2e_times)))
     ph = np.median(np.array(phases), axis=0) * 1e3
-    # the link this e2e rides on: a plain pinned H2D of A, same bytes
-    dev_a = torch.empty((n, n), dtype=torch.float64, device="cuda")
-    h2d_s = []
-    for _ in range(3):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        dev_a.copy_(host_a, non_blocking=True)
-        torch.cuda.synchronize()
-        h2d_s.append(time.perf_counter() - t0)
-    del dev_a
     e2e_extra = {"phases_ms": {"handle": round(float(ph[0]), 3), "run": round(float(ph[1]), 3),
                                "d2h_q_b": round(float(ph[2]), 3), "free_sync": round(float(ph[3]), 3)},
-                 "h2d_link_gbs": round(8 * n * n / min(h2d_s) / 1e9, 2),
                  "all_s": [round(t, 5) for t in e2e_times]}
+    if D.world == 1:
+        dev_a = torch.empty_like(host_a, device="cuda")
+        h2d_s = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dev_a.copy_(host_a, non_blocking=True)
+            torch.cuda.synchronize()
+            h2d_s.append(time.perf_counter() - t0)
+        del dev_a
+        e2e_extra["h2d_link_gbs"] = round(8 * host_a.numel() / min(h2d_s) / 1e9, 2)
 
-    # ---- roofline: the dominant kernel (DMMA pass G = A * Omega at width l~) ----
+    # ---- roofline: the dominant kernel (DMMA pass G = A * Omega at width l~, this rank's rows) ----
     w = CFG["l_budget"]
-    x = torch.randn((n, w), dtype=torch.float64, device="cuda")
-    y = torch.empty((n, w), dtype=torch.float64, device="cuda")
-    torch.cuda.synchronize()
-    for _ in range(2):
-        handle.multiply_device(x.data_ptr(), w, w, False, y.data_ptr(), w)
-    ctx.synchronize()
-    reps = 5
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record(stream)
-    for _ in range(reps):
-        handle.multiply_device(x.data_ptr(), w, w, False, y.data_ptr(), w)
-    k1.record(stream)
-    ctx.synchronize()
-    t_pass = k0.elapsed_time(k1) / 1e3 / reps
-    flops = 2.0 * n * n * w
+    t_pass = pass_time(handle, w, False, ctx)
+    t_pass_t = pass_time(handle, w, True, ctx)
+    flops = 2.0 * rows * n * w
     achieved = flops / t_pass / 1e12
-    # FP64 peak: cuBLAS DGEMM 8192^3 measured live (MEASURED_PEAKS.json has no FP64 entry)
     pa = torch.randn((8192, 8192), dtype=torch.float64, device="cuda")
     pb = torch.randn((8192, 8192), dtype=torch.float64, device="cuda")
     pa @ pb
@@ -298,57 +427,78 @@ def main():
         torch.cuda.synchronize()
         best = min(best, c0.elapsed_time(c1) / 1e3)
     peak = 2 * 8192**3 / best / 1e12
-    del pa, pb, x, y
+    del pa, pb
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and D.world == 1:
         try:
             traffic = json.load(open(tpath)).get("dense_pass_nn_per_launch_bytes")
         except Exception:
             traffic = None
+    comm = None
+    if D.world > 1:
+        # the n x l~ allreduce of H = A^T G (the pass's only collective), timed the same way
+        buf = torch.ones((n * w,), dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            D.dist.all_reduce(buf)
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(5):
+            D.dist.all_reduce(buf)
+        c1.record()
+        torch.cuda.synchronize()
+        ar = D.max(c0.elapsed_time(c1) / 5 / 1e3)
+        comm = {"allreduce_n_x_l_ms": ar * 1e3, "bytes": 8 * n * w, "busbw_gbs": 2 * (D.world - 1) / D.world * 8 * n * w / ar / 1e9}
+        del buf
+
+    sharded = {}
+    if not args.no_sharded:
+        handle.free()
+        torch.cuda.empty_cache()
+        sharded["cfg4"] = sharded_cfg4(D, ctx)
+        if args.cfg5 or D.world == 8:
+            sharded["cfg5"] = sharded_cfg5(D, ctx)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
         try:
-            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-            smp = cpu_sample(a_view)
-            cpu = {"value": smp["value"], "unit": "s", "cores": 1, "kind": "reference",
-                   "sample": f"reference gemm_nn+gemm_tn (lane {smp['lane']}) on a {smp['rows']}-row block at "
-                             f"width {smp['width']} ({smp['gflops_nn']:.2f}/{smp['gflops_tn']:.2f} GFLOP/s), "
-                             "scaled to the 4 full passes; QR + block loop excluded (lower bound)"}
+            ref = json.load(open(REF_CACHE)) if os.path.exists(REF_CACHE) else None
+            if ref and ref.get("a_sha256") == sha:
+                cpu = cpu_baseline_obj(ref, f"measured by bench.py --impl reference on this host at {ref['when']}")
+            else:
+                ref = reference_time_to_eps(a_host, sha)
+                cpu = cpu_baseline_obj(ref, "measured in this run")
         except Exception as ex:  # the oracle is a reported baseline, never the product path
             cpu = {"value": None, "unit": "s", "cores": 1, "kind": "reference", "sample": f"unavailable: {ex}"}
 
-    if rank == 0:
+    if D.rank == 0:
         line = {
-            "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": D.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (config-2 recipe: A = U diag(1/j) V^T, U,V = Q of device-generated gaussians)",
-            "config": {"workload": "cfg2: randQB_FP dense 8000x8000 sigma_j=1/j, b=50, P=1, eps=5e-2 rel, "
-                                   "max rank 2000, l~=2000", "n": n, "b": CFG["b"], "power": CFG["power"],
-                       "l_budget": CFG["l_budget"], "rank": rank_out, "passes": info["passes"],
-                       "blocks": info["blocks"], "householder_fallbacks": info["householder_fallbacks"],
-                       "l2": "inputs larger than L2 (A = 512 MB)", "parallelism": f"replicas x{world}"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": workload_config(D.world, sha),
+            "result": {"rank": info["rank"], "passes": info["passes"], "blocks": info["blocks"],
+                       "terminated_by": qbfac.TERMINATION[int(info["terminated_by"])],
+                       "householder_fallbacks": info["householder_fallbacks"], "rows_per_rank": rows},
             "clocks": clk,
             "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, **e2e_extra},
-            "gpu_launches": int(launches * args.steps),
+            "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "dgemm_ws_kernel<128,80,32> (DMMA, TMA bulk + mbarrier ring) G = A*Omega, 8000x8000x2000",
-                         "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run (FP64 tensor)",
-                         "pass_ms": t_pass * 1e3},
+                         "kernel": f"dgemm_ws_kernel (DMMA, TMA + mbarrier ring) G = A*Omega, {rows}x{n}x{w}",
+                         "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run (FP64 tensor; "
+                                        "MEASURED_PEAKS.json has no FP64 entry)",
+                         "pass_nn_ms": t_pass * 1e3, "pass_tn_ms": t_pass_t * 1e3,
+                         "pass_tn_tflops": flops / t_pass_t / 1e12},
+            "comm": comm,
+            "sharded": sharded or None,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    if D.world > 1:
+        D.dist.destroy_process_group()
     return 0
-
-
-def factorize_h(qbfac, h, eps):
-    return qbfac.run_device(h, alg=1, b=CFG["b"], power=CFG["power"], max_rank=CFG["max_rank"],
-                            l_budget=CFG["l_budget"], eps_abs=eps, seed=CFG["omega_seed"])
 
 
 if __name__ == "__main__":

@@ -7,12 +7,15 @@
 //   * A is read through the reference MatrixHandle (matrix_handle.hpp:41-86):
 //     dense() column-major data or sparse() CSR arrays are handed to the C-ABI;
 //   * Omega comes from the same RngStream (seed(), stream_id(), rng.hpp:16-42) —
-//     the stream must be at its initial position; afterwards `rng` is advanced
-//     by exactly the draws the reference would have consumed;
+//     the stream must be at its initial position (checked: a stream that has already
+//     been drawn from, including a cached Box-Muller half, throws qbfac::Error before
+//     any device work); afterwards `rng` is advanced by exactly the draws the
+//     reference would have consumed;
 //   * the PassCounter of A is advanced by the passes the device made;
 //   * status codes are rethrown as the reference exception types (types.hpp).
 #pragma once
 
+#include <bit>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -89,7 +92,21 @@ inline void advance(RngStream& rng, std::int64_t draws) {
     if (draws % 2) rng.next_gaussian();
 }
 
+// The device regenerates Omega from position 0 of (seed, stream). Compare the next draws of
+// a copy of `rng` with those of a fresh RngStream(seed, stream): one next_gaussian() (a
+// cached sin half shows here) and one next_u64() (the xoshiro state). Bitwise.
+inline void require_fresh(const RngStream& rng) {
+    RngStream used = rng;
+    RngStream fresh(rng.seed(), rng.stream_id());
+    const double g0 = used.next_gaussian(), g1 = fresh.next_gaussian();
+    const std::uint64_t u0 = used.next_u64(), u1 = fresh.next_u64();
+    if (std::bit_cast<std::uint64_t>(g0) != std::bit_cast<std::uint64_t>(g1) || u0 != u1)
+        throw Error("qbfac::gpu: the RngStream has already been drawn from; the device path generates Omega "
+                    "from the initial position of (seed, stream) — pass a fresh RngStream");
+}
+
 inline QBFactorization run(const MatrixHandle& a, qbfac_params p, RngStream& rng) {
+    require_fresh(rng);
     qbfac_gpu_ctx* c = context();
     p.seed = rng.seed();
     p.stream = rng.stream_id();

@@ -122,7 +122,8 @@ const char* qbfac_gpu_last_error(const qbfac_gpu_ctx* ctx);
 int qbfac_gpu_synchronize(qbfac_gpu_ctx* ctx);
 /* The CUDA stream (cudaStream_t) every call of this context is ordered on. */
 void* qbfac_gpu_stream(qbfac_gpu_ctx* ctx);
-/* Number of kernels this context launched so far. */
+/* Number of kernels this context launched so far (counted per context; NULL = the
+ * process-wide total). */
 int64_t qbfac_gpu_kernel_launches(const qbfac_gpu_ctx* ctx);
 
 /* ---- the matrix A (MatrixHandle) ----------------------------------------------- */

@@ -87,6 +87,21 @@ int main() {
                 std::printf("{\"case\": \"floor\", \"thrown\": true, \"floor\": %.17g}\n", e.floor_value());
             }
         }
+        for (int draws : {1, 2}) {
+            // a stream already drawn from (odd count: cached Box-Muller half; even: advanced state)
+            MatrixHandle a(synth(100, 7.0, 1));
+            RngStream r2(7);
+            for (int d = 0; d < draws; ++d) r2.next_gaussian();
+            const long long p0 = a.passes();
+            bool thrown = false;
+            try {
+                gpu::rand_qb_ei(a, StopRule::fixed_precision(1e-2 * std::sqrt(a.frob_norm_sq())), 10, 0, r2);
+            } catch (const Error&) {
+                thrown = true;
+            }
+            std::printf("{\"case\": \"consumed_rng_%d\", \"thrown\": %s, \"passes\": %lld}\n", draws,
+                        thrown ? "true" : "false", a.passes() - p0);
+        }
     } catch (const std::exception& e) {
         std::printf("{\"error\": \"%s\"}\n", e.what());
         return 1;

@@ -39,7 +39,8 @@ class QboResult(C.Structure):
     _fields_ = [("rank", C.c_int64), ("E", C.c_double), ("norm_a_sq", C.c_double),
                 ("passes", C.c_int64), ("terminated_by", C.c_int32), ("status", C.c_int32),
                 ("diag_index", C.c_int64), ("floor", C.c_double), ("m", C.c_int64),
-                ("n", C.c_int64), ("n_trace", C.c_int64), ("msg", C.c_char * 256)]
+                ("n", C.c_int64), ("n_trace", C.c_int64), ("msg", C.c_char * 256),
+                ("seconds", C.c_double)]
 
 
 def build(force: bool = False) -> str:
@@ -233,6 +234,7 @@ class OracleQB:
     passes: int
     terminated_by: str
     e_trace: np.ndarray
+    seconds: float = 0.0  # steady_clock around the rand_qb_* call inside the oracle
 
 
 class OracleError(Exception):
@@ -274,7 +276,7 @@ def run(alg: str, a=None, csr=None, *, b=10, power=0, eps_abs=0.0, fixed_rank=No
         L.qbo_copy_trace(h, _p(tr))
     L.qbo_free(h)
     return OracleQB(Q, B, r, res.E, res.norm_a_sq, int(res.passes),
-                    TERMINATION[res.terminated_by], tr)
+                    TERMINATION[res.terminated_by], tr, float(res.seconds))
 
 
 def explicit_error(q, b, a=None, csr=None) -> float:

@@ -10,6 +10,7 @@
 //   4 FormatError, 5 ResourceError, 6 Error, 7 other.
 
 #include <cstdint>
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -47,6 +48,7 @@ struct qbo_result {
     std::int64_t m, n;
     std::int64_t n_trace;
     char msg[256];
+    double seconds;  // steady_clock around the rand_qb_* call (matrix wrap excluded)
 };
 
 }  // extern "C"
@@ -288,7 +290,9 @@ void* qbo_run_dense(std::int64_t m, std::int64_t n, const double* a, const qbo_p
     res->status = guard(res, [&] {
         MatrixHandle mh(DenseMatrix::from_data(m, n, std::vector<double>(a, a + m * n)));
         auto hh = std::make_unique<Handle>();
+        const auto t0 = std::chrono::steady_clock::now();
         hh->f = run(mh, *p);
+        res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         fill(res, hh->f, m, n);
         h = hh.release();
     });
@@ -304,7 +308,9 @@ void* qbo_run_csr(std::int64_t m, std::int64_t n, std::int64_t nnz, const std::i
             m, n, std::vector<std::int64_t>(rp, rp + m + 1), std::vector<std::int32_t>(ci, ci + nnz),
             std::vector<double>(v, v + nnz)));
         auto hh = std::make_unique<Handle>();
+        const auto t0 = std::chrono::steady_clock::now();
         hh->f = run(mh, *p);
+        res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         fill(res, hh->f, m, n);
         h = hh.release();
     });

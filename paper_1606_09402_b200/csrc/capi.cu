@@ -15,6 +15,7 @@
 struct qbfac_gpu_ctx {
     std::unique_ptr<qbgpu::Context> c;
     std::string last_error;
+    long long launches = 0;  // kernels launched by this context's C-ABI calls
 };
 struct qbfac_gpu_matrix {
     qbfac_gpu_ctx* ctx = nullptr;
@@ -37,6 +38,12 @@ int guard(qbfac_gpu_ctx* ctx, Fn&& fn, qbfac_info* info = nullptr) {
         if (info) info->status = st;
         return st;
     };
+    // launches made while this call runs are this context's (QB_LAUNCH_CHECK)
+    struct CounterScope {
+        long long* prev;
+        explicit CounterScope(long long* c) : prev(qbgpu::t_launch_counter) { qbgpu::t_launch_counter = c; }
+        ~CounterScope() { qbgpu::t_launch_counter = prev; }
+    } scope(ctx ? &ctx->launches : qbgpu::t_launch_counter);
     try {
         if (ctx && ctx->c) {
             cudaError_t e = cudaSetDevice(ctx->c->device);
@@ -95,7 +102,9 @@ int qbfac_gpu_synchronize(qbfac_gpu_ctx* ctx) {
 
 void* qbfac_gpu_stream(qbfac_gpu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c->st) : nullptr; }
 
-int64_t qbfac_gpu_kernel_launches(const qbfac_gpu_ctx*) { return qbgpu::g_kernel_launches.load(); }
+int64_t qbfac_gpu_kernel_launches(const qbfac_gpu_ctx* ctx) {
+    return ctx ? ctx->launches : qbgpu::g_kernel_launches.load();
+}
 
 // ---- matrices ---------------------------------------------------------------------
 int qbfac_gpu_matrix_dense(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,

@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cstdlib>
+#include <mutex>
 #include <utility>
 #include <cstdint>
 #include <stdexcept>
@@ -45,13 +46,37 @@ struct QbError : std::runtime_error {
     } while (0)
 
 // Every kernel launch of the library is followed by QB_LAUNCH_CHECK(), which
-// also counts it (qbfac_gpu_kernel_launches()).
+// also counts it: process-wide, and for the context whose C-ABI call is running on this
+// thread (qbfac_gpu_kernel_launches(ctx); the C-ABI guard installs t_launch_counter).
 extern std::atomic<long long> g_kernel_launches;
+extern thread_local long long* t_launch_counter;
 #define QB_LAUNCH_CHECK()                                   \
     do {                                                    \
         ::qbgpu::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
+        if (::qbgpu::t_launch_counter) ++*::qbgpu::t_launch_counter; \
         QB_CUDA(cudaPeekAtLastError());                     \
     } while (0)
+
+// One-time, per-DEVICE kernel setup (cudaFuncSetAttribute and occupancy queries are
+// per-device state): `init` runs once for each device a process launches on, under
+// std::call_once, and its value (e.g. resident CTAs per SM) is cached per device.
+template <typename T>
+class PerDevice {
+public:
+    template <typename F>
+    T get(F&& init) {
+        int dev = 0;
+        QB_CUDA(cudaGetDevice(&dev));
+        if (dev < 0 || dev >= kMax) throw QbError(kError, "device ordinal out of range");
+        std::call_once(once_[dev], [&] { val_[dev] = init(); });
+        return val_[dev];
+    }
+
+private:
+    static constexpr int kMax = 64;
+    std::once_flag once_[kMax];
+    T val_[kMax] = {};
+};
 
 inline std::int64_t round_up(std::int64_t x, std::int64_t a) { return (x + a - 1) / a * a; }
 inline std::int64_t ceil_div(std::int64_t x, std::int64_t a) { return (x + a - 1) / a; }

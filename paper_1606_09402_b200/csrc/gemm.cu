@@ -310,12 +310,13 @@ void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, s
     using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
     auto kern = dgemm_ws_kernel<BM, BN, BK, WM, WN, STAGES, AR, BR, NP>;
     constexpr int smem = T::SMEM_BYTES + 2 * STAGES * 8;
-    static int per_sm = 0;
-    if (!per_sm) {
+    static PerDevice<int> setup;
+    const int per_sm = setup.get([&] {
+        int v = 0;
         QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (WM * WN + NP) * 32, smem));
-        if (per_sm < 1) per_sm = 1;
-    }
+        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, (WM * WN + NP) * 32, smem));
+        return v < 1 ? 1 : v;
+    });
     WsArgs p{};
     p.A = a.p; p.lda = a.ld; p.B = b.p; p.ldb = b.ld; p.C = c; p.ldc = ldc; p.c_row = c_row ? 1 : 0;
     p.M = M; p.N = N; p.K = K; p.k_split_len = klen; p.splits = splits;
@@ -385,11 +386,11 @@ void launch_cfg(cudaStream_t st, const MatView& a, const MatView& b, double* c, 
                 double* partial, int flags) {
     using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
     auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, AR, BR, VEC>;
-    static bool configured = false;  // per template instance
-    if (!configured) {
+    static PerDevice<bool> setup;  // per template instance and device
+    setup.get([&] {
         QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES));
-        configured = true;
-    }
+        return true;
+    });
     dim3 grid(static_cast<unsigned>(ceil_div(M, BM)), static_cast<unsigned>(ceil_div(N, BN)),
               static_cast<unsigned>(splits));
     kern<<<grid, T::NT, T::SMEM_BYTES, st>>>(a.p, a.ld, b.p, b.ld, c, ldc, c_row ? 1 : 0, M, N, K,
@@ -461,13 +462,13 @@ void make_tensor_map_rows(void* map, const double* base, std::int64_t rows, int 
 }
 
 int gemm_num_sms() {
-    static int sms = [] {
+    static PerDevice<int> sms;
+    return sms.get([] {
         int dev = 0, n = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        QB_CUDA(cudaGetDevice(&dev));
+        QB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
         return n;
-    }();
-    return sms;
+    });
 }
 
 void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const MatView& b,

@@ -73,6 +73,20 @@ int qbm_gaussian(std::uint64_t seed, std::uint64_t stream, std::int64_t skip, st
     return 0;
 }
 
+// out[i] += alpha * (draw skip + i of RngStream(seed, stream)), i < count: the noise term
+// of config 4 added in place (no count-sized temporary). alpha * g is rounded before the
+// add (no FMA contraction: built without -mfma).
+int qbm_gaussian_add(std::uint64_t seed, std::uint64_t stream, std::int64_t skip, std::int64_t count, double alpha,
+                     double* out) {
+    Rng r(seed, stream);
+    for (std::int64_t i = 0; i < skip; ++i) r.normal();
+    for (std::int64_t i = 0; i < count; ++i) {
+        const double t = alpha * r.normal();
+        out[i] += t;
+    }
+    return 0;
+}
+
 int qbm_u64(std::uint64_t seed, std::uint64_t stream, std::int64_t count, std::uint64_t* out) {
     Rng r(seed, stream);
     for (std::int64_t i = 0; i < count; ++i) out[i] = r.u64();
@@ -118,10 +132,12 @@ int qbm_csr_uniform(std::uint64_t seed, std::int64_t m, std::int64_t n, std::int
 // Config 5 recipe (term-document-like, builder's choices recorded in
 // DESIGN.md): row lengths L_r = clamp(round(c * rank_r^-alpha), 1, n) over a seeded
 // random row permutation (rank_r = position of row r in the permutation, 1-based);
-// columns drawn from Zipf(alpha) popularity over a seeded column permutation, with
-// replacement then de-duplicated (so a row may end with fewer than L_r entries);
-// rows with L_r >= n/2 take every column. Values log(1+k), k ~ Poisson(3), redrawn
-// while k == 0. Pass 1 (rp == nullptr) only returns nnz.
+// each row holds exactly L_r distinct columns drawn from Zipf(alpha) popularity over a
+// seeded column permutation WITHOUT replacement: light rows (L_r <= n/16) redraw a
+// column already taken, heavy rows (n/16 < L_r < n) take the L_r largest
+// Efraimidis-Spirakis keys log(u_j)/w_j over all n columns, rows with L_r = n take every
+// column. So nnz = sum_r L_r exactly. Values log(1+k), k ~ Poisson(3), redrawn while
+// k == 0. Pass 1 (rp == nullptr) only returns nnz (no column draws).
 std::int64_t qbm_csr_zipf(std::uint64_t seed, std::int64_t m, std::int64_t n, double alpha, double c,
                           std::int64_t* rp, std::int32_t* ci, double* v) {
     Rng rperm(seed, 1), rcol(seed, 2), rval(seed, 3), rpick(seed, 4);
@@ -133,29 +149,50 @@ std::int64_t qbm_csr_zipf(std::uint64_t seed, std::int64_t m, std::int64_t n, do
         for (std::int64_t i = m - 1; i > 0; --i) std::swap(perm[i], perm[rperm.u64() % static_cast<std::uint64_t>(i + 1)]);
         for (std::int64_t i = 0; i < m; ++i) rank_of[perm[i]] = i + 1;
     }
+    auto row_len = [&](std::int64_t i) {
+        const double lr = std::round(c * std::pow(static_cast<double>(rank_of[i]), -alpha));
+        return std::max<std::int64_t>(1, std::min<std::int64_t>(n, static_cast<std::int64_t>(std::min(lr, 9.0e18))));
+    };
+    if (!rp) {
+        std::int64_t nnz = 0;
+        for (std::int64_t i = 0; i < m; ++i) nnz += row_len(i);
+        return nnz;
+    }
     std::vector<std::int32_t> colperm(n);
     for (std::int64_t j = 0; j < n; ++j) colperm[j] = static_cast<std::int32_t>(j);
     for (std::int64_t j = n - 1; j > 0; --j) std::swap(colperm[j], colperm[rcol.u64() % static_cast<std::uint64_t>(j + 1)]);
-    // Zipf CDF over popularity ranks 1..n
-    std::vector<double> cdf(n);
+    // Zipf weights / CDF over popularity ranks 1..n
+    std::vector<double> cdf(n), logw(n);
     double acc = 0.0;
     for (std::int64_t j = 0; j < n; ++j) {
-        acc += std::pow(static_cast<double>(j + 1), -alpha);
+        const double w = std::pow(static_cast<double>(j + 1), -alpha);
+        logw[j] = std::log(w);
+        acc += w;
         cdf[j] = acc;
     }
     for (auto& x : cdf) x /= acc;
     std::int64_t nnz = 0;
     std::vector<std::int32_t> row;
     std::vector<char> mark(n, 0);
-    if (rp) rp[0] = 0;
+    std::vector<std::pair<double, std::int32_t>> keys;
+    rp[0] = 0;
     for (std::int64_t i = 0; i < m; ++i) {
-        const double lr = std::round(c * std::pow(static_cast<double>(rank_of[i]), -alpha));
-        const std::int64_t L = std::max<std::int64_t>(1, std::min<std::int64_t>(n, static_cast<std::int64_t>(lr)));
+        const std::int64_t L = row_len(i);
         row.clear();
-        if (2 * L >= n) {
+        if (L >= n) {
             for (std::int64_t j = 0; j < n; ++j) row.push_back(static_cast<std::int32_t>(j));
+        } else if (16 * L > n) {
+            // weighted sampling without replacement: the L largest log(u)/w (u in (0,1])
+            keys.resize(n);
+            for (std::int64_t k = 0; k < n; ++k) {
+                const double u = static_cast<double>((rpick.u64() >> 11) + 1) * 0x1.0p-53;
+                keys[k] = {std::log(-std::log(u)) - logw[k], colperm[k]};  // ascending = largest key
+            }
+            std::nth_element(keys.begin(), keys.begin() + (L - 1), keys.end());
+            for (std::int64_t q = 0; q < L; ++q) row.push_back(keys[q].second);
+            std::sort(row.begin(), row.end());
         } else {
-            for (std::int64_t t = 0; t < L; ++t) {
+            while (static_cast<std::int64_t>(row.size()) < L) {
                 const double u = rpick.uniform();
                 const std::int64_t k = std::lower_bound(cdf.begin(), cdf.end(), u) - cdf.begin();
                 const std::int32_t col = colperm[std::min<std::int64_t>(k, n - 1)];
@@ -167,26 +204,24 @@ std::int64_t qbm_csr_zipf(std::uint64_t seed, std::int64_t m, std::int64_t n, do
             for (auto col : row) mark[col] = 0;
             std::sort(row.begin(), row.end());
         }
-        if (rp) {
-            for (std::size_t q = 0; q < row.size(); ++q) {
-                ci[nnz + static_cast<std::int64_t>(q)] = row[q];
-                // Poisson(3) by inversion, redrawn while 0
-                std::int64_t k = 0;
-                do {
-                    const double u = rval.uniform();
-                    double p = std::exp(-3.0), cdfp = p;
-                    k = 0;
-                    while (u > cdfp && k < 64) {
-                        ++k;
-                        p *= 3.0 / static_cast<double>(k);
-                        cdfp += p;
-                    }
-                } while (k == 0);
-                v[nnz + static_cast<std::int64_t>(q)] = std::log1p(static_cast<double>(k));
-            }
-            rp[i + 1] = nnz + static_cast<std::int64_t>(row.size());
+        for (std::size_t q = 0; q < row.size(); ++q) {
+            ci[nnz + static_cast<std::int64_t>(q)] = row[q];
+            // Poisson(3) by inversion, redrawn while 0
+            std::int64_t k = 0;
+            do {
+                const double u = rval.uniform();
+                double p = std::exp(-3.0), cdfp = p;
+                k = 0;
+                while (u > cdfp && k < 64) {
+                    ++k;
+                    p *= 3.0 / static_cast<double>(k);
+                    cdfp += p;
+                }
+            } while (k == 0);
+            v[nnz + static_cast<std::int64_t>(q)] = std::log1p(static_cast<double>(k));
         }
         nnz += static_cast<std::int64_t>(row.size());
+        rp[i + 1] = nnz;
     }
     return nnz;
 }

@@ -31,6 +31,7 @@
 namespace qbgpu {
 
 std::atomic<long long> g_kernel_launches{0};
+thread_local long long* t_launch_counter = nullptr;
 
 namespace {
 
@@ -185,6 +186,8 @@ std::unique_ptr<Matrix> make_dense_stream(Context& c, std::int64_t m, std::int64
                                           std::int64_t lda, std::int64_t chunk_rows) {
     if (m < 0 || n < 0 || lda < std::max<std::int64_t>(1, m) || (m > 0 && n > 0 && !a))
         throw QbError(kDimensionError, "matrix_dense_stream: bad dimensions");
+    // the streamed single pass forms H and ||A||^2 of the local rows only: no row-sharded RowStream
+    if (c.world > 1) throw QbError(kError, "matrix_dense_stream: a host RowStream is single-GPU (world == 1)");
     auto mat = std::make_unique<Matrix>();
     mat->ctx = &c;
     mat->m = m;
@@ -1197,6 +1200,20 @@ int qb_to_svd(Context& c, Result& r, std::int64_t k, double* u_out, std::int64_t
 }
 
 // ---- operator layer ------------------------------------------------------------------
+// DenseMatrix::from_data rejects non-finite entries (dense_matrix.cpp:17-18). An async upload
+// defers that check to its first ||A||^2 (frob_device); a consumer that never forms the norm
+// (randQB, the range finder, a bare multiply) runs it here, once, before its result is returned.
+void finish_finite_check(Context& c, Matrix& a) {
+    if (!a.check_finite) return;
+    a.wait_resident(c.st);
+    double* d = c.d_small + static_cast<std::size_t>(kSlot) * kNumSlots + 3;
+    sum_squares(c.st, c.ws_red, a.dense_view(), d);
+    QB_CUDA(cudaMemcpyAsync(c.h_scalar, d, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    QB_CUDA(cudaStreamSynchronize(c.st));
+    a.check_finite = false;
+    if (!std::isfinite(c.h_scalar[0])) throw QbError(kError, "from_data: non-finite entry");
+}
+
 double frob_norm_sq(Context& c, Matrix& a) {
     Engine eng(c, a);
     a.passes += 1;
@@ -1208,6 +1225,7 @@ void multiply(Context& c, Matrix& a, const MatView& x, const MatView& y, bool tr
     if (trans) eng.apply_t(x, y);
     else eng.apply(x, y);
     a.passes += 1;
+    finish_finite_check(c, a);
 }
 
 // ---- baselines (§8(f) 4) ---------------------------------------------
@@ -1439,6 +1457,7 @@ std::unique_ptr<Result> run(Context& c, Matrix& a, const Params& p) {
         case 6: r = run_arf(c, a, p); break;
         default: throw QbError(kError, "unknown algorithm id");
     }
+    finish_finite_check(c, a);
     r->device_ms = t.stop();
     return r;
 }

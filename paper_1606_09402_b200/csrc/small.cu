@@ -1525,12 +1525,12 @@ void column_sumsq(cudaStream_t st, Workspace& ws, const MatView& v, double* out)
 template <int BP>
 void launch_chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, double* r, double* rinv,
                        std::int64_t ldr, SmallStatus* status) {
-    static bool configured = false;
-    if (!configured) {
+    static PerDevice<bool> setup;
+    setup.get([] {
         QB_CUDA(cudaFuncSetAttribute(chol_small_kernel<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      CholCfg<BP>::SMEM));
-        configured = true;
-    }
+        return true;
+    });
     chol_small_kernel<BP><<<1, kCholThreads, CholCfg<BP>::SMEM, st>>>(g, ldg, b, r, rinv, ldr, status);
 }
 
@@ -1553,13 +1553,13 @@ void chol_small(cudaStream_t st, const double* g, std::int64_t ldg, int b, doubl
 void chol_wide(cudaStream_t st, double* w, std::int64_t ldw, int l, double* r, double* rinv, std::int64_t ldr,
                SmallStatus* stats) {
     if (l < 1) throw QbError(kDimensionError, "chol_wide: empty");
-    static int grid = 0;
-    if (!grid) {
+    static PerDevice<int> setup;
+    const int grid = setup.get([] {
         QB_CUDA(cudaFuncSetAttribute(chol_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCwSmemBytes));
         int per_sm = 0;
         QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_wide_kernel, kCholThreads, kCwSmemBytes));
-        grid = std::max(1, std::min(per_sm, 1) * gemm_num_sms());
-    }
+        return std::max(1, std::min(per_sm, 1) * gemm_num_sms());
+    });
     CholWideArgs a{w, ldw, r, rinv, ldr, l, static_cast<int>(ceil_div(l, kCwNb)), stats};
     void* args[] = {&a};
     QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(chol_wide_kernel), grid, kCholThreads, args,
@@ -1572,12 +1572,14 @@ void launch_cholqr2_panel(cudaStream_t st, PanelArgs& a, int grid_cap) {
     using C = PanelCfg<BP>;
     auto kern = cholqr2_panel_kernel<BP>;
     a.nsub = static_cast<int>(ceil_div(a.rows, C::SUB));
-    static int per_sm = 0;
-    if (!per_sm) {
+    static PerDevice<int> setup;
+    const int per_sm = setup.get([&] {
+        int v = 0;
         QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCholThreads, C::SMEM));
-        if (per_sm < 1) throw QbError(kError, "cholqr2_panel: kernel does not fit on an SM");
-    }
+        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, kCholThreads, C::SMEM));
+        if (v < 1) throw QbError(kError, "cholqr2_panel: kernel does not fit on an SM");
+        return v;
+    });
     const int grid = std::max(1, std::min(std::min(a.nsub, grid_cap), per_sm * gemm_num_sms()));
     static const bool tm_on = [] {
         const char* e = std::getenv("QBFAC_PANEL_TM");
@@ -1672,12 +1674,12 @@ void trmm_upper_small(cudaStream_t st, const double* a, const double* b, double*
 void trmm_upper_pair(cudaStream_t st, const double* a0, const double* b0, double* c0, const double* a1,
                      const double* b1, double* c1, int n, std::int64_t ld) {
     if (n < 1 || n > kSmallMax) throw QbError(kDimensionError, "trmm_upper: size out of range");
-    static bool configured = false;
-    if (!configured) {
+    static PerDevice<bool> setup;
+    setup.get([] {
         QB_CUDA(cudaFuncSetAttribute(trmm_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      2 * kSmallMax * (kSmallMax + 1) * 8));
-        configured = true;
-    }
+        return true;
+    });
     TrmmPair p{{a0, a1}, {b0, b1}, {c0, c1}};
     const int smem = 2 * n * (n + 1) * static_cast<int>(sizeof(double));
     launch_pdl(trmm_upper_kernel, dim3(c1 ? 2 : 1), dim3(1024), static_cast<std::size_t>(smem), st, p, n, ld);

@@ -30,6 +30,7 @@ def mglib():
         P, I64, U64, D = C.c_void_p, C.c_int64, C.c_uint64, C.c_double
         L.qbm_gaussian.argtypes = [U64, U64, I64, I64, P]
         L.qbm_u64.argtypes = [U64, U64, I64, P]
+        L.qbm_gaussian_add.argtypes = [U64, U64, I64, I64, D, P]
         L.qbm_csr_uniform.argtypes = [U64, I64, I64, I64, P, P, P]
         L.qbm_csr_zipf.argtypes = [U64, I64, I64, D, D, P, P, P]
         L.qbm_csr_zipf.restype = I64

@@ -26,6 +26,9 @@ def test_reference_binding_drop_in():
         assert c["rng_next_cpu"] == c["rng_next_gpu"], c      # RngStream left in the same state
         assert abs(c["err_cpu"] - c["err_gpu"]) <= 1e-8 * c["err_cpu"], c
     assert cases["floor"]["thrown"] is True
+    for draws in (1, 2):  # a consumed RngStream is rejected before any device work
+        c = cases[f"consumed_rng_{draws}"]
+        assert c["thrown"] is True and c["passes"] == 0, c
 
 
 def test_binding_header_compiles_against_reference_headers():

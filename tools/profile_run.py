@@ -53,7 +53,7 @@ def main():
         run = lambda: qbfac.run_device(h, alg=3, mode=0, b=100, k=400, s=0, seed=42)
         w = 400
     else:
-        csr = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=3e8, seed=5)
+        csr = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=2e8, seed=5)
         h = qbfac.MatrixHandle.csr(*csr, ctx=ctx)
         eps = 0.6 * float(np.sqrt((csr[4] ** 2).sum()))
         run = lambda: qbfac.run_device(h, alg=0, b=100, power=2, max_rank=2000, eps_abs=eps, seed=42)

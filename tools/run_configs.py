@@ -143,7 +143,7 @@ def main():
             torch.cuda.empty_cache()
             continue
         elif c == 5:
-            csr = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=3e8, seed=5)  # ~2e8 after de-dup
+            csr = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=2e8, seed=5)
             r["gen_s"] = time.perf_counter() - t0
             r["nnz"] = len(csr[4])
             h = qbfac.MatrixHandle.csr(*csr, ctx=ctx)

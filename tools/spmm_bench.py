@@ -24,7 +24,7 @@ def main():
         if cfg == 3:
             csr, w = matgen.csr_uniform(100000, 50000, 50, seed=3), 50
         else:
-            csr, w = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=3e8, seed=5), 100
+            csr, w = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=2e8, seed=5), 100
         h = qbfac.MatrixHandle.csr(*csr, ctx=ctx)
         nnz = len(csr[4])
         m, n = h.m, h.n
