@@ -114,7 +114,9 @@ typedef struct qbfac_gpu_result qbfac_gpu_result;
 /* ---- context -------------------------------------------------------------------- */
 int qbfac_gpu_create(int device, qbfac_gpu_ctx** out);
 /* Row-sharded context: this process is `rank` of `world`, one GPU each; the
- * 128-byte NCCL unique id comes from qbfac_gpu_nccl_unique_id() on rank 0. */
+ * 128-byte NCCL unique id comes from qbfac_gpu_nccl_unique_id() on rank 0. world == 1
+ * with a non-NULL id builds a one-rank NCCL communicator (same results as
+ * qbfac_gpu_create). */
 int qbfac_gpu_create_dist(int device, int rank, int world, const void* nccl_id, qbfac_gpu_ctx** out);
 int qbfac_gpu_nccl_unique_id(void* out128);
 void qbfac_gpu_destroy(qbfac_gpu_ctx* ctx);
@@ -156,6 +158,15 @@ int qbfac_gpu_matrix_dense_stream(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, cons
                                   int64_t chunk_rows, qbfac_gpu_matrix** out);
 int qbfac_gpu_matrix_csr(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
                          const int32_t* col_idx, const double* values, qbfac_gpu_matrix** out);
+/* Host-streamed CSR — the CsrRowStream of single_pass_fp (matrix_handle.cpp:60-73,
+ * SPEC.md:300-308): the arrays stay in host memory (borrowed, must outlive the run) and
+ * QBFAC_ALG_SINGLE_PASS uploads row chunks of about chunk_nnz entries (0 = 16 Mi) one at a
+ * time, validating each as SparseCsrMatrix::from_parts (FormatError / Error) before
+ * G_c = A_c Omega, H += A_c^T G_c and ||A_c||^2. row_ptr is checked whole at creation.
+ * Any other use of the handle returns QBFAC_ERROR; world must be 1. */
+int qbfac_gpu_matrix_csr_stream(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                                const int32_t* col_idx, const double* values, int64_t chunk_nnz,
+                                qbfac_gpu_matrix** out);
 int qbfac_gpu_matrix_csr_shard(qbfac_gpu_ctx* ctx, int64_t m_global, int64_t row0, int64_t m_local,
                                int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
                                const double* values, qbfac_gpu_matrix** out);

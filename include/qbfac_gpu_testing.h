@@ -12,6 +12,7 @@
  *   qbfac_gpu_test_orth_wide the power step's orth() of a wide sketch (CholQR2 or BCGS2)
  *   qbfac_gpu_test_colsumsq  per-column sums of squares (the indicator's row norms)
  *   qbfac_gpu_test_create_local_group  in-process rank group on one GPU (sharded-engine tests)
+ *   qbfac_gpu_test_allreduce the context's allreduce (NCCL, or the local group) on a device buffer
  *   qbfac_gpu_test_chol_wide_trace  per-step stamps of the wide Cholesky
  *   qbfac_gpu_test_panel_trace  per-phase %globaltimer stamps (ns) of the last CholQR2 panel launch
  *   qbfac_gpu_test_csr_spmm  CSR pass Y = alpha A X + beta Y on device arrays
@@ -47,6 +48,9 @@ int qbfac_gpu_test_panel_trace(qbfac_gpu_ctx* ctx, unsigned long long* out);
    driven by its own host thread (qbfac_gpu_run blocks in the collectives). Test harness for the
    NCCL path's arithmetic on a single GPU; outs[world] receives the contexts. */
 int qbfac_gpu_test_create_local_group(int device, int world, qbfac_gpu_ctx** outs);
+/* In-place sum over the context's ranks of count doubles at dev (ncclAllReduce for an NCCL
+   context, including a one-rank communicator made with qbfac_gpu_create_dist(dev, 0, 1, id)). */
+int qbfac_gpu_test_allreduce(qbfac_gpu_ctx* ctx, double* dev, int64_t count);
 /* 64 x 4 %globaltimer stamps (ns) per step k of the last chol_wide launch (CTA 0): step start, phase 2
    done, phase 3 done (incl. the next diagonal Cholesky on CTA 0), step end */
 int qbfac_gpu_test_chol_wide_trace(qbfac_gpu_ctx* ctx, unsigned long long* out);

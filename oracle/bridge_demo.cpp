@@ -92,10 +92,11 @@ int main() {
             MatrixHandle a(synth(100, 7.0, 1));
             RngStream r2(7);
             for (int d = 0; d < draws; ++d) r2.next_gaussian();
+            const double eps = 1e-2 * std::sqrt(a.frob_norm_sq());
             const long long p0 = a.passes();
             bool thrown = false;
             try {
-                gpu::rand_qb_ei(a, StopRule::fixed_precision(1e-2 * std::sqrt(a.frob_norm_sq())), 10, 0, r2);
+                gpu::rand_qb_ei(a, StopRule::fixed_precision(eps), 10, 0, r2);
             } catch (const Error&) {
                 thrown = true;
             }

@@ -77,6 +77,7 @@ int qbfac_gpu_create_dist(int device, int rank, int world, const void* nccl_id, 
     auto h = std::make_unique<qbfac_gpu_ctx>();
     int st = guard(nullptr, [&] {
         if (world > 1 && !nccl_id) throw qbgpu::QbError(qbgpu::kError, "world > 1 needs an NCCL unique id");
+        if (world < 1 || rank < 0 || rank >= world) throw qbgpu::QbError(qbgpu::kDimensionError, "bad rank/world");
         h->c = std::make_unique<qbgpu::Context>(device, rank, world, nccl_id);
     });
     if (st == QBFAC_OK) *out = h.release();
@@ -163,6 +164,19 @@ int qbfac_gpu_matrix_dense_stream(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, cons
 int qbfac_gpu_matrix_csr(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
                          const int32_t* col_idx, const double* values, qbfac_gpu_matrix** out) {
     return qbfac_gpu_matrix_csr_shard(ctx, m, 0, m, n, nnz, row_ptr, col_idx, values, out);
+}
+
+int qbfac_gpu_matrix_csr_stream(qbfac_gpu_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                                const int32_t* col_idx, const double* values, int64_t chunk_nnz,
+                                qbfac_gpu_matrix** out) {
+    if (!ctx || !out) return QBFAC_ERROR;
+    *out = nullptr;
+    return guard(ctx, [&] {
+        auto h = std::make_unique<qbfac_gpu_matrix>();
+        h->ctx = ctx;
+        h->m = qbgpu::make_csr_stream(*ctx->c, m, n, nnz, row_ptr, col_idx, values, chunk_nnz);
+        *out = h.release();
+    });
 }
 
 int qbfac_gpu_matrix_csr_shard(qbfac_gpu_ctx* ctx, int64_t m_global, int64_t row0, int64_t m_local, int64_t n,
@@ -535,6 +549,15 @@ int qbfac_gpu_test_create_local_group(int device, int world, qbfac_gpu_ctx** out
     if (st == QBFAC_OK)
         for (int r = 0; r < world; ++r) outs[r] = hs[static_cast<std::size_t>(r)].release();
     return st;
+}
+
+int qbfac_gpu_test_allreduce(qbfac_gpu_ctx* ctx, double* dev, int64_t count) {
+    if (!ctx) return QBFAC_ERROR;
+    return guard(ctx, [&] {
+        if (!ctx->c->comm) throw qbgpu::QbError(qbgpu::kError, "context has no communicator");
+        ctx->c->allreduce(dev, static_cast<std::size_t>(count));
+        QB_CUDA(cudaStreamSynchronize(ctx->c->st));
+    });
 }
 
 int qbfac_gpu_test_chol_wide_trace(qbfac_gpu_ctx* ctx, unsigned long long* out) {

@@ -86,7 +86,7 @@ Comm::Comm(int rank, int world, std::shared_ptr<LocalGroup> group) : rank_(rank)
 
 Comm::Comm(int rank, int world, const void* unique_id128) : rank_(rank), world_(world) {
     if (world < 1 || rank < 0 || rank >= world) throw QbError(kDimensionError, "bad rank/world");
-    if (world == 1) return;
+    if (!unique_id128) throw QbError(kError, "NCCL communicator needs a unique id");
     ncclUniqueId id;
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
     std::memcpy(&id, unique_id128, sizeof(id));
@@ -123,7 +123,7 @@ void Comm::allreduce_sum(double* p, std::size_t count, cudaStream_t st) {
         g.barrier();
         return;
     }
-    if (world_ == 1 || count == 0) return;
+    if (!comm_ || count == 0) return;
     check(api().all_reduce(p, p, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), st),
           "ncclAllReduce");
 }

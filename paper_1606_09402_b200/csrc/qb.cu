@@ -72,7 +72,9 @@ Context::Context(int dev, int rank_, int world_, const void* nccl_id, std::share
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     rng.device();
-    if (world > 1) comm = local ? std::make_unique<Comm>(rank, world, std::move(local)) : std::make_unique<Comm>(rank, world, nccl_id);
+    // world == 1 with an NCCL id: a one-rank communicator (exercises the NCCL path on one GPU)
+    if (world > 1 || nccl_id)
+        comm = local ? std::make_unique<Comm>(rank, world, std::move(local)) : std::make_unique<Comm>(rank, world, nccl_id);
 }
 
 Context::~Context() {
@@ -211,9 +213,37 @@ void Matrix::wait_resident(cudaStream_t s) {
     pending.clear();
 }
 
+std::unique_ptr<Matrix> make_csr_stream(Context& c, std::int64_t m, std::int64_t n, std::int64_t nnz,
+                                        const std::int64_t* rp, const std::int32_t* ci, const double* v,
+                                        std::int64_t chunk_nnz) {
+    if (n > static_cast<std::int64_t>(INT32_MAX))
+        throw QbError(kDimensionError, "csr: column count exceeds 32-bit index range");
+    if (m < 0 || n < 0 || nnz < 0 || !rp || (nnz > 0 && (!ci || !v)))
+        throw QbError(kFormatError, "csr: inconsistent structure arrays");
+    if (c.world > 1) throw QbError(kError, "matrix_csr_stream: a host RowStream is single-GPU (world == 1)");
+    // row_ptr must be a valid partition before it is used to cut chunks (sparse_csr.cpp:16-20);
+    // column indices and values are validated per chunk on the device as each one is uploaded
+    if (rp[0] != 0 || rp[m] != nnz) throw QbError(kFormatError, "csr: row_ptr does not span the entries");
+    for (std::int64_t i = 0; i < m; ++i)
+        if (rp[i + 1] < rp[i]) throw QbError(kFormatError, "csr: row_ptr not non-decreasing");
+    auto mat = std::make_unique<Matrix>();
+    mat->ctx = &c;
+    mat->sparse = true;
+    mat->m = m;
+    mat->n = n;
+    mat->m_global = m;
+    mat->nnz = nnz;
+    mat->host_stream = true;
+    mat->host_rp = rp;
+    mat->host_ci = ci;
+    mat->host_v = v;
+    mat->chunk_nnz = chunk_nnz > 0 ? chunk_nnz : (std::int64_t{16} << 20);  // ~200 MB of entries
+    return mat;
+}
+
 std::unique_ptr<Matrix> make_csr(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
                                  std::int64_t n, std::int64_t nnz, const std::int64_t* rp, const std::int32_t* ci,
-                                 const double* v) {
+                                 const double* v, bool allow_hybrid) {
     if (n > static_cast<std::int64_t>(INT32_MAX))
         throw QbError(kDimensionError, "csr: column count exceeds 32-bit index range");
     if (m < 0 || n < 0 || nnz < 0) throw QbError(kFormatError, "csr: inconsistent structure arrays");
@@ -246,7 +276,7 @@ std::unique_ptr<Matrix> make_csr(Context& c, std::int64_t m_global, std::int64_t
     // 1/16, 1/32; QBFAC_DENSE_DIVR / _DIVC override, QBFAC_CSR_DENSE=0 disables). Blocks are
     // capped at 4 GB each.
     const char* hyb_env = std::getenv("QBFAC_CSR_DENSE");
-    const bool hyb_ok = !(hyb_env && hyb_env[0] == '0') && m > 0 && n > 0 && nnz > 0;
+    const bool hyb_ok = allow_hybrid && !(hyb_env && hyb_env[0] == '0') && m > 0 && n > 0 && nnz > 0;
     std::vector<std::int32_t> rowmap, colmap;
     std::vector<std::int64_t> drows, dcols;
     std::int64_t extracted = 0;
@@ -384,6 +414,7 @@ public:
     // G_c = A_c Omega, H += A_c^T G_c and ||A_c||^2 (summed in chunk order). Returns ||A||^2.
     double stream_single_pass(const MatView& om, const MatView& g, const MatView& h) {
         if (!a_.host_stream) throw QbError(kInternal, "stream_single_pass on a resident matrix");
+        if (a_.sparse) return stream_single_pass_csr(om, g, h);
         const std::int64_t m = a_.m, n = a_.n, cr = a_.chunk_rows;
         const std::int64_t nchunk = ceil_div(m, cr);
         constexpr int kRing = 3;
@@ -428,6 +459,54 @@ public:
         double nrm = 0.0;
         for (double x : hn) nrm += x;
         if (!std::isfinite(nrm)) throw QbError(kError, "from_data: non-finite entry");  // dense_matrix.cpp:17-18
+        return nrm;
+    }
+
+    // CsrRowStream (matrix_handle.cpp:60-73) over host CSR arrays: row chunks of about
+    // chunk_nnz entries are uploaded and validated as SparseCsrMatrix::from_parts would
+    // (make_csr on the chunk: FormatError / Error), then G_c = A_c Omega (CSR SpMM),
+    // H += A_c^T G_c (CSR SpMM over the chunk's device-built transpose) and ||A_c||^2 over
+    // its values, in chunk order. Only one chunk of A is ever resident.
+    double stream_single_pass_csr(const MatView& om, const MatView& g, const MatView& h) {
+        const std::int64_t m = a_.m, n = a_.n, w = om.cols;
+        const std::int64_t* rp = a_.host_rp;
+        std::vector<std::int64_t> cuts{0};  // chunk row boundaries
+        while (cuts.back() < m) {
+            const std::int64_t r0 = cuts.back();
+            std::int64_t r1 = static_cast<std::int64_t>(std::upper_bound(rp + r0 + 1, rp + m + 1, rp[r0] + a_.chunk_nnz) - rp) - 1;
+            cuts.push_back(std::max(r1, r0 + 1));
+        }
+        const std::size_t nchunk = cuts.size() - 1;
+        if (nchunk == 0) {  // no rows: G is empty and H = A^T G = 0
+            if (h.rows * h.cols) QB_CUDA(cudaMemsetAsync(h.p, 0, sizeof(double) * h.rows * h.ld, st_));
+            return 0.0;
+        }
+        DBuf ht(nchunk > 1 ? static_cast<std::size_t>(n) * std::max<std::int64_t>(w, 1) : 0, st_);
+        MatView htv{ht.p, n, w, w, true};
+        DBuf dn(nchunk, st_);
+        for (std::size_t k = 0; k < nchunk; ++k) {
+            const std::int64_t r0 = cuts[k], r1 = cuts[k + 1], e0 = rp[r0], nnz_c = rp[r1] - e0;
+            std::vector<std::int64_t> lrp(static_cast<std::size_t>(r1 - r0 + 1));
+            for (std::int64_t i = r0; i <= r1; ++i) lrp[static_cast<std::size_t>(i - r0)] = rp[i] - e0;
+            auto chunk = make_csr(c_, m, r0, r1 - r0, n, nnz_c, lrp.data(), a_.host_ci + e0, a_.host_v + e0, false);
+            Engine ec(c_, *chunk);
+            MatView gc = g.rowmajor ? MatView{g.p + r0 * g.ld, r1 - r0, g.cols, g.ld, true}
+                                    : MatView{g.p + r0, r1 - r0, g.cols, g.ld, false};
+            ec.apply(om, gc);
+            if (k == 0) {
+                ec.apply_t(gc, h);
+            } else {
+                ec.apply_t(gc, htv);
+                add_matrix(st_, htv, h, 1.0);
+            }
+            sum_squares_vec(st_, c_.ws_red, chunk->v, nnz_c, dn.p + k);
+            QB_CUDA(cudaStreamSynchronize(st_));  // the chunk's device arrays are released next
+        }
+        std::vector<double> norms(nchunk);
+        QB_CUDA(cudaMemcpyAsync(norms.data(), dn.p, sizeof(double) * nchunk, cudaMemcpyDeviceToHost, st_));
+        QB_CUDA(cudaStreamSynchronize(st_));
+        double nrm = 0.0;
+        for (double x : norms) nrm += x;
         return nrm;
     }
 
@@ -577,24 +656,43 @@ public:
             }
         }
         // Householder fallback: exact deficiency decisions (qr.hpp:15-21).
-        if (sharded && c_.world > 1)
-            throw QbError(kError, "numerically rank-deficient sketch under row sharding (Householder panel "
-                                  "fallback is single-GPU)");
         ++hh_fallbacks;
+        if (sharded && c_.world > 1) {
+            // Row-sharded panel: assemble the whole m x b panel on every rank (each rank writes its
+            // rows into a zeroed buffer; the sum over ranks adds only zeros to them, so it is exact),
+            // factor it redundantly (identical inputs, identical R and deficiency decision on every
+            // rank) and keep this rank's rows of Q.
+            const std::int64_t mg = a_.m_global, r0 = a_.row0;
+            DBuf full(static_cast<std::size_t>(std::max<std::int64_t>(mg, 1)) * b, st_);
+            QB_CUDA(cudaMemsetAsync(full.p, 0, sizeof(double) * full.n, st_));
+            MatView fv{full.p, mg, b, std::max<std::int64_t>(mg, 1), false};
+            if (rows) copy_matrix(st_, y, fv.rows_range(r0, rows));
+            c_.allreduce(full.p, full.n);
+            householder_panel(st_, c_.ws_hh, fv.p, mg, b, fv.ld, slot(r_slot), kSmallMax);
+            const int d = householder_rank(r_slot, b);
+            if (rows) copy_matrix(st_, fv.rows_range(r0, rows), qout);
+            if (d > 0) tri_inverse_small(st_, slot(r_slot), slot(rinv_slot), d, kSmallMax);
+            return d;
+        }
         MatView ycol{t1.p, rows, b, std::max<std::int64_t>(rows, 1), false};
         copy_matrix(st_, y, ycol);
         householder_panel(st_, c_.ws_hh, ycol.p, rows, b, ycol.ld, slot(r_slot), kSmallMax);
+        const int d = householder_rank(r_slot, b);
+        copy_matrix(st_, ycol, qout);
+        if (d > 0) tri_inverse_small(st_, slot(r_slot), slot(rinv_slot), d, kSmallMax);
+        return d;
+    }
+    // Leading rank of the Householder R in `r_slot`: the first j with |R_jj| <= 1e-12 max |R_jj|
+    // (rank_deficiency_report, qr.hpp:20-21); b when none.
+    int householder_rank(int r_slot, int b) {
         std::vector<double> rh(static_cast<std::size_t>(kSlot));
         QB_CUDA(cudaMemcpyAsync(rh.data(), slot(r_slot), sizeof(double) * kSlot, cudaMemcpyDeviceToHost, st_));
         QB_CUDA(cudaStreamSynchronize(st_));
         double mx = 0.0;
         for (int j = 0; j < b; ++j) mx = std::max(mx, std::fabs(rh[j + j * kSmallMax]));
-        int d = b;
         for (int j = 0; j < b; ++j)
-            if (std::fabs(rh[j + j * kSmallMax]) <= kRankTol * mx) { d = j; break; }
-        copy_matrix(st_, ycol, qout);
-        if (d > 0) tri_inverse_small(st_, slot(r_slot), slot(rinv_slot), d, kSmallMax);
-        return d;
+            if (std::fabs(rh[j + j * kSmallMax]) <= kRankTol * mx) return j;
+        return b;
     }
 
     // Blocked right-looking Cholesky of the l x l SPD matrix W (column-major, upper
@@ -923,9 +1021,7 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             s.indicator_enqueue(d, fixed_prec);
             eng.fetch_lazy();
             std::tie(keep, met) = s.indicator_finish();
-            if (attempt == 0 && !eng.lazy_ok()) {
-                if (sharded) throw QbError(kError, "numerically rank-deficient sketch under row sharding (Householder "
-                                                   "panel fallback is single-GPU)");
+            if (attempt == 0 && !eng.lazy_ok()) {  // every rank sees the same (reduced) statuses
                 s.set_e(e_host);  // undo this block's indicator update
                 continue;
             }
@@ -1084,9 +1180,7 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
                 s.indicator_enqueue(d, !fixed);                                    // steps 19-20
                 eng.fetch_lazy();
                 std::tie(keep, met) = s.indicator_finish();
-                if (attempt == 0 && !eng.lazy_ok()) {
-                    if (sharded) throw QbError(kError, "numerically rank-deficient sketch under row sharding "
-                                                       "(Householder panel fallback is single-GPU)");
+                if (attempt == 0 && !eng.lazy_ok()) {  // every rank sees the same (reduced) statuses
                     s.set_e(e_host);
                     continue;
                 }

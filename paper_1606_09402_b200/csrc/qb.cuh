@@ -119,6 +119,12 @@ struct Matrix {
     bool host_stream = false;
     const double* host_a = nullptr;
     std::int64_t host_lda = 0, chunk_rows = 0;
+    // Host-streamed CSR (qbfac_gpu_matrix_csr_stream, CsrRowStream of matrix_handle.cpp:60-73):
+    // row chunks of about chunk_nnz entries are uploaded, validated and multiplied one at a time.
+    const std::int64_t* host_rp = nullptr;
+    const std::int32_t* host_ci = nullptr;
+    const double* host_v = nullptr;
+    std::int64_t chunk_nnz = 0;
     void wait_resident(cudaStream_t s);
 
     ~Matrix();
@@ -141,7 +147,11 @@ std::unique_ptr<Matrix> make_dense_stream(Context& c, std::int64_t m, std::int64
                                           std::int64_t lda, std::int64_t chunk_rows);
 std::unique_ptr<Matrix> make_csr(Context& c, std::int64_t m_global, std::int64_t row0, std::int64_t m,
                                  std::int64_t n, std::int64_t nnz, const std::int64_t* rp,
-                                 const std::int32_t* ci, const double* v);
+                                 const std::int32_t* ci, const double* v, bool allow_hybrid = true);
+// Host-streamed CSR (borrowed host arrays): consumed only by single_pass_fp, chunk by chunk.
+std::unique_ptr<Matrix> make_csr_stream(Context& c, std::int64_t m, std::int64_t n, std::int64_t nnz,
+                                        const std::int64_t* rp, const std::int32_t* ci, const double* v,
+                                        std::int64_t chunk_nnz);
 
 struct Params {
     int alg = 0;          // 0 EI, 1 FP, 2 FP fixed rank, 3 single pass

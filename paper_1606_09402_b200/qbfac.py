@@ -121,6 +121,7 @@ def lib():
         L.qbfac_gpu_matrix_dense_shard.argtypes = [P, I64, I64, I64, I64, P, I64, PP]
         L.qbfac_gpu_matrix_csr.argtypes = [P, I64, I64, I64, P, P, P, PP]
         L.qbfac_gpu_matrix_csr_shard.argtypes = [P, I64, I64, I64, I64, I64, P, P, P, PP]
+        L.qbfac_gpu_matrix_csr_stream.argtypes = [P, I64, I64, I64, P, P, P, I64, PP]
         L.qbfac_gpu_matrix_free.argtypes = [P]
         L.qbfac_gpu_matrix_passes.argtypes = [P]
         L.qbfac_gpu_matrix_passes.restype = I64
@@ -180,7 +181,7 @@ class Context:
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
         L = lib()
         h = C.c_void_p()
-        if world > 1:
+        if world > 1 or nccl_id is not None:
             buf = C.create_string_buffer(bytes(nccl_id), 128)
             st = L.qbfac_gpu_create_dist(device, rank, world, C.cast(buf, C.c_void_p), C.byref(h))
         else:
@@ -415,6 +416,24 @@ class MatrixHandle:
         h = C.c_void_p()
         ctx.check(lib().qbfac_gpu_matrix_csr(ctx.handle, m, n, len(v), _p(rp), _p(ci), _p(v), C.byref(h)))
         return MatrixHandle(h, ctx, m, n, True)
+
+    @staticmethod
+    def csr_stream(m: int, n: int, row_ptr, col_idx, values, ctx: Optional[Context] = None,
+                   chunk_nnz: int = 0) -> "MatrixHandle":
+        """CsrRowStream (matrix_handle.cpp:60-73): A stays in host memory; single_pass_fp
+        uploads and validates row chunks of ~chunk_nnz entries one at a time."""
+        ctx = ctx or default_context()
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        if len(rp) != m + 1 or len(ci) != len(v):
+            raise FormatError("csr: inconsistent structure arrays")
+        h = C.c_void_p()
+        ctx.check(lib().qbfac_gpu_matrix_csr_stream(ctx.handle, m, n, len(v), _p(rp), _p(ci), _p(v), chunk_nnz,
+                                                    C.byref(h)))
+        mh = MatrixHandle(h, ctx, m, n, True)
+        mh._host_ref = (rp, ci, v)
+        return mh
 
     @staticmethod
     def csr_shard(m_global: int, row0: int, n: int, row_ptr, col_idx, values, ctx: Context) -> "MatrixHandle":

@@ -167,6 +167,8 @@ def test_cfg5_full_size_vs_oracle(ctx):
     """Config 5: randQB_EI CSR 2e6 x 5e5, 2e8 nnz Zipf, b=100, P=2, eps=0.6, cap 2000."""
     from paper_1606_09402_b200 import matgen, qbfac
     import oracle_full
+    if not os.path.exists(os.path.join(GOLD, "cfg5_full_avx2.json")):
+        pytest.skip("cfg5 fixture not generated yet (tools/oracle_full.py --cfg 5, ~1 h)")
     ref = _gold("cfg5_full_avx2.json")
     csr = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=2e8, seed=5)
     assert oracle_full.csr_sha(csr) == ref["csr_sha256"]

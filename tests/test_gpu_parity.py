@@ -357,3 +357,75 @@ def test_ei_power_law_hybrid(ctx, oracle, P):
     got = qbfac.rand_qb_ei(qbfac.MatrixHandle.csr(*csr, ctx=ctx), qbfac.StopRule.fixed_precision(eps), 20, P,
                            qbfac.RngStream(11), max_rank=120)
     _compare(got, ref, csr=csr, oracle=oracle)
+
+
+# ---- randQB_FP / single pass on CSR inputs (matrix_handle.cpp:21-34, 60-73) ----------------
+def test_fp_csr_vs_oracle(ctx, oracle):
+    """rand_qb_fp on a resident CSR A (the sketch passes are CSR SpMMs over A and its
+    device-built transpose) against the oracle, within the reference lanes' spread."""
+    from oracle import lanes
+    from paper_1606_09402_b200 import matgen, qbfac
+    csr = matgen.csr_zipf(20000, 5000, alpha=1.1, target_nnz=300000, seed=7)
+    eps = 0.6 * np.sqrt((csr[4] ** 2).sum())
+    kw = dict(b=20, power=1, eps_abs=eps, l_budget=200, max_rank=200, seed=5)
+    ref = oracle.run("fp", csr=csr, **kw)
+    lane = lanes.run_scalar("fp", csr=csr, **kw)
+    got = qbfac.rand_qb_fp(qbfac.MatrixHandle.csr(*csr, ctx=ctx), eps, 20, 1, 200, qbfac.RngStream(5), max_rank=200)
+    _compare(got, ref, csr=csr, oracle=oracle, lane=lane)
+
+
+@pytest.mark.parametrize("stream,chunk", [(False, 0), (True, 0), (True, 20000), (True, 1)])
+def test_single_pass_csr_vs_oracle(ctx, oracle, stream, chunk):
+    """single_pass_fp on CSR: resident, and over the host CsrRowStream (row chunks of ~chunk
+    entries uploaded and validated one at a time; chunk=1 = one row per chunk) — the oracle
+    runs the reference's own CsrRowStream (matrix_handle.cpp:60-73)."""
+    from oracle import lanes
+    from paper_1606_09402_b200 import matgen, qbfac
+    m, n, rp, ci, v = csr = matgen.csr_uniform(3000 if chunk == 1 else 6000, 2500, 30, seed=21)
+    kw = dict(b=20, fixed_rank=(60, 0), seed=7)
+    ref = oracle.run("single_pass", csr=csr, **kw)
+    lane = lanes.run_scalar("single_pass", csr=csr, **kw)
+    h = (qbfac.MatrixHandle.csr_stream(m, n, rp, ci, v, ctx, chunk_nnz=chunk) if stream
+         else qbfac.MatrixHandle.csr(m, n, rp, ci, v, ctx))
+    got = qbfac.single_pass_fp(h, 60, 20, qbfac.RngStream(7))
+    assert got.passes == 1
+    _compare(got, ref, csr=csr, oracle=oracle, lane=lane)
+
+
+def test_csr_stream_errors(ctx):
+    """The CsrRowStream handle: bad row_ptr -> FormatError at creation; a bad column index or a
+    non-finite value in a later chunk -> FormatError / Error when that chunk is uploaded; any
+    consumer other than single_pass_fp -> Error."""
+    from paper_1606_09402_b200 import matgen, qbfac
+    m, n, rp, ci, v = matgen.csr_uniform(2000, 500, 10, seed=2)
+    bad_rp = rp.copy()
+    bad_rp[5] = bad_rp[7]
+    with pytest.raises(qbfac.FormatError):
+        qbfac.MatrixHandle.csr_stream(m, n, bad_rp, ci, v, ctx)
+    ci2 = ci.copy()
+    ci2[15000] = n + 3
+    with pytest.raises(qbfac.FormatError):
+        qbfac.single_pass_fp(qbfac.MatrixHandle.csr_stream(m, n, rp, ci2, v, ctx, chunk_nnz=2000), 20, 10,
+                             qbfac.RngStream(1))
+    v2 = v.copy()
+    v2[19000] = np.inf
+    with pytest.raises(qbfac.Error):
+        qbfac.single_pass_fp(qbfac.MatrixHandle.csr_stream(m, n, rp, ci, v2, ctx, chunk_nnz=2000), 20, 10,
+                             qbfac.RngStream(1))
+    h = qbfac.MatrixHandle.csr_stream(m, n, rp, ci, v, ctx)
+    with pytest.raises(qbfac.Error):
+        qbfac.rand_qb_ei(h, qbfac.StopRule.fixed_precision(1.0), 10, 0, qbfac.RngStream(1))
+
+
+def test_async_upload_non_finite_any_consumer(ctx):
+    """The deferred from_data finiteness check (dense_matrix.cpp:17-18) of an async upload also
+    covers consumers that never form ||A||^2 (a bare multiply, randQB)."""
+    from paper_1606_09402_b200 import qbfac
+    a = _matrix2(200)
+    a[150, 9] = np.inf
+    h = qbfac.MatrixHandle.dense_async(np.asfortranarray(a), ctx)
+    with pytest.raises(qbfac.Error):
+        h.multiply(np.ones((200, 3)), False)
+    h = qbfac.MatrixHandle.dense_async(np.asfortranarray(a), ctx)
+    with pytest.raises(qbfac.Error):
+        qbfac.rand_qb(h, 20, 0, qbfac.RngStream(1))

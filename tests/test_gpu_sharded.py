@@ -108,3 +108,34 @@ def test_sharded_csr_ei_matches_single(world):
         hs.append(qbfac.MatrixHandle.csr_shard(csr[0], r0, csr[1], loc[2], loc[3], loc[4], ctxs[g]))
     shards = _run_ranks(hs, **run)
     _check(a, ref, shards, 1e-10)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("alg", [0, 1])
+def test_sharded_rank_collapse_householder(world, alg, oracle):
+    """Exact rank-15 A with a tiny tolerance: the third block's sketch is numerically rank
+    deficient. Under row sharding the Householder fallback assembles the panel on every rank
+    (exact sum over ranks of zero-padded row blocks), factors it redundantly and keeps the
+    local rows: the run ends rank_collapse exactly like the oracle and the
+    unsharded device run."""
+    rs = np.random.default_rng(0)
+    a = np.asfortranarray(rs.standard_normal((120, 15)) @ rs.standard_normal((15, 90)))
+    eps = 1e-6 * np.linalg.norm(a)
+    run = dict(alg=alg, b=10, power=0, eps_abs=eps, seed=8, max_rank=90)
+    if alg == 1:
+        run["l_budget"] = 40
+    ref = _single(qbfac.MatrixHandle.dense(a, qbfac.default_context()), **run)
+    if alg == 0:
+        o = oracle.run("ei", a, b=10, power=0, eps_abs=eps, seed=8, max_rank=90)
+        assert (ref[0], qbfac.TERMINATION[ref[2]]) == (o.rank, o.terminated_by)
+    assert qbfac.TERMINATION[ref[2]] == "rank_collapse"
+    ctxs = _local_group(world)
+    plan = dist.plan_dense_rows(a.shape[0], world, align=8)
+    hs = [qbfac.MatrixHandle.dense_shard(dist.shard_dense(a, r0, rows), a.shape[0], r0, ctxs[g])
+          for g, (r0, rows) in enumerate(plan)]
+    shards = _run_ranks(hs, **run)
+    for s in shards:
+        assert (s[0], s[1], s[2]) == ref[:3]
+        assert np.array_equal(s[5], shards[0][5])
+    qs = np.vstack([s[4] for s in shards])
+    assert np.linalg.norm(a - qs @ shards[0][5]) <= 1e-10 * np.linalg.norm(a)
