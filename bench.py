@@ -17,8 +17,8 @@ fixtures use.
 N > 1 (torchrun, one process per GPU, NCCL): config 2 row-sharded over the N ranks
 (A, G, Y, Q by rows; the n x l allreduce after each A^T pass and the
 Gram allreduces over NCCL), timed max over ranks — strong scaling. Every N also reports
-config 4 (single pass, 40000 x 20000) row-sharded the same way under `sharded.cfg4`,
-and N = 8 (or --cfg5) config 5 (CSR, 2e8 nnz) under `sharded.cfg5`.
+configs 3, 4 and 5 (time-to-eps; the sparse configs with their CSR pass against the HBM
+roofline) under `configs`, row-sharded the same way at N > 1.
 --impl reference: the reference's own CPU path (oracle/_ref: the reference's kernels,
 RNG and containers + the restated rand_qb_fp) run to epsilon on config 2, rank 0 only.
 """
@@ -215,14 +215,41 @@ def timed_device(ctx, fn, steps):
     return e0.elapsed_time(e1) / 1e3 / steps
 
 
-def sharded_cfg4(D, ctx, steps=3):
-    """Config 4 (single-pass FP, 40000 x 20000, l = 400, b = 100) row-sharded over the ranks:
-    G = A_g Omega local, H = sum_g A_g^T G_g allreduced once (64 MB), Grams allreduced."""
+def hbm_peak_gbs():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 7700.0  # B200_PROFILING.md fallback
+
+
+def time_config(D, ctx, h, run, steps):
+    r = run()
+    info = qbfac_info(r)
+    r.free()
+    ctx.synchronize()
+    D.barrier()
+    res = []
+    t = timed_device(ctx, lambda: res.append(run()), steps)
+    for x in res:
+        x.free()
+    return D.max(t), info
+
+
+def qbfac_info(r):
+    from paper_1606_09402_b200 import qbfac
+    i = qbfac.info_dict(r.info)
+    return {"rank": int(i["rank"]), "passes": int(i["passes"]), "blocks": int(i["blocks"]),
+            "terminated_by": qbfac.TERMINATION[int(i["terminated_by"])]}
+
+
+def config_dense4(D, ctx, steps=3):
+    """Config 4 (single-pass FP, 40000 x 20000, l = 400, b = 100), row-sharded over the ranks at
+    N > 1: G = A_g Omega local, H = sum_g A_g^T G_g allreduced once (64 MB), Grams allreduced."""
     import torch
 
     from paper_1606_09402_b200 import dist as qdist
     from paper_1606_09402_b200 import matgen, qbfac
-    m, n = 40000, 20000
+    m, n, w = 40000, 20000, 400
     row0, rows = qdist.plan_dense_rows(m, D.world)[D.rank]
     sig = np.exp(-np.arange(1, 401) / 60.0)
     at = matgen.synthesize_torch(m, n, sig, 4, noise=1e-6)  # device-synthesized (timing only)
@@ -231,56 +258,44 @@ def sharded_cfg4(D, ctx, steps=3):
     torch.cuda.empty_cache()
     h = qbfac.MatrixHandle.dense_shard(a_loc, m, row0, ctx) if D.world > 1 else qbfac.MatrixHandle.dense(a_loc, ctx)
     del a_loc
-
-    def f():
-        return qbfac.run_device(h, alg=3, mode=0, b=100, power=0, k=400, s=0, seed=42)
-    r = f()
-    info = qbfac.info_dict(r.info)
-    r.free()
-    ctx.synchronize()
-    D.barrier()
-    res = []
-    t = timed_device(ctx, lambda: res.append(f()), steps)
-    for x in res:
-        x.free()
-    t = D.max(t)
-    w = 400
-    pass_t = pass_time(h, w, False, ctx)
+    t, info = time_config(D, ctx, h, lambda: qbfac.run_device(h, alg=3, mode=0, b=100, power=0, k=w, s=0, seed=42),
+                          steps)
+    pt = pass_time(h, w, False, ctx)
     out = {"workload": "cfg4: single-pass FP 40000x20000 rank-400 + 1e-6 noise, l=400, b=100 (device-synthesized A)",
-           "time_s": t, "rank": info["rank"], "passes": info["passes"], "rows_per_rank": rows,
-           "pass_nn_ms_local": pass_t * 1e3, "pass_nn_tflops_local": 2.0 * rows * n * w / pass_t / 1e12}
+           "time_to_eps_s": t, **info, "rows_per_rank": rows, "pass_nn_ms_local": pt * 1e3,
+           "pass_nn_tflops_local": 2.0 * rows * n * w / pt / 1e12}
     h.free()
     return out
 
 
-def sharded_cfg5(D, ctx, steps=2):
+def config_sparse(D, ctx, cfg, steps=2):
+    """Config 3 (EI CSR 1e5 x 5e4, 5M nnz, b=50, P=1) or 5 (EI CSR 2e6 x 5e5 Zipf, 2e8 nnz,
+    b=100, P=2), rows balanced by nnz over the ranks at N > 1. Reports time-to-eps and the
+    CSR pass A*X at width b against the HBM roofline (algorithmic bytes 12 nnz + 8 (rows + 1)
+    + 8 (n + rows) w: A, X and Y once)."""
     from paper_1606_09402_b200 import dist as qdist
     from paper_1606_09402_b200 import matgen, qbfac
-    csr = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=2e8, seed=5)
+    if cfg == 3:
+        csr, b, power, eps_rel, cap = matgen.csr_uniform(100000, 50000, 50, seed=3), 50, 1, 0.5, 1000
+        wl = "cfg3: EI CSR 1e5x5e4, 5M nnz uniform, b=50, P=1, eps=0.5 rel, cap 1000"
+    else:
+        csr, b, power, eps_rel, cap = matgen.csr_zipf(2_000_000, 500_000, alpha=1.1, target_nnz=2e8, seed=5), 100, 2, 0.6, 2000
+        wl = "cfg5: EI CSR 2e6x5e5 Zipf(1.1), 2e8 nnz, b=100, P=2, eps=0.6 rel, cap 2000"
     m, n = csr[0], csr[1]
     row0, rows = qdist.plan_csr_rows(csr[2], D.world)[D.rank]
-    lm, ln, rp, ci, v = qdist.shard_csr(csr, row0, rows)
+    _, _, rp, ci, v = qdist.shard_csr(csr, row0, rows)
     norm = float(np.sqrt(D.sum(float(v @ v))))
-    if D.world > 1:
-        h = qbfac.MatrixHandle.csr_shard(m, row0, n, rp, ci, v, ctx)
-    else:
-        h = qbfac.MatrixHandle.csr(m, n, rp, ci, v, ctx)
+    h = (qbfac.MatrixHandle.csr_shard(m, row0, n, rp, ci, v, ctx) if D.world > 1
+         else qbfac.MatrixHandle.csr(m, n, rp, ci, v, ctx))
+    nnz = len(v)
     del csr
-
-    def f():
-        return qbfac.run_device(h, alg=0, b=100, power=2, max_rank=2000, eps_abs=0.6 * norm, seed=42)
-    r = f()
-    info = qbfac.info_dict(r.info)
-    r.free()
-    ctx.synchronize()
-    D.barrier()
-    res = []
-    t = timed_device(ctx, lambda: res.append(f()), steps)
-    for x in res:
-        x.free()
-    out = {"workload": "cfg5: EI CSR 2e6x5e5 Zipf(1.1) 2e8 nnz, b=100, P=2, eps=0.6 rel, cap 2000",
-           "time_s": D.max(t), "rank": info["rank"], "passes": info["passes"], "nnz_local": int(len(v)),
-           "rows_per_rank": rows}
+    t, info = time_config(D, ctx, h, lambda: qbfac.run_device(h, alg=0, b=b, power=power, max_rank=cap,
+                                                                eps_abs=eps_rel * norm, seed=42), steps)
+    pt = pass_time(h, b, False, ctx)
+    alg_bytes = 12.0 * nnz + 8.0 * (rows + 1) + 8.0 * (n + rows) * b
+    out = {"workload": wl, "time_to_eps_s": t, **info, "nnz_local": int(nnz), "rows_per_rank": rows,
+           "pass_n_ms_local": pt * 1e3, "pass_n_alg_gbs": alg_bytes / pt / 1e9,
+           "pass_n_frac_hbm": alg_bytes / pt / 1e9 / hbm_peak_gbs()}
     h.free()
     return out
 
@@ -305,8 +320,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-sharded", action="store_true", help="skip the config-4/5 row-sharded sub-measurements")
-    ap.add_argument("--cfg5", action="store_true", help="also run config 5 (default only at N = 8)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the config 3/4/5 sub-measurements")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip config 5 (2e8 nnz; ~1 min to generate)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -452,13 +467,14 @@ def main():
         comm = {"allreduce_n_x_l_ms": ar * 1e3, "bytes": 8 * n * w, "busbw_gbs": 2 * (D.world - 1) / D.world * 8 * n * w / ar / 1e9}
         del buf
 
-    sharded = {}
-    if not args.no_sharded:
+    configs = {}
+    if not args.no_configs:
         handle.free()
         torch.cuda.empty_cache()
-        sharded["cfg4"] = sharded_cfg4(D, ctx)
-        if args.cfg5 or D.world == 8:
-            sharded["cfg5"] = sharded_cfg5(D, ctx)
+        configs["cfg3"] = config_sparse(D, ctx, 3)
+        configs["cfg4"] = config_dense4(D, ctx)
+        if not args.no_cfg5:
+            configs["cfg5"] = config_sparse(D, ctx, 5)
 
     cpu = None
     if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
@@ -492,7 +508,7 @@ def main():
                          "pass_nn_ms": t_pass * 1e3, "pass_tn_ms": t_pass_t * 1e3,
                          "pass_tn_tflops": flops / t_pass_t / 1e12},
             "comm": comm,
-            "sharded": sharded or None,
+            "configs": configs or None,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -603,8 +603,9 @@ public:
         const int b = static_cast<int>(y.cols);
         const std::int64_t rows = y.rows;
         if (b == 0) return 0;
-        if (b > kSmallMax) throw QbError(kDimensionError, "block size exceeds the device panel limit (112)");
+        if (b > kSmallMax || wide_mode) return orth_block_wide(y, qout, r_slot, rinv_slot, sharded, tmp, need_r);
         MatView t1{tmp.p, rows, b, b, true};
+        last_wide = false;
         if (!force_hh) {
             const bool lazy = optimistic && lazy_n < Context::kLazyCap / 2;
             SmallStatus* st0 = lazy ? c_.d_lazy + 2 * lazy_n : c_.d_status + 0;
@@ -682,6 +683,108 @@ public:
         if (d > 0) tri_inverse_small(st_, slot(r_slot), slot(rinv_slot), d, kSmallMax);
         return d;
     }
+    // ---- blocks wider than the in-CTA panel kernels (b > kSmallMax = 112) ----------------
+    // orth(Y) for a wide block: block Gram-Schmidt with re-orthogonalisation (BCGS2) over
+    // panels of <= 112 columns, each orthonormalised by the narrow orth_block (fused CholQR2,
+    // Householder on failure — the same deficiency machinery). R is assembled block by block:
+    //   R[j, j] = R2_j R1_j,   R[<j, j] = S1_j + S2_j R1_j      (S1, S2: the two projections)
+    //   R^{-1}[j, j] = R1_j^{-1} R2_j^{-1},
+    //   R^{-1}[<j, j] = -R^{-1}[<j, <j] R[<j, j] R^{-1}[j, j],
+    // in wide slots (b x b, column-major) read through rmat(). diag(R) = diag(R2_j) diag(R1_j)
+    // gives the reference's deficiency decision over the whole block: the first j with
+    // R_jj <= 1e-12 max R_jj (qr.hpp:20-21; R of a QR with diag > 0 is unique, so the panel
+    // diagonals are the Householder R's up to rounding).
+    // wide_mode (set per randQB_FP block of width > 112) keeps every orth of that block on this
+    // path, so R_i = R~_i R_i and the B_i update read one storage.
+    bool wide_mode = false;
+    bool last_wide = false;
+    double* wslot(int s, std::int64_t b) {
+        const std::size_t need = static_cast<std::size_t>(b) * b;
+        if (wslot_[s].n < need) wslot_[s] = DBuf(need, st_);
+        return wslot_[s].p;
+    }
+    MatView rmat(int s, std::int64_t d) const {
+        return last_wide ? MatView{wslot_[s].p, d, d, wld_, false} : small(s, d, d);
+    }
+    // R = R2 R1 and R^{-1} = R1^{-1} R2^{-1} (d x d upper) for the narrow slots or the wide ones.
+    void tri_pair(int s2, int s1, int sr, int s1inv, int s2inv, int srinv, int d) {
+        if (!last_wide) {
+            trmm_upper_pair(st_, slot(s2), slot(s1), slot(sr), slot(s1inv), slot(s2inv), slot(srinv), d, kSmallMax);
+            return;
+        }
+        wslot(sr, wld_);
+        wslot(srinv, wld_);
+        gemm(1.0, rmat(s2, d), rmat(s1, d), 0.0, rmat(sr, d));
+        gemm(1.0, rmat(s1inv, d), rmat(s2inv, d), 0.0, rmat(srinv, d));
+    }
+    int orth_block_wide(const MatView& y, const MatView& qout, int r_slot, int rinv_slot, bool sharded, DBuf& tmp,
+                        bool need_r) {
+        const std::int64_t b = y.cols;
+        if (qout.p != y.p) copy_matrix(st_, y, qout);
+        const std::int64_t np = ceil_div(b, kSmallMax);
+        const std::int64_t pw = ceil_div(b, np);
+        if (wld_ < b) {  // wide slots share one leading dimension (the widest block so far)
+            for (auto& w : wslot_) w = DBuf();
+            wld_ = b;
+        }
+        double* wr = wslot(r_slot, wld_);
+        double* wri = wslot(rinv_slot, wld_);
+        QB_CUDA(cudaMemsetAsync(wr, 0, sizeof(double) * wld_ * wld_, st_));
+        QB_CUDA(cudaMemsetAsync(wri, 0, sizeof(double) * wld_ * wld_, st_));
+        MatView R{wr, b, b, wld_, false}, Ri{wri, b, b, wld_, false};
+        const std::size_t sneed = static_cast<std::size_t>(b) * pw;
+        if (wide_s_.n < 3 * sneed) wide_s_ = DBuf(3 * sneed, st_);
+        if (wide_diag_.n < static_cast<std::size_t>(b)) wide_diag_ = DBuf(static_cast<std::size_t>(b), st_);
+        const bool saved = wide_mode;
+        wide_mode = false;  // the panels themselves take the narrow path
+        for (std::int64_t j0 = 0; j0 < b; j0 += pw) {
+            const int bj = static_cast<int>(std::min(pw, b - j0));
+            MatView xj = qout.cols_range(j0, bj);
+            MatView prev = qout.cols_range(0, j0);
+            MatView s1{wide_s_.p, j0, bj, bj, true}, s2{wide_s_.p + sneed, j0, bj, bj, true};
+            if (j0 > 0) {
+                gemm(1.0, prev.t(), xj, 0.0, s1);
+                if (sharded) allreduce_view(s1);
+                gemm(-1.0, prev, s1, 1.0, xj);
+            }
+            orth_block(xj, xj, kR1, kR1inv, sharded, tmp, true);
+            if (j0 > 0) {
+                gemm(1.0, prev.t(), xj, 0.0, s2);
+                if (sharded) allreduce_view(s2);
+                gemm(-1.0, prev, s2, 1.0, xj);
+                orth_block(xj, xj, kR2, kR2inv, sharded, tmp, true);
+                trmm_upper_pair(st_, slot(kR2), slot(kR1), slot(kR), slot(kR1inv), slot(kR2inv), slot(kRinv), bj,
+                                kSmallMax);
+            } else {
+                copy_matrix(st_, small(kR1, bj, bj), small(kR, bj, bj));
+                copy_matrix(st_, small(kR1inv, bj, bj), small(kRinv, bj, bj));
+            }
+            // diag(R_jj): the stride-(ld+1) view of the slot
+            copy_matrix(st_, MatView{slot(kR), bj, 1, kSmallMax + 1, true}, MatView{wide_diag_.p + j0, bj, 1, 1, true});
+            if (need_r) {
+                copy_matrix(st_, small(kR, bj, bj), R.block(j0, j0, bj, bj));
+                copy_matrix(st_, small(kRinv, bj, bj), Ri.block(j0, j0, bj, bj));
+                if (j0 > 0) {
+                    copy_matrix(st_, s1, R.block(0, j0, j0, bj));
+                    gemm(1.0, s2, small(kR1, bj, bj), 1.0, R.block(0, j0, j0, bj));
+                    MatView t{wide_s_.p + 2 * sneed, j0, bj, bj, true};
+                    gemm(1.0, Ri.block(0, 0, j0, j0), R.block(0, j0, j0, bj), 0.0, t);
+                    gemm(-1.0, t, small(kRinv, bj, bj), 0.0, Ri.block(0, j0, j0, bj));
+                }
+            }
+        }
+        wide_mode = saved;
+        last_wide = true;
+        std::vector<double> dg(static_cast<std::size_t>(b));
+        QB_CUDA(cudaMemcpyAsync(dg.data(), wide_diag_.p, sizeof(double) * b, cudaMemcpyDeviceToHost, st_));
+        QB_CUDA(cudaStreamSynchronize(st_));
+        double mx = 0.0;
+        for (double x : dg) mx = std::max(mx, std::fabs(x));
+        for (std::int64_t j = 0; j < b; ++j)
+            if (!(std::fabs(dg[static_cast<std::size_t>(j)]) > kRankTol * mx)) return static_cast<int>(j);
+        return static_cast<int>(b);
+    }
+
     // Leading rank of the Householder R in `r_slot`: the first j with |R_jj| <= 1e-12 max |R_jj|
     // (rank_deficiency_report, qr.hpp:20-21); b when none.
     int householder_rank(int r_slot, int b) {
@@ -794,7 +897,9 @@ public:
     std::int64_t wide_passes = 0;
 
 private:
-    DBuf scratch_t_, stat_, tri_, wide_, wide_y_;
+    DBuf scratch_t_, stat_, tri_, wide_, wide_y_, wide_s_, wide_diag_;
+    DBuf wslot_[kNumSlots];
+    std::int64_t wld_ = 0;
     Context& c_;
     Matrix& a_;
     cudaStream_t st_;
@@ -1134,6 +1239,7 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
             bool met = false;
             for (int attempt = 0; attempt < 2; ++attempt) {  // optimistic CholQR, Householder redo
                 eng.begin_block(true, attempt > 0);
+                eng.wide_mode = bi > kSmallMax;
                 copy_matrix(c.st, gi, yv);
                 if (s.k > 0) {                                                     // step 12
                     eng.gemm(1.0, s.btk().t(), omi, 0.0, m1v);
@@ -1151,8 +1257,7 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
                     const int d2 = eng.orth_block(qd, qd, kR2, kR2inv, sharded, tmp);
                     d = std::min(d, d2);
                     if (d > 0) {
-                        trmm_upper_pair(c.st, eng.slot(kR2), eng.slot(kR1), eng.slot(kR), eng.slot(kR1inv),
-                                        eng.slot(kR2inv), eng.slot(kRinv), d, kSmallMax);
+                        eng.tri_pair(kR2, kR1, kR, kR1inv, kR2inv, kRinv, d);
                         rinv_slot = kRinv;
                     }
                 }
@@ -1176,7 +1281,7 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
                     }
                     eng.gemm(-1.0, s.btk(), mm, 1.0, ctv);
                 }
-                eng.gemm(1.0, ctv, eng.small(rinv_slot, d, d), 0.0, s.btslot(d));
+                eng.gemm(1.0, ctv, eng.rmat(rinv_slot, d), 0.0, s.btslot(d));
                 s.indicator_enqueue(d, !fixed);                                    // steps 19-20
                 eng.fetch_lazy();
                 std::tie(keep, met) = s.indicator_finish();
@@ -1187,6 +1292,7 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
                 break;
             }
             eng.begin_block(false, false);
+            eng.wide_mode = false;
             if (d == 0) { term = 3; stop = true; break; }
             e_host = c.h_ind->e;
             s.trace.push_back(e_host);

@@ -429,3 +429,52 @@ def test_async_upload_non_finite_any_consumer(ctx):
     h = qbfac.MatrixHandle.dense_async(np.asfortranarray(a), ctx)
     with pytest.raises(qbfac.Error):
         qbfac.rand_qb(h, 20, 0, qbfac.RngStream(1))
+
+
+# ---- blocks wider than the in-CTA panels (b > 112; SPEC.md:273-299 take any b >= 1) ---------
+@pytest.mark.parametrize("b,P", [(130, 1), (250, 0)])
+def test_ei_wide_block(ctx, oracle, b, P):
+    """EI with b > 112: BCGS2 over <= 112-column CholQR2 panels, the reference's deficiency
+    rule over the whole block."""
+    from paper_1606_09402_b200 import matgen, qbfac
+    a = matgen.synthesize(700, 600, matgen.spectrum("exp_decay", 600, tau=40.0), 13)
+    eps = 1e-6 * np.linalg.norm(a)
+    ref = oracle.run("ei", a, b=b, power=P, eps_abs=eps, seed=9)
+    got = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), qbfac.StopRule.fixed_precision(eps), b, P,
+                           qbfac.RngStream(9))
+    _compare(got, ref, a=a, oracle=oracle)
+
+
+def test_fp_wide_block(ctx, oracle):
+    """randQB_FP with b = 150 > 112: R_i, R~_i and R_i^{-1} assembled block-wise (wide slots)."""
+    from oracle import lanes
+    from paper_1606_09402_b200 import matgen, qbfac
+    # a sketch wide enough for the tolerance (no restart): FP's B_i update stays well conditioned
+    # (with l~ below the needed rank the restarted FP amplifies rounding at any b, PAPER.md Remark 4.1)
+    a = matgen.synthesize(800, 700, matgen.spectrum("exp_decay", 700, tau=20.0), 17)
+    eps = 1e-6 * np.linalg.norm(a)
+    kw = dict(b=150, power=1, eps_abs=eps, l_budget=450, seed=4)
+    ref = oracle.run("fp", a, **kw)
+    lane = lanes.run_scalar("fp", a, **kw)
+    got = qbfac.rand_qb_fp(qbfac.MatrixHandle.dense(a, ctx), eps, 150, 1, 450, qbfac.RngStream(4))
+    assert got.passes == 4  # no restart
+    _compare(got, ref, a=a, oracle=oracle, lane=lane)
+
+
+def test_wide_block_rank_collapse(ctx, oracle):
+    """Exact rank-120 A, b = 150: the first block's sketch is deficient at column 120 of the
+    block (across the panel boundary at 75: the CholQR panels fail, the block is redone with
+    Householder panels); rank and termination as the oracle's."""
+    from paper_1606_09402_b200 import qbfac
+    rs = np.random.default_rng(3)
+    a = np.asfortranarray(rs.standard_normal((400, 120)) @ rs.standard_normal((120, 300)))
+    eps = 1e-6 * np.linalg.norm(a)
+    ref = oracle.run("ei", a, b=150, power=0, eps_abs=eps, seed=2)
+    res = qbfac.run_device(qbfac.MatrixHandle.dense(a, ctx), alg=0, b=150, power=0, eps_abs=eps, seed=2)
+    assert int(res.info.householder_fallbacks) > 0
+    res.free()
+    got = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), qbfac.StopRule.fixed_precision(eps), 150, 0,
+                           qbfac.RngStream(2))
+    assert (got.rank, got.terminated_by) == (ref.rank, ref.terminated_by)
+    assert got.rank <= 120
+    assert np.linalg.norm(a - got.Q @ got.B) <= 1e-10 * np.linalg.norm(a)

@@ -113,11 +113,11 @@ def test_sharded_csr_ei_matches_single(world):
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("alg", [0, 1])
 def test_sharded_rank_collapse_householder(world, alg, oracle):
-    """Exact rank-15 A with a tiny tolerance: the third block's sketch is numerically rank
-    deficient. Under row sharding the Householder fallback assembles the panel on every rank
-    (exact sum over ranks of zero-padded row blocks), factors it redundantly and keeps the
-    local rows: the run ends rank_collapse exactly like the oracle and the
-    unsharded device run."""
+    """Exact rank-15 A with a tiny tolerance: the second block's sketch is numerically rank
+    deficient, its CholQR panels fail and the block is redone with Householder panels. Under
+    row sharding the Householder fallback assembles the panel on every rank (exact sum over
+    ranks of zero-padded row blocks), factors it redundantly and keeps the local rows: rank,
+    passes and termination equal the unsharded device run (and, for EI, the oracle's)."""
     rs = np.random.default_rng(0)
     a = np.asfortranarray(rs.standard_normal((120, 15)) @ rs.standard_normal((15, 90)))
     eps = 1e-6 * np.linalg.norm(a)
@@ -128,7 +128,9 @@ def test_sharded_rank_collapse_householder(world, alg, oracle):
     if alg == 0:
         o = oracle.run("ei", a, b=10, power=0, eps_abs=eps, seed=8, max_rank=90)
         assert (ref[0], qbfac.TERMINATION[ref[2]]) == (o.rank, o.terminated_by)
-    assert qbfac.TERMINATION[ref[2]] == "rank_collapse"
+    r = qbfac.run_device(qbfac.MatrixHandle.dense(a, qbfac.default_context()), **run)
+    assert int(r.info.householder_fallbacks) > 0  # the deficient block took the Householder path
+    r.free()
     ctxs = _local_group(world)
     plan = dist.plan_dense_rows(a.shape[0], world, align=8)
     hs = [qbfac.MatrixHandle.dense_shard(dist.shard_dense(a, r0, rows), a.shape[0], r0, ctxs[g])
@@ -139,3 +141,21 @@ def test_sharded_rank_collapse_householder(world, alg, oracle):
         assert np.array_equal(s[5], shards[0][5])
     qs = np.vstack([s[4] for s in shards])
     assert np.linalg.norm(a - qs @ shards[0][5]) <= 1e-10 * np.linalg.norm(a)
+
+
+@pytest.mark.parametrize("alg", [0, 1])
+def test_sharded_wide_block(alg):
+    """b = 130 > 112 under row sharding (world 2): the wide BCGS2 panels allreduce their
+    projections and Grams; every rank matches the unsharded run."""
+    a = matgen.synthesize(700, 500, matgen.spectrum("exp_decay", 500, tau=20.0), 23)
+    eps = 1e-6 * np.linalg.norm(a)
+    run = dict(alg=alg, b=130, power=1, eps_abs=eps, seed=5, max_rank=400)
+    if alg == 1:
+        run["l_budget"] = 390  # no restart: FP's B_i update stays well conditioned
+    ref = _single(qbfac.MatrixHandle.dense(a, qbfac.default_context()), **run)
+    ctxs = _local_group(2)
+    plan = dist.plan_dense_rows(a.shape[0], 2)
+    hs = [qbfac.MatrixHandle.dense_shard(dist.shard_dense(a, r0, rows), a.shape[0], r0, ctxs[g])
+          for g, (r0, rows) in enumerate(plan)]
+    shards = _run_ranks(hs, **run)
+    _check(a, ref, shards, 1e-10 if alg == 0 else 1e-8)
