@@ -1218,6 +1218,151 @@ __global__ void __launch_bounds__(256) jacobi_svd_kernel(JacobiArgs p) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *p.sweeps_out = sweep;
 }
 
+// ---- block one-sided Jacobi (qb_to_svd at large r) -------------------------------------
+// The columns of N are grouped into nblk blocks of nb (nblk even; padding blocks are empty).
+// An outer sweep runs the circle method over the blocks: nblk - 1 steps, each with nblk / 2
+// disjoint block pairs, one CTA per pair. The CTA stages the pair's 2 nb columns of N in shared
+// memory, runs ONE inner one-sided Jacobi sweep over them (circle method on the 2 nb local
+// columns, one warp per disjoint column pair, fixed-order warp dots: deterministic) while
+// accumulating the 2nb x 2nb rotation V, writes the columns back and applies V to the same
+// columns of W (W[:, pair] = W[:, pair] V, row by row). Every pair of global columns meets once
+// per outer sweep; the sweep count of the scalar kernel drops by the inner sweeps, and each grid
+// barrier now covers nb^2 more rotations (r = 1000: 125 barriers per sweep instead of 999).
+struct JacobiBlockArgs {
+    double* nmat;
+    double* w;
+    int r, nb, nblk, max_sweeps;
+    double tol;
+    unsigned* gbar;
+    unsigned* rotated;
+    int* sweeps_out;
+};
+
+__device__ __forceinline__ void circle_pair(int round, int t, int n, int& a, int& b) {
+    if (t == 0) {
+        a = round;
+        b = n - 1;
+    } else {
+        a = (round + t) % (n - 1);
+        b = (round - t + (n - 1)) % (n - 1);
+    }
+    if (a > b) { const int x = a; a = b; b = x; }
+}
+
+constexpr int kJbMaxCols = 16;  // 2 nb <= 16
+
+__global__ void __launch_bounds__(256) jacobi_block_kernel(JacobiBlockArgs p) {
+    extern __shared__ __align__(16) double jsm[];
+    const int r = p.r, nb = p.nb, nc = 2 * nb;
+    double* cols = jsm;                                   // nc columns of r (column c at cols + c r)
+    double* V = jsm + static_cast<std::size_t>(nc) * r;  // nc x nc, column-major
+    __shared__ unsigned s_cnt;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+    const int half = p.nblk / 2;
+    int sweep = 0;
+    for (; sweep < p.max_sweeps; ++sweep) {
+        for (int step = 0; step < p.nblk - 1; ++step) {
+            for (int t = blockIdx.x; t < half; t += gridDim.x) {
+                int bi, bj;
+                circle_pair(step, t, p.nblk, bi, bj);
+                const int i0 = bi * nb, j0 = bj * nb;
+                const int ni = max(0, min(nb, r - i0)), nj = max(0, min(nb, r - j0));
+                auto gcol = [&](int c) -> int {  // local column -> global column (-1: empty)
+                    return c < nb ? (c < ni ? i0 + c : -1) : (c - nb < nj ? j0 + c - nb : -1);
+                };
+                // 8 loads in flight per thread (a load -> store chain per element serialises on L2 latency)
+                for (int base = tid; base < nc * r; base += 8 * blockDim.x) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int idx = base + u * blockDim.x;
+                        v[u] = 0.0;
+                        if (idx < nc * r) {
+                            const int c = idx / r, g = gcol(c);
+                            if (g >= 0) v[u] = p.nmat[static_cast<std::int64_t>(g) * r + (idx - c * r)];
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int idx = base + u * blockDim.x;
+                        if (idx < nc * r) cols[idx] = v[u];
+                    }
+                }
+                for (int idx = tid; idx < nc * nc; idx += blockDim.x) V[idx] = (idx % nc == idx / nc) ? 1.0 : 0.0;
+                if (tid == 0) s_cnt = 0;
+                __syncthreads();
+                for (int rd = 0; rd < nc - 1; ++rd) {
+                    for (int q = warp; q < nb; q += nwarps) {
+                        int a, b;
+                        circle_pair(rd, q, nc, a, b);
+                        double* ca = cols + static_cast<std::size_t>(a) * r;
+                        double* cb = cols + static_cast<std::size_t>(b) * r;
+                        double al = 0.0, be = 0.0, ga = 0.0;
+                        for (int i = lane; i < r; i += 32) {
+                            const double x = ca[i], y = cb[i];
+                            al = fma(x, x, al);
+                            be = fma(y, y, be);
+                            ga = fma(x, y, ga);
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            al += __shfl_xor_sync(0xffffffffu, al, o);
+                            be += __shfl_xor_sync(0xffffffffu, be, o);
+                            ga += __shfl_xor_sync(0xffffffffu, ga, o);
+                        }
+                        if (!(fabs(ga) > p.tol * sqrt(al * be))) continue;
+                        const double zeta = (be - al) / (2.0 * ga);
+                        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                        const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+                        for (int i = lane; i < r; i += 32) {
+                            const double x = ca[i], y = cb[i];
+                            ca[i] = c * x - sn * y;
+                            cb[i] = sn * x + c * y;
+                        }
+                        if (lane < nc) {
+                            const double x = V[lane + a * nc], y = V[lane + b * nc];
+                            V[lane + a * nc] = c * x - sn * y;
+                            V[lane + b * nc] = sn * x + c * y;
+                        }
+                        if (lane == 0) atomicAdd(&s_cnt, 1u);
+                    }
+                    __syncthreads();
+                }
+                for (int idx = tid; idx < nc * r; idx += blockDim.x) {
+                    const int c = idx / r, i = idx - c * r, g = gcol(c);
+                    if (g >= 0) p.nmat[static_cast<std::int64_t>(g) * r + i] = cols[idx];
+                }
+                if (s_cnt) {
+                    for (int i = tid; i < r; i += blockDim.x) {
+                        double wv[kJbMaxCols];
+#pragma unroll
+                        for (int c = 0; c < kJbMaxCols; ++c) {
+                            const int g = c < nc ? gcol(c) : -1;
+                            wv[c] = g >= 0 ? p.w[static_cast<std::int64_t>(g) * r + i] : 0.0;
+                        }
+#pragma unroll
+                        for (int c = 0; c < kJbMaxCols; ++c) {
+                            if (c >= nc) break;
+                            const int g = gcol(c);
+                            if (g < 0) continue;
+                            double acc = 0.0;
+#pragma unroll
+                            for (int k = 0; k < kJbMaxCols; ++k)
+                                if (k < nc) acc = fma(wv[k], V[k + c * nc], acc);
+                            p.w[static_cast<std::int64_t>(g) * r + i] = acc;
+                        }
+                    }
+                    if (tid == 0) atomicAdd(p.rotated + sweep, s_cnt);
+                }
+                __syncthreads();
+            }
+            grid_barrier(p.gbar, gridDim.x);
+        }
+        if (*reinterpret_cast<volatile unsigned*>(p.rotated + sweep) == 0) break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.sweeps_out = sweep;
+}
+
 // C = A * B for upper-triangular n x n operands staged in shared memory; blockIdx.x
 // selects one of two independent products so R = Rb*Ra and Rinv = Ra^{-1} Rb^{-1}
 // are formed in one launch.
@@ -1655,9 +1800,36 @@ int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, 
     QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rotated), sizeof(unsigned) * (max_sweeps + 1) + sizeof(int), st));
     sweeps = reinterpret_cast<int*>(rotated + max_sweeps + 1);
     QB_CUDA(cudaMemsetAsync(rotated, 0, sizeof(unsigned) * (max_sweeps + 1) + sizeof(int), st));
-    JacobiArgs a{nmat, w, r, rp, max_sweeps, 1e-15, gbar, rotated, sweeps};
-    void* args[] = {&a};
-    QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_svd_kernel), grid, 256, args, 0, st));
+    // block Jacobi when 2 nb columns of N fit in shared memory (nb = 8, 4, 2 or 1)
+    int nb = 0;
+    const char* nb_env = std::getenv("QBFAC_JACOBI_NB");
+    const int nb_max = nb_env ? std::max(1, std::min(8, std::atoi(nb_env))) : 8;
+    for (int cand : {8, 4, 2, 1})
+        if (cand <= nb_max && (2 * cand * static_cast<std::int64_t>(r) + 4 * cand * cand) * 8 <= 200 * 1024 &&
+            r > 2 * cand) {
+            nb = cand;
+            break;
+        }
+    const char* force_scalar = std::getenv("QBFAC_JACOBI_SCALAR");
+    if (nb > 0 && !(force_scalar && force_scalar[0] == '1')) {
+        const int nblk = static_cast<int>(2 * ceil_div(ceil_div(r, nb), 2));
+        const int smem = static_cast<int>((2 * nb * static_cast<std::int64_t>(r) + 4 * nb * nb) * 8);
+        static PerDevice<bool> setup;
+        setup.get([] {
+            QB_CUDA(cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            return true;
+        });
+        int per_sm = 0;
+        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_block_kernel, 256, smem));
+        const int gb = std::max(1, std::min(nblk / 2, std::max(per_sm, 1) * gemm_num_sms()));
+        JacobiBlockArgs a{nmat, w, r, nb, nblk, max_sweeps, 1e-15, gbar, rotated, sweeps};
+        void* args[] = {&a};
+        QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_block_kernel), gb, 256, args, smem, st));
+    } else {
+        JacobiArgs a{nmat, w, r, rp, max_sweeps, 1e-15, gbar, rotated, sweeps};
+        void* args[] = {&a};
+        QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_svd_kernel), grid, 256, args, 0, st));
+    }
     QB_LAUNCH_CHECK();
     int h = 0;
     QB_CUDA(cudaMemcpyAsync(&h, sweeps, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -529,14 +529,18 @@ class TruncatedSvd:
 class DeviceResult:
     """Result resident on the device; Q/B are copied to the host on demand."""
 
-    def svd(self, k: Optional[int] = None) -> TruncatedSvd:
+    def svd(self, k: Optional[int] = None, u_out: Optional[np.ndarray] = None,
+            v_out: Optional[np.ndarray] = None) -> TruncatedSvd:
         """qb_to_svd(f, k) on the device: orth(B^T), one-sided Jacobi of the
-        r x r factor, U = Q U_r, V = Q_b W."""
+        r x r factor, U = Q U_r, V = Q_b W. `u_out` / `v_out`: caller buffers (e.g. pinned),
+        column-major m x k / n x k."""
         k = self.rank if k is None else k
         m, n = int(self.info.m), int(self.info.n)
-        u = np.zeros((m, k), order="F")
+        u = np.zeros((m, k), order="F") if u_out is None else u_out
         sv = np.zeros(k)
-        v = np.zeros((n, k), order="F")
+        v = np.zeros((n, k), order="F") if v_out is None else v_out
+        if u.shape != (m, k) or v.shape != (n, k) or not (u.flags.f_contiguous and v.flags.f_contiguous):
+            raise DimensionError("svd: output buffers must be column-major m x k / n x k")
         sw = C.c_int(0)
         self.ctx.check(lib().qbfac_gpu_result_svd(self._h, k, _p(u), max(m, 1), _p(sv), _p(v), max(n, 1),
                                                   C.byref(sw)))

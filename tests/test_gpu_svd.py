@@ -56,3 +56,28 @@ def test_k_too_large(ctx):
     r = qbfac.run_device(qbfac.MatrixHandle.dense(a, ctx), alg=0, mode=0, b=10, k=20, s=0, seed=1)
     with pytest.raises(qbfac.DimensionError):
         r.svd(21)
+
+
+@pytest.mark.parametrize("rank", [600, 1000])
+def test_block_jacobi_large_rank(ctx, rank):
+    """qb_to_svd at rank 600 / 1000 (block one-sided Jacobi: nb = 8 column blocks, one inner sweep
+    per block pair): S equals the SVD of B to 1e-12 relative, U and V orthonormal, U S V^T = Q B,
+    and the scalar Jacobi (QBFAC_JACOBI_SCALAR=1) agrees."""
+    import os
+    from paper_1606_09402_b200 import matgen, qbfac
+    csr = matgen.csr_uniform(6000, 3000, 30, seed=8)
+    r = qbfac.run_device(qbfac.MatrixHandle.csr(*csr, ctx=ctx), alg=0, mode=0, b=50, power=1, k=rank, s=0, seed=2)
+    t = r.svd(rank)
+    b = r.b()
+    sb = np.linalg.svd(b, compute_uv=False)
+    assert np.max(np.abs(t.S - sb) / sb) <= 1e-12
+    assert np.abs(t.U.T @ t.U - np.eye(rank)).max() <= 1e-10
+    assert np.abs(t.V.T @ t.V - np.eye(rank)).max() <= 1e-10
+    qb = r.q() @ b
+    assert np.linalg.norm(t.U @ np.diag(t.S) @ t.V.T - qb) <= 1e-10 * np.linalg.norm(qb)
+    os.environ["QBFAC_JACOBI_SCALAR"] = "1"
+    try:
+        t2 = r.svd(rank)
+    finally:
+        os.environ.pop("QBFAC_JACOBI_SCALAR")
+    assert np.max(np.abs(t2.S - t.S) / t.S) <= 1e-12
