@@ -279,7 +279,7 @@ __device__ __forceinline__ void chol_mark(int slot, bool on = true) {
     if (on && blockIdx.x == 0 && threadIdx.x == 0) g_chol_trace[slot] = clock64();
 }
 
-template <int BP>
+template <int BP, bool SRC_SHARED = false>
 __device__ __forceinline__ void chol_tile_block(const double* __restrict__ gsrc, std::int64_t ldg, int b,
                                              double* __restrict__ r, double* __restrict__ rinv, std::int64_t ldr,
                                              SmallStatus* status, double* sm, bool trace = true) {
@@ -303,7 +303,10 @@ __device__ __forceinline__ void chol_tile_block(const double* __restrict__ gsrc,
         for (int q = 0; q < 8; ++q) {
             const int idx = base + q * nthr + tid;
             const int j = idx / BP, i = idx - j * BP;
-            v[q] = (idx < BP * BP && i <= j && j < b) ? __ldcg(gsrc + i + static_cast<std::int64_t>(j) * ldg) : 0.0;
+            if constexpr (SRC_SHARED)
+                v[q] = (idx < BP * BP && i <= j && j < b) ? gsrc[i + static_cast<std::int64_t>(j) * ldg] : 0.0;
+            else
+                v[q] = (idx < BP * BP && i <= j && j < b) ? __ldcg(gsrc + i + static_cast<std::int64_t>(j) * ldg) : 0.0;
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -1142,6 +1145,227 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
     panel_mark(10);
 }
 
+// ---- CholQR2 of a small panel in ONE thread-block cluster -------------------------------
+// Panels with b <= 32 and rows <= 8 x 512 (config 1's 2000 x 20 sketches, the re-orthogonalised
+// Q_i of every small block): the cluster's C <= 8 CTAs each keep their row slice of Y resident in
+// shared memory for the whole factorization (Y is read from HBM once, Q written once). The b x b
+// partial Grams are summed over the cluster through distributed shared memory in rank order (the
+// same bits in every CTA), and every CTA factors the reduced Gram itself (the in-CTA blocked
+// Cholesky + inverse on a shared-memory source), so no grid barrier, no global partials and no
+// broadcast of R are needed; CTA 0 publishes R_a, R_a^{-1}, R_b, R_b^{-1}, the Gram and the two
+// statuses exactly as cholqr2_panel_kernel does (same one-pass rule for a near-identity Gram).
+constexpr int kClusterRowsPerCta = 512;
+constexpr int kClusterMaxCtas = 8;
+
+template <int BP>
+struct ClusterPanelCfg {
+    using P = PanelCfg<BP>;
+    static constexpr int LD = P::LD;
+    static constexpr int YS = kClusterRowsPerCta * LD;      // resident row slice
+    static constexpr int SQ = BP * BP;
+    static constexpr int DOUBLES = YS + 4 * SQ + BP * LD + CholCfg<BP>::SMEM_DOUBLES;
+    static constexpr int SMEM = DOUBLES * 8;
+};
+
+template <int BP>
+__global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_constant__ PanelArgs p, int rr) {
+    pdl_wait();
+    using C = PanelCfg<BP>;
+    using K = ClusterPanelCfg<BP>;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int crank = static_cast<int>(cluster.block_rank()), ncta = static_cast<int>(cluster.num_blocks());
+    extern __shared__ __align__(128) double csm[];
+    double* ys = csm;                       // rr_pad x LD rows of Y (then T)
+    double* gpart = ys + K::YS;              // this CTA's partial Gram (BP x BP, col-major)
+    double* gsum = gpart + K::SQ;            // the reduced Gram (identical in every CTA)
+    double* rloc = gsum + K::SQ;             // R (col-major, ld BP)
+    double* rinvloc = rloc + K::SQ;          // R^{-1}
+    double* rs = rinvloc + K::SQ;            // R^{-1} staged for the triangular products (BP x LD)
+    double* ws = rs + BP * K::LD;            // in-CTA Cholesky workspace
+    __shared__ SmallStatus sst;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const std::int64_t r0 = static_cast<std::int64_t>(crank) * rr;
+    const std::int64_t left = p.rows - r0;
+    const int nr = left <= 0 ? 0 : static_cast<int>(left < rr ? left : rr);
+    const int nsub = (nr + C::SUB - 1) / C::SUB;
+    const int b = p.b;
+    // load the slice (zero-padded to whole sub-tiles and to BP columns)
+    for (int base = tid; base < nsub * C::SUB * BP; base += 4 * blockDim.x) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int idx = base + u * blockDim.x, i = idx / BP, c = idx - i * BP;
+            v[u] = (idx < nsub * C::SUB * BP && i < nr && c < b) ? p.y[(r0 + i) * p.ldy + c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int idx = base + u * blockDim.x, i = idx / BP, c = idx - i * BP;
+            if (idx < nsub * C::SUB * BP) ys[i * K::LD + c] = v[u];
+        }
+    }
+    // this warp's upper Gram fragments (as cholqr2_panel_kernel)
+    int fm[C::MAXG], fn[C::MAXG];
+#pragma unroll
+    for (int f = 0; f < C::MAXG; ++f) {
+        int e = warp + 8 * f, mi = 0;
+        fm[f] = -1;
+        fn[f] = 0;
+        const int nb8 = (b + 7) >> 3;
+        int nf = 0;
+        for (int m2 = 0; m2 < BP / 16; ++m2) nf += max(0, nb8 - 2 * m2);
+        if (e >= nf) continue;
+        while (e >= nb8 - 2 * mi) { e -= nb8 - 2 * mi; ++mi; }
+        fm[f] = mi;
+        fn[f] = 2 * mi + e;
+    }
+    int nvf = 0;
+#pragma unroll
+    for (int f = 0; f < C::MAXG; ++f) nvf += fm[f] >= 0 ? 1 : 0;
+    double acc[C::MAXG][C::KSG][4];
+    auto zero_acc = [&]() {
+#pragma unroll
+        for (int f = 0; f < C::MAXG; ++f)
+#pragma unroll
+            for (int c = 0; c < C::KSG; ++c)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[f][c][e] = 0.0;
+    };
+    // partial Gram -> gpart; cluster-wide fixed-order sum -> gsum (every CTA); factor -> rloc, rinvloc
+    auto gram_reduce_factor = [&](SmallStatus* st_out, double* r_out, double* rinv_out, bool first) {
+        for (int idx = tid; idx < K::SQ; idx += blockDim.x) gpart[idx] = 0.0;
+        __syncthreads();
+#pragma unroll
+        for (int f = 0; f < C::MAXG; ++f) {
+            if (fm[f] < 0) continue;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int row = 16 * fm[f] + g + (e >= 2 ? 8 : 0), col = 8 * fn[f] + 2 * t + (e & 1);
+                double v = acc[f][0][e];
+#pragma unroll
+                for (int c = 1; c < C::KSG; ++c) v += acc[f][c][e];
+                gpart[row + col * BP] = v;
+            }
+        }
+        cluster.sync();
+        for (int idx = tid; idx < K::SQ; idx += blockDim.x) {
+            const int i = idx % BP, j = idx / BP;
+            double sum = 0.0;
+            if (i <= j && j < b)
+                for (int c = 0; c < ncta; ++c) sum += cluster.map_shared_rank(gpart, c)[idx];
+            gsum[idx] = sum;
+        }
+        cluster.sync();  // every CTA has read every partial before any gpart is reused
+        chol_tile_block<BP, true>(gsum, BP, b, rloc, rinvloc, BP, &sst, ws, false);
+        if (crank == 0) {
+            for (int idx = tid; idx < b * b; idx += blockDim.x) {
+                const int i = idx % b, j = idx / b;
+                r_out[i + j * kSmallMax] = rloc[i + j * BP];
+                rinv_out[i + j * kSmallMax] = rinvloc[i + j * BP];
+                if (first) p.g[i + j * kSmallMax] = gsum[i + j * BP];
+            }
+            if (tid == 0) *st_out = sst;
+        }
+        __syncthreads();
+    };
+    auto stage_r = [&]() {
+        for (int idx = tid; idx < BP * BP; idx += blockDim.x) {
+            const int k = idx / BP, n = idx - k * BP;
+            rs[k * K::LD + n] = (k < b && n < b && k <= n) ? rinvloc[k + n * BP] : 0.0;
+        }
+        __syncthreads();
+    };
+    // out rows of this slice = ys * rs, to global (q) or back into ys
+    auto product = [&](bool to_q, bool gram_after) {
+        for (int sub = 0; sub < nsub; ++sub) {
+            double* cur = ys + sub * C::SUB * K::LD;
+            double tacc[C::MAXT][4];
+            panel_trmm<BP>(cur, rs, tacc, b);
+            __syncthreads();
+            const int mi = warp % C::MI, h = warp / C::MI;
+#pragma unroll
+            for (int j = 0; j < C::MAXT; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int row = 16 * mi + g + (e >= 2 ? 8 : 0), col = 8 * (h + C::NG * j) + 2 * t + (e & 1);
+                    if (col >= BP) continue;
+                    if (to_q) {
+                        const std::int64_t gr = r0 + sub * C::SUB + row;
+                        if (sub * C::SUB + row < nr && col < b) p.q[gr * p.ldq + col] = tacc[j][e];
+                    } else {
+                        cur[row * K::LD + col] = tacc[j][e];
+                    }
+                }
+            __syncthreads();
+            if (gram_after) panel_gram<BP>(cur, acc, fm, fn, nvf);
+        }
+    };
+    __syncthreads();
+    // ---- Gram of Y, R_a
+    zero_acc();
+    for (int sub = 0; sub < nsub; ++sub) panel_gram<BP>(ys + sub * C::SUB * K::LD, acc, fm, fn, nvf);
+    gram_reduce_factor(p.st0, p.ra, p.rainv, true);
+    const bool one_pass = sst.gram_dev <= kFirstOrderDev && sst.breakdown == 0;
+    stage_r();
+    if (one_pass) {  // near-orthonormal Y: Q = Y R_a^{-1}, R_b = I (as the panel kernel)
+        product(true, false);
+        if (crank == 0) {
+            for (int idx = tid; idx < b * b; idx += blockDim.x) {
+                const int i = idx % b, j = idx / b;
+                p.rb[i + j * kSmallMax] = i == j ? 1.0 : 0.0;
+                p.rbinv[i + j * kSmallMax] = i == j ? 1.0 : 0.0;
+            }
+            if (tid == 0) {
+                p.st1->breakdown = 0;
+                p.st1->bad_index = -1;
+                p.st1->diag_min = 1.0;
+                p.st1->diag_max = 1.0;
+                p.st1->gram_dev = 0.0;
+            }
+        }
+        return;
+    }
+    // ---- T = Y R_a^{-1} (kept in shared memory) and its Gram, R_b
+    zero_acc();
+    product(false, true);
+    gram_reduce_factor(p.st1, p.rb, p.rbinv, false);
+    stage_r();
+    // ---- Q = T R_b^{-1}
+    product(true, false);
+}
+
+template <int BP>
+void launch_cholqr2_cluster(cudaStream_t st, PanelArgs& a) {
+    using K = ClusterPanelCfg<BP>;
+    auto kern = cholqr2_cluster_kernel<BP>;
+    static PerDevice<bool> setup;
+    setup.get([&] {
+        QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
+        return true;
+    });
+    const int ncta = static_cast<int>(std::min<std::int64_t>(kClusterMaxCtas, std::max<std::int64_t>(1, ceil_div(a.rows, 128))));
+    const int rr = static_cast<int>(ceil_div(a.rows, ncta));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(ncta));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = K::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = static_cast<unsigned>(ncta);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    QB_CUDA(cudaLaunchKernelEx(&cfg, kern, a, rr));
+}
+
+bool cluster_panel_enabled() {
+    const char* e = std::getenv("QBFAC_PANEL_CLUSTER");
+    return !(e && e[0] == '0');
+}
+
 // ---- one-sided Jacobi SVD of a small square matrix (qb_to_svd) ---------
 // Hestenes one-sided Jacobi on the columns of N (r x r, column-major): rotations from the
 // right orthogonalise the columns, N W = U Sigma, W accumulates the rotations (W starts as
@@ -1769,6 +1993,13 @@ void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t
     PanelArgs a{};
     a.y = y; a.ldy = ldy; a.t1 = t1; a.q = q; a.ldq = ldq; a.rows = rows; a.b = b;
     a.g = g; a.ra = ra; a.rainv = rainv; a.rb = rb; a.rbinv = rbinv; a.st0 = st0; a.st1 = st1; a.gbar = gbar;
+    if (bp <= 32 && rows > 0 && rows <= static_cast<std::int64_t>(kClusterMaxCtas) * kClusterRowsPerCta &&
+        cluster_panel_enabled()) {
+        if (bp == 16) launch_cholqr2_cluster<16>(st, a);
+        else launch_cholqr2_cluster<32>(st, a);
+        QB_LAUNCH_CHECK();
+        return;
+    }
     const int cap = gemm_num_sms();
     a.part = ws.get(static_cast<std::size_t>(cap) * bp * bp);
     switch (bp) {

@@ -215,12 +215,17 @@ def test_chol_small_breakdown(ctx):
     assert status.value == 1
 
 
+@pytest.mark.parametrize("cluster", ["1", "0"])
 @pytest.mark.parametrize("rows,b,ldy", [(1, 1, 1), (40, 7, 9), (100, 16, 16), (5000, 33, 40), (100001, 50, 50),
-                                        (3000, 64, 64), (3000, 65, 70), (20000, 100, 100), (777, 112, 112)])
-def test_cholqr2_panel(ctx, rows, b, ldy):
+                                        (3000, 64, 64), (3000, 65, 70), (20000, 100, 100), (777, 112, 112),
+                                        (2000, 20, 20), (4096, 32, 40), (513, 17, 17), (4000, 30, 31)])
+def test_cholqr2_panel(ctx, rows, b, ldy, cluster, monkeypatch):
     """Fused one-launch CholQR2: Q orthonormal, Y = Q R with R upper and diag(R) > 0 (the
     QR factor numpy/LAPACK returns up to signs), R R^{-1} = I; rows beyond a sub-tile,
-    widths off the 16-column padding and strided rows included."""
+    widths off the 16-column padding and strided rows included. cluster=1: panels with b <= 32 and
+    rows <= 4096 take the one-cluster kernel (slices resident in shared memory, DSMEM Gram
+    reduction); cluster=0 forces the grid-wide kernel for the same inputs."""
+    monkeypatch.setenv("QBFAC_PANEL_CLUSTER", cluster)
     L = _lib()
     L.qbfac_gpu_test_cholqr2.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_void_p,
                                          C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
