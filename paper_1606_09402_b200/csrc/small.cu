@@ -360,8 +360,15 @@ __device__ __forceinline__ void chol_tile_block(const double* __restrict__ gsrc,
                 for (int i = 0; i < 16; ++i)
                     x[i] = left ? W[(c0 + min(i, j)) * C::LD + c0 + max(i, j)] : (i == j ? 1.0 : 0.0);
                 double pv[16];
+                // pivots past b (identity padding) are no-op steps: their column of D is e_k, so every
+                // multiplier is 0 and the pivot is 1 (b = 20: 4 steps in the second panel, not 16)
+                const int nval = min(16, b - c0);
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
+                    if (k >= nval) {
+                        pv[k] = 1.0;
+                        continue;
+                    }
                     double piv = __shfl_sync(0xffffffffu, x[k], k);
                     const bool bad = !(piv > 0.0) || !isfinite(piv);
                     if (bad) {
@@ -1170,6 +1177,7 @@ struct ClusterPanelCfg {
 template <int BP>
 __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_constant__ PanelArgs p, int rr) {
     pdl_wait();
+    panel_mark(0);
     using C = PanelCfg<BP>;
     using K = ClusterPanelCfg<BP>;
     cg::cluster_group cluster = cg::this_cluster();
@@ -1189,20 +1197,19 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
     const int nr = left <= 0 ? 0 : static_cast<int>(left < rr ? left : rr);
     const int nsub = (nr + C::SUB - 1) / C::SUB;
     const int b = p.b;
-    // load the slice (zero-padded to whole sub-tiles and to BP columns)
-    for (int base = tid; base < nsub * C::SUB * BP; base += 4 * blockDim.x) {
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int idx = base + u * blockDim.x, i = idx / BP, c = idx - i * BP;
-            v[u] = (idx < nsub * C::SUB * BP && i < nr && c < b) ? p.y[(r0 + i) * p.ldy + c] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int idx = base + u * blockDim.x, i = idx / BP, c = idx - i * BP;
-            if (idx < nsub * C::SUB * BP) ys[i * K::LD + c] = v[u];
+    // load the slice (zero-padded to whole sub-tiles and to BP columns): every element an 8-byte
+    // cp.async straight into shared memory, all in flight at once (no register round trip)
+    for (int idx = tid; idx < nsub * C::SUB * BP; idx += blockDim.x) {
+        const int i = idx / BP, c = idx - i * BP;
+        double* dst = ys + i * K::LD + c;
+        if (i < nr && c < b) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sm_addr(dst)), "l"(p.y + (r0 + i) * p.ldy + c)
+                         : "memory");
+        } else {
+            *dst = 0.0;
         }
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     // this warp's upper Gram fragments (as cholqr2_panel_kernel)
     int fm[C::MAXG], fn[C::MAXG];
 #pragma unroll
@@ -1247,6 +1254,7 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
             }
         }
         cluster.sync();
+        panel_mark(first ? 2 : 6);
         for (int idx = tid; idx < K::SQ; idx += blockDim.x) {
             const int i = idx % BP, j = idx / BP;
             double sum = 0.0;
@@ -1255,6 +1263,7 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
             gsum[idx] = sum;
         }
         cluster.sync();  // every CTA has read every partial before any gpart is reused
+        panel_mark(first ? 3 : 7);
         chol_tile_block<BP, true>(gsum, BP, b, rloc, rinvloc, BP, &sst, ws, false);
         if (crank == 0) {
             for (int idx = tid; idx < b * b; idx += blockDim.x) {
@@ -1266,6 +1275,8 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
             if (tid == 0) *st_out = sst;
         }
         __syncthreads();
+        panel_mark(first ? 4 : 8);
+        panel_mark(first ? 5 : 9);
     };
     auto stage_r = [&]() {
         for (int idx = tid; idx < BP * BP; idx += blockDim.x) {
@@ -1303,6 +1314,7 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
     // ---- Gram of Y, R_a
     zero_acc();
     for (int sub = 0; sub < nsub; ++sub) panel_gram<BP>(ys + sub * C::SUB * K::LD, acc, fm, fn, nvf);
+    panel_mark(1);
     gram_reduce_factor(p.st0, p.ra, p.rainv, true);
     const bool one_pass = sst.gram_dev <= kFirstOrderDev && sst.breakdown == 0;
     stage_r();
@@ -1322,6 +1334,7 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
                 p.st1->gram_dev = 0.0;
             }
         }
+        panel_mark(11);
         return;
     }
     // ---- T = Y R_a^{-1} (kept in shared memory) and its Gram, R_b
@@ -1331,6 +1344,7 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
     stage_r();
     // ---- Q = T R_b^{-1}
     product(true, false);
+    panel_mark(10);
 }
 
 template <int BP>
