@@ -370,6 +370,7 @@ bool dispatch_ws(int fam, cudaStream_t st, const MatView& a, const MatView& b, d
     else if (fam == 3) launch_ws<128, 56, 32, 8, 1, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
     else if (fam == 4) launch_ws<128, 80, 32, 4, 2, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
     else if (fam == 5) launch_ws<128, 112, 32, 4, 2, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
+    else if (fam == 6) launch_ws<128, 104, 32, 8, 1, 3, AR, BR, NP>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
     else launch_ws<64, 32, 32, 2, 2, 4, AR, BR, 2>(st, a, b, c, ldc, c_row, M, N, K, splits, klen, alpha, beta, partial, flags, tws);
     return true;
 }
@@ -510,6 +511,13 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     if (ws_path) bk = 32;  // the warp-specialised kernels use BK = 32 in every family
     // b = 100: 112-column tiles (14 n8 fragments, 12 % padding) instead of 128 (28 %)
     if (ws_path && fam == Family::kWide && N > 96 && N <= 112) bn = 112;
+    // b = 97..104: 104-column tiles (13 n8 fragments, 8 x 1 warps of 16 x 104): 4 % padding at b = 100
+    // instead of 12 % (QBFAC_GEMM_104=0 keeps the 112-column tile)
+    static const bool use104 = [] {
+        const char* e = std::getenv("QBFAC_GEMM_104");
+        return !(e && e[0] == '0');
+    }();
+    if (ws_path && fam == Family::kWide && N > 96 && N <= 104 && use104 && !(flags & kGemmUpperC)) bn = 104;
     if (ws_path && fam == Family::kSkinny56 && !a.rowmajor) bn = 64;
     const std::int64_t tiles = output_tiles(M, N, bm, bn, flags);
     const int sms = gemm_num_sms();
@@ -531,7 +539,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     if (ws_path) {
         // warp-specialised TMA/mbarrier pipeline (gemm_ws.cuh)
         // the 56-wide tile measured slower than 64 on the TMA path (tools/gemm_bench.py): use 64 there
-        const int famid = fam == Family::kWide ? (bn == 112 ? 5 : 0) : fam == Family::kWide80 ? 4
+        const int famid = fam == Family::kWide ? (bn == 112 ? 5 : bn == 104 ? 6 : 0) : fam == Family::kWide80 ? 4
                           : fam == Family::kSkinny56 ? (a.rowmajor ? 3 : 1) : fam == Family::kSkinny ? 1 : 2;
         {
             if (a.rowmajor) {

@@ -94,7 +94,8 @@ def test_gaussian_ulp_mismatch_rate(ctx, oracle):
 
 # ---- GEMM (kernels_drivers.cpp:21-65) --------------------------------------------------
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (7, 5, 3), (64, 32, 32), (129, 65, 33), (2000, 20, 2000),
-                                   (300, 130, 1000), (50, 50, 100000), (1000, 2000, 257), (8, 1, 4096)])
+                                   (300, 130, 1000), (50, 50, 100000), (1000, 2000, 257), (8, 1, 4096),
+                                   (3000, 100, 700), (777, 97, 300), (500, 104, 20000)])
 @pytest.mark.parametrize("a_row,b_row,c_row", [(0, 0, 0), (1, 0, 1), (0, 1, 1), (1, 1, 0)])
 def test_gemm_layouts(ctx, m, n, k, a_row, b_row, c_row):
     L = _lib()
