@@ -223,15 +223,27 @@ def hbm_peak_gbs():
 
 
 def time_config(D, ctx, h, run, steps):
+    """Device time per run (CUDA events on the library stream, max over ranks) after one warm run;
+    also the per-run wall times and the SM clock during the runs."""
     r = run()
     info = qbfac_info(r)
     r.free()
     ctx.synchronize()
     D.barrier()
-    res = []
-    t = timed_device(ctx, lambda: res.append(run()), steps)
-    for x in res:
+    clocks = ClockSampler(D.local)
+    clocks.start()
+    time.sleep(0.2)
+    walls = []
+
+    def one():
+        t0 = time.perf_counter()
+        x = run()
         x.free()
+        ctx.synchronize()
+        walls.append(time.perf_counter() - t0)
+    t = timed_device(ctx, one, steps)
+    info["run_wall_s"] = [round(w, 5) for w in walls]
+    info["clocks"] = clocks.stop()
     return D.max(t), info
 
 
@@ -367,12 +379,11 @@ def main():
     D.barrier()
     ctx.synchronize()
     l0 = ctx.kernel_launches()
-    res = []
-    t_step = timed_device(ctx, lambda: res.append(factorize()), args.steps)
+    # each result is released right away (stream-ordered free: no sync); results kept alive across
+    # the timed runs would grow the memory pool inside the timed region
+    t_step = timed_device(ctx, lambda: factorize().free(), args.steps)
     D.barrier()
     launches = ctx.kernel_launches() - l0
-    for x in res:
-        x.free()
     clk = clocks.stop()
     t_step = D.max(t_step)
 

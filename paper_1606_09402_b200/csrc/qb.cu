@@ -1558,9 +1558,10 @@ std::unique_ptr<Result> run_qb_b(Context& c, Matrix& a, const Params& p) {
 std::unique_ptr<Result> run_arf(Context& c, Matrix& a, const Params& p) {
     const std::int64_t r = p.b;
     if (r < 1) throw QbError(kDimensionError, "adaptive_range_finder: r must be >= 1");
-    if (c.world > 1) throw QbError(kError, "adaptive_range_finder: single GPU only");
+    // Row-sharded (world > 1): samples and Q rows live on their ranks; the column norms, the
+    // projections Q^T v and the final A^T Q are summed over ranks (the same allreduces as EI).
     const std::int64_t m = a.m, n = a.n;
-    std::int64_t cap = std::min(m, n);
+    std::int64_t cap = std::min(a.m_global, n);
     if (p.max_rank > 0) cap = std::min(cap, p.max_rank);
     Engine eng(c, a);
     const std::int64_t passes0 = a.passes;
@@ -1592,6 +1593,7 @@ std::unique_ptr<Result> run_arf(Context& c, Matrix& a, const Params& p) {
         MatView vv{v, m, 1, 1, true};
         MatView cc{cv.p, s.k, 1, 1, true};
         eng.gemm(1.0, s.qk().t(), vv, 0.0, cc);
+        eng.allreduce_view(cc);
         eng.gemm(-1.0, s.qk(), cc, 1.0, vv);
     };
     std::int64_t head = 0;
@@ -1599,6 +1601,7 @@ std::unique_ptr<Result> run_arf(Context& c, Matrix& a, const Params& p) {
     while (true) {
         MatView wv{win.p, m, r, std::max<std::int64_t>(m, 1), false};
         column_sumsq(c.st, c.ws_red, wv, nrm.p);
+        c.allreduce(nrm.p, static_cast<std::size_t>(r));
         QB_CUDA(cudaMemcpyAsync(hn.data(), nrm.p, sizeof(double) * r, cudaMemcpyDeviceToHost, c.st));
         QB_CUDA(cudaStreamSynchronize(c.st));
         double mx = 0.0;
@@ -1611,6 +1614,7 @@ std::unique_ptr<Result> run_arf(Context& c, Matrix& a, const Params& p) {
         project(yv.p);
         MatView y1{yv.p, m, 1, 1, true};
         column_sumsq(c.st, c.ws_red, MatView{yv.p, m, 1, std::max<std::int64_t>(m, 1), false}, nrm.p + r);
+        c.allreduce(nrm.p + r, 1);
         QB_CUDA(cudaMemcpyAsync(hn.data() + r, nrm.p + r, sizeof(double), cudaMemcpyDeviceToHost, c.st));
         QB_CUDA(cudaStreamSynchronize(c.st));
         const double yn = std::sqrt(hn[r]);
@@ -1634,6 +1638,7 @@ std::unique_ptr<Result> run_arf(Context& c, Matrix& a, const Params& p) {
             MatView vi{yi, m, 1, 1, true};
             MatView cc{cv.p, 1, 1, 1, true};
             eng.gemm(1.0, y1.t(), vi, 0.0, cc);
+            eng.allreduce_view(cc);
             eng.gemm(-1.0, y1, cc, 1.0, vi);
         }
         head = (head + 1) % r;

@@ -159,3 +159,24 @@ def test_sharded_wide_block(alg):
           for g, (r0, rows) in enumerate(plan)]
     shards = _run_ranks(hs, **run)
     _check(a, ref, shards, 1e-10 if alg == 0 else 1e-8)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_range_finder(world):
+    """The adaptive range finder row-sharded: window norms, projections Q^T v and
+    A^T Q summed over ranks; every rank matches the unsharded device run."""
+    a = matgen.synthesize(400, 300, matgen.spectrum("exp_decay", 300, tau=6.0), 31)
+    run = dict(alg=6, b=8, eps_abs=1e-6 * np.linalg.norm(a, 2), seed=12, max_rank=200)
+    ref = _single(qbfac.MatrixHandle.dense(a, qbfac.default_context()), **run)
+    ctxs = _local_group(world)
+    plan = dist.plan_dense_rows(a.shape[0], world, align=8)
+    hs = [qbfac.MatrixHandle.dense_shard(dist.shard_dense(a, r0, rows), a.shape[0], r0, ctxs[g])
+          for g, (r0, rows) in enumerate(plan)]
+    shards = _run_ranks(hs, **run)
+    for s in shards:
+        assert (s[0], s[1], s[2]) == ref[:3]
+        assert np.array_equal(s[5], shards[0][5])
+    qs = np.vstack([s[4] for s in shards])
+    assert np.abs(qs.T @ qs - np.eye(qs.shape[1])).max() < 1e-10
+    sg, sr = np.linalg.svd(shards[0][5], compute_uv=False), np.linalg.svd(ref[5], compute_uv=False)
+    assert np.max(np.abs(sg - sr) / sr) < 1e-8
