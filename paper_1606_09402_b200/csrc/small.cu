@@ -745,6 +745,7 @@ struct PanelArgs {
     double *ra, *rainv, *rb, *rbinv;  // ld kSmallMax
     SmallStatus *st0, *st1;
     unsigned* gbar;  // grid barrier words
+    int nstages;     // sub-tile ring depth (<= PanelCfg<BP>::STAGES; fewer -> 2 CTAs per SM)
 };
 
 template <int BP>
@@ -893,14 +894,15 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
     pdl_wait();
     using C = PanelCfg<BP>;
     extern __shared__ __align__(128) double psm[];
-    double* ys2 = psm;                              // STAGES sub-tile buffers (SUB x LD)
-    double* rs = psm + C::STAGES * C::SUB * C::LD;  // BP x LD triangular factor
+    const int NST = p.nstages;
+    double* ys2 = psm;                         // NST sub-tile buffers (SUB x LD)
+    double* rs = psm + NST * C::SUB * C::LD;   // BP x LD triangular factor
     __shared__ __align__(8) std::uint64_t full[C::STAGES], empty[C::STAGES];
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const bool mma_warp = warp < 8;
     if (tid == 0) {
-        for (int s = 0; s < C::STAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             pb_init(&full[s], 1);
             pb_init(&empty[s], 8);
         }
@@ -911,7 +913,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
     // Gram entries.
     const int kpad = ((p.b + 3) & ~3) - p.b;
     auto zero_pad = [&]() {
-        for (int idx = tid; idx < C::STAGES * C::SUB * kpad; idx += blockDim.x)
+        for (int idx = tid; idx < NST * C::SUB * kpad; idx += blockDim.x)
             ys2[(idx / kpad) * C::LD + p.b + idx % kpad] = 0.0;
     };
     zero_pad();
@@ -1032,7 +1034,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
                     __syncwarp();
                     if (lane == 0) pb_arrive(&full[ring_stage]);
                 }
-                if (++ring_stage == C::STAGES) { ring_stage = 0; ring_phase ^= 1; }
+                if (++ring_stage == NST) { ring_stage = 0; ring_phase ^= 1; }
             }
         } else {
             for (int sub = cta; sub < p.nsub; sub += G) {
@@ -1041,7 +1043,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
                 pb_fence_async();  // phase B writes T into the buffer before the next bulk copy lands there
                 __syncwarp();
                 if (lane == 0) pb_arrive(&empty[ring_stage]);
-                if (++ring_stage == C::STAGES) { ring_stage = 0; ring_phase ^= 1; }
+                if (++ring_stage == NST) { ring_stage = 0; ring_phase ^= 1; }
             }
         }
         __syncthreads();
@@ -1955,14 +1957,18 @@ void launch_cholqr2_panel(cudaStream_t st, PanelArgs& a, int grid_cap) {
     using C = PanelCfg<BP>;
     auto kern = cholqr2_panel_kernel<BP>;
     a.nsub = static_cast<int>(ceil_div(a.rows, C::SUB));
-    static PerDevice<int> setup;
-    const int per_sm = setup.get([&] {
-        int v = 0;
+    // ring depth: QBFAC_PANEL_STAGES (2..STAGES) trades in-flight sub-tiles for a second CTA per SM
+    const char* st_env = std::getenv("QBFAC_PANEL_STAGES");
+    a.nstages = st_env ? std::max(2, std::min(C::STAGES, std::atoi(st_env))) : C::STAGES;
+    const int smem = std::max<int>((a.nstages * C::SUB + BP) * C::LD * 8, CholCfg<BP>::SMEM);
+    static PerDevice<bool> setup;
+    setup.get([&] {
         QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, kCholThreads, C::SMEM));
-        if (v < 1) throw QbError(kError, "cholqr2_panel: kernel does not fit on an SM");
-        return v;
+        return true;
     });
+    int per_sm = 0;
+    QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCholThreads, smem));
+    if (per_sm < 1) throw QbError(kError, "cholqr2_panel: kernel does not fit on an SM");
     const int grid = std::max(1, std::min(std::min(a.nsub, grid_cap), per_sm * gemm_num_sms()));
     static const bool tm_on = [] {
         const char* e = std::getenv("QBFAC_PANEL_TM");
@@ -1986,7 +1992,7 @@ void launch_cholqr2_panel(cudaStream_t st, PanelArgs& a, int grid_cap) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kCholThreads);
-    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
@@ -2014,7 +2020,7 @@ void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t
         QB_LAUNCH_CHECK();
         return;
     }
-    const int cap = gemm_num_sms();
+    const int cap = 2 * gemm_num_sms();  // up to 2 CTAs per SM with a shallow ring
     a.part = ws.get(static_cast<std::size_t>(cap) * bp * bp);
     switch (bp) {
         case 16: launch_cholqr2_panel<16>(st, a, cap); break;

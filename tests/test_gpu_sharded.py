@@ -180,3 +180,39 @@ def test_sharded_range_finder(world):
     assert np.abs(qs.T @ qs - np.eye(qs.shape[1])).max() < 1e-10
     sg, sr = np.linalg.svd(shards[0][5], compute_uv=False), np.linalg.svd(ref[5], compute_uv=False)
     assert np.max(np.abs(sg - sr) / sr) < 1e-8
+
+
+def test_sharded_qb_to_svd():
+    """qb_to_svd on a row-sharded result: B^T is replicated, so every rank forms the same
+    r x r factor and Jacobi rotations (deterministic) and returns its own rows of U; stacked,
+    they equal the unsharded U S V^T."""
+    a = matgen.synthesize(600, 300, matgen.spectrum("exp_decay", 300, tau=9.0), 41)
+    run = dict(alg=0, mode=0, b=20, power=1, k=60, s=0, seed=3)
+    single = qbfac.run_device(qbfac.MatrixHandle.dense(a, qbfac.default_context()), **run)
+    ref = single.svd(40)
+    single.free()
+    ctxs = _local_group(2)
+    plan = dist.plan_dense_rows(a.shape[0], 2, align=8)
+    hs = [qbfac.MatrixHandle.dense_shard(dist.shard_dense(a, r0, rows), a.shape[0], r0, ctxs[g])
+          for g, (r0, rows) in enumerate(plan)]
+    out, errs = [None, None], []
+
+    def work(r):
+        try:
+            res = qbfac.run_device(hs[r], **run)
+            out[r] = res.svd(40)
+            res.free()
+        except Exception as ex:  # pragma: no cover
+            errs.append(repr(ex))
+    ths = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=300)
+    assert not errs, errs
+    assert np.array_equal(out[0].S, out[1].S) and np.array_equal(out[0].V, out[1].V)
+    u = np.vstack([out[0].U, out[1].U])
+    np.testing.assert_allclose(out[0].S, ref.S, rtol=1e-10)
+    lr = ref.U @ np.diag(ref.S) @ ref.V.T
+    assert np.linalg.norm(u @ np.diag(out[0].S) @ out[0].V.T - lr) <= 1e-9 * np.linalg.norm(lr)
+    assert np.abs(u.T @ u - np.eye(40)).max() < 1e-10
