@@ -23,6 +23,8 @@ struct NcclApi {
     decltype(&ncclGetUniqueId) get_unique_id = nullptr;
     decltype(&ncclCommInitRank) init_rank = nullptr;
     decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclReduceScatter) reduce_scatter = nullptr;
+    decltype(&ncclAllGather) all_gather = nullptr;
     decltype(&ncclCommDestroy) destroy = nullptr;
     decltype(&ncclGetErrorString) error_string = nullptr;
 };
@@ -39,10 +41,13 @@ NcclApi& api() {
         a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(a.handle, "ncclGetUniqueId"));
         a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(a.handle, "ncclCommInitRank"));
         a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(a.handle, "ncclAllReduce"));
+        a.reduce_scatter = reinterpret_cast<decltype(a.reduce_scatter)>(dlsym(a.handle, "ncclReduceScatter"));
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(a.handle, "ncclAllGather"));
         a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(a.handle, "ncclCommDestroy"));
         a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(a.handle, "ncclGetErrorString"));
     });
-    if (!a.handle || !a.get_unique_id || !a.init_rank || !a.all_reduce || !a.destroy)
+    if (!a.handle || !a.get_unique_id || !a.init_rank || !a.all_reduce || !a.reduce_scatter || !a.all_gather ||
+        !a.destroy)
         throw QbError(kError, "NCCL (libnccl.so.2) is not available");
     return a;
 }
@@ -126,6 +131,76 @@ void Comm::allreduce_sum(double* p, std::size_t count, cudaStream_t st) {
     if (!comm_ || count == 0) return;
     check(api().all_reduce(p, p, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), st),
           "ncclAllReduce");
+}
+
+void Comm::reduce_scatter_sum(const double* send, double* recv, std::size_t recvcount, cudaStream_t st) {
+    if (local_) {
+        // loopback: rank 0 sums the full send buffers in rank order, every rank copies its block
+        LocalGroup& g = *local_;
+        const std::size_t total = recvcount * static_cast<std::size_t>(world_);
+        QB_CUDA(cudaStreamSynchronize(st));
+        g.cptrs[static_cast<std::size_t>(rank_)] = send;
+        g.barrier();
+        if (rank_ == 0 && total) {
+            if (g.cap < total) {
+                if (g.sum) QB_CUDA(cudaFree(g.sum));
+                QB_CUDA(cudaMalloc(&g.sum, total * sizeof(double)));
+                g.cap = total;
+            }
+            QB_CUDA(cudaMemcpyAsync(g.sum, g.cptrs[0], total * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            for (int r = 1; r < world_; ++r)
+                local_add_kernel<<<static_cast<unsigned>(std::min<std::size_t>((total + 255) / 256, 1024)), 256, 0, st>>>(
+                    g.sum, g.cptrs[static_cast<std::size_t>(r)], total);
+            QB_CUDA(cudaStreamSynchronize(st));
+        }
+        g.barrier();
+        if (recvcount)
+            QB_CUDA(cudaMemcpyAsync(recv, g.sum + static_cast<std::size_t>(rank_) * recvcount, recvcount * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, st));
+        QB_CUDA(cudaStreamSynchronize(st));
+        g.barrier();
+        return;
+    }
+    if (!comm_) {
+        if (recvcount && recv != send)
+            QB_CUDA(cudaMemcpyAsync(recv, send, recvcount * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        return;
+    }
+    if (recvcount == 0) return;
+    check(api().reduce_scatter(send, recv, recvcount, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), st),
+          "ncclReduceScatter");
+}
+
+void Comm::all_gather(const double* send, double* recv, std::size_t sendcount, cudaStream_t st) {
+    if (local_) {
+        // loopback: every rank writes its block of a shared buffer, then copies the whole buffer
+        LocalGroup& g = *local_;
+        const std::size_t total = sendcount * static_cast<std::size_t>(world_);
+        QB_CUDA(cudaStreamSynchronize(st));
+        g.barrier();
+        if (rank_ == 0 && g.cap < total) {
+            if (g.sum) QB_CUDA(cudaFree(g.sum));
+            QB_CUDA(cudaMalloc(&g.sum, total * sizeof(double)));
+            g.cap = total;
+        }
+        g.barrier();
+        if (sendcount)
+            QB_CUDA(cudaMemcpyAsync(g.sum + static_cast<std::size_t>(rank_) * sendcount, send, sendcount * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, st));
+        QB_CUDA(cudaStreamSynchronize(st));
+        g.barrier();
+        if (total) QB_CUDA(cudaMemcpyAsync(recv, g.sum, total * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        QB_CUDA(cudaStreamSynchronize(st));
+        g.barrier();
+        return;
+    }
+    if (!comm_) {
+        if (sendcount && recv != send)
+            QB_CUDA(cudaMemcpyAsync(recv, send, sendcount * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        return;
+    }
+    if (sendcount == 0) return;
+    check(api().all_gather(send, recv, sendcount, ncclDouble, static_cast<ncclComm_t>(comm_), st), "ncclAllGather");
 }
 
 void Comm::unique_id(void* out128) {

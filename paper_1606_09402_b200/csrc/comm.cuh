@@ -19,7 +19,8 @@ namespace qbgpu {
 // others at a host barrier, and rank 0 sums the buffers in rank order (deterministic, the same
 // order NCCL's ring would not guarantee). Kernels never wait on each other — only host threads do.
 struct LocalGroup {
-    explicit LocalGroup(int w) : world(w), ptrs(static_cast<std::size_t>(w), nullptr) {}
+    explicit LocalGroup(int w)
+        : world(w), ptrs(static_cast<std::size_t>(w), nullptr), cptrs(static_cast<std::size_t>(w), nullptr) {}
     ~LocalGroup();
     void barrier();
     int world;
@@ -28,6 +29,7 @@ struct LocalGroup {
     int arrived = 0;
     unsigned gen = 0;
     std::vector<double*> ptrs;
+    std::vector<const double*> cptrs;
     double* sum = nullptr;
     std::size_t cap = 0;
 };
@@ -44,6 +46,11 @@ public:
     int world() const { return world_; }
     // In-place sum over ranks on `st` (ncclAllReduce, ncclDouble, ncclSum).
     void allreduce_sum(double* p, std::size_t count, cudaStream_t st);
+    // recv (recvcount) = block `rank` of the sum over ranks of send (world * recvcount)
+    // (ncclReduceScatter, ncclDouble, ncclSum).
+    void reduce_scatter_sum(const double* send, double* recv, std::size_t recvcount, cudaStream_t st);
+    // recv (world * sendcount) = the send blocks of all ranks in rank order (ncclAllGather).
+    void all_gather(const double* send, double* recv, std::size_t sendcount, cudaStream_t st);
 
     static void unique_id(void* out128);
 

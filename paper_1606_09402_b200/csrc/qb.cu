@@ -511,11 +511,11 @@ public:
     }
 
     // Y (n x w) = A^T X (X: m x w), summed over ranks.
-    void apply_t(const MatView& x, const MatView& y) {
+    void apply_t(const MatView& x, const MatView& y, bool reduce = true) {
         if (a_.host_stream) throw QbError(kError, "host-streamed matrix: only single_pass_fp consumes a RowStream");
         a_.wait_resident(st_);
         const bool contiguous = (y.rowmajor && y.ld == y.cols) || (!y.rowmajor && y.ld == y.rows);
-        if (c_.world > 1 && !contiguous) {
+        if (reduce && c_.world > 1 && !contiguous) {
             // allreduce needs a packed buffer: compute there, reduce, scatter into y
             if (scratch_t_.n < static_cast<std::size_t>(y.rows * y.cols))
                 scratch_t_ = DBuf(static_cast<std::size_t>(y.rows * y.cols), st_);
@@ -546,7 +546,24 @@ public:
         } else {
             gemm(1.0, a_.dense_view().t(), x, 0.0, y);
         }
-        allreduce_view(y);
+        if (reduce) allreduce_view(y);
+    }
+    // Column-sharded n-side (randQB_EI at world > 1): yl (blk x w, rows [rank blk, rank blk + blk) of
+    // the n rows padded to n_pad = world blk) = this rank's block of A^T X summed over ranks — one
+    // reduce-scatter instead of an allreduce of the whole n x w. Rows past n are zero.
+    void apply_t_rs(const MatView& x, const MatView& yl, std::int64_t n_pad, std::int64_t blk) {
+        const std::int64_t w = x.cols;
+        if (rs_full_.n < static_cast<std::size_t>(n_pad * w)) rs_full_ = DBuf(static_cast<std::size_t>(n_pad * w), st_);
+        if (n_pad > a_.n)
+            QB_CUDA(cudaMemsetAsync(rs_full_.p + a_.n * w, 0, sizeof(double) * (n_pad - a_.n) * w, st_));
+        apply_t(x, MatView{rs_full_.p, a_.n, w, w, true}, false);
+        if (yl.rowmajor && yl.ld == w && yl.rows == blk) {
+            c_.reduce_scatter(rs_full_.p, yl.p, static_cast<std::size_t>(blk * w));
+            return;
+        }
+        if (rs_loc_.n < static_cast<std::size_t>(blk * w)) rs_loc_ = DBuf(static_cast<std::size_t>(blk * w), st_);
+        c_.reduce_scatter(rs_full_.p, rs_loc_.p, static_cast<std::size_t>(blk * w));
+        if (yl.rows) copy_matrix(st_, MatView{rs_loc_.p, yl.rows, w, w, true}, yl);
     }
     void allreduce_view(const MatView& y) {
         if (c_.world == 1) return;
@@ -663,7 +680,7 @@ public:
             // rows into a zeroed buffer; the sum over ranks adds only zeros to them, so it is exact),
             // factor it redundantly (identical inputs, identical R and deficiency decision on every
             // rank) and keep this rank's rows of Q.
-            const std::int64_t mg = a_.m_global, r0 = a_.row0;
+            const std::int64_t mg = geo_rows >= 0 ? geo_rows : a_.m_global, r0 = geo_rows >= 0 ? geo_row0 : a_.row0;
             DBuf full(static_cast<std::size_t>(std::max<std::int64_t>(mg, 1)) * b, st_);
             QB_CUDA(cudaMemsetAsync(full.p, 0, sizeof(double) * full.n, st_));
             MatView fv{full.p, mg, b, std::max<std::int64_t>(mg, 1), false};
@@ -895,9 +912,12 @@ public:
 
     std::int64_t hh_fallbacks = 0;
     std::int64_t wide_passes = 0;
+    // Row geometry of a sharded panel for the Householder fallback: -1 = the rows of A; the
+    // column-sharded n-side panels set (n_pad, rank blk) around their orth.
+    std::int64_t geo_rows = -1, geo_row0 = 0;
 
 private:
-    DBuf scratch_t_, stat_, tri_, wide_, wide_y_, wide_s_, wide_diag_;
+    DBuf scratch_t_, stat_, tri_, wide_, wide_y_, wide_s_, wide_diag_, rs_full_, rs_loc_;
     DBuf wslot_[kNumSlots];
     std::int64_t wld_ = 0;
     Context& c_;
@@ -943,27 +963,34 @@ struct State {
     Engine& eng;
     std::int64_t m, n, cap, ld;
     std::int64_t k = 0;
+    // B^T rows held here: all n (replicated), or this rank's column block of B (column-sharded
+    // n-side: nb_store = blk rows of storage, nb = the real ones, n_pad = world blk)
+    std::int64_t nb, nb_store, n_pad = 0;
+    bool nsh = false;
     DBuf q, bt;
     double* d_e;
     double eps2 = 0.0;
     std::vector<double> trace;
 
-    State(Context& cc, Engine& e, std::int64_t m_, std::int64_t n_, std::int64_t cap_)
-        : c(cc), eng(e), m(m_), n(n_), cap(cap_), ld(even(cap_)),
+    State(Context& cc, Engine& e, std::int64_t m_, std::int64_t n_, std::int64_t cap_, std::int64_t nb_ = -1,
+          std::int64_t nb_store_ = -1, std::int64_t n_pad_ = 0)
+        : c(cc), eng(e), m(m_), n(n_), cap(cap_), ld(even(cap_)), nb(nb_ < 0 ? n_ : nb_),
+          nb_store(nb_store_ < 0 ? n_ : nb_store_), n_pad(n_pad_), nsh(nb_ >= 0),
           q(static_cast<std::size_t>(std::max<std::int64_t>(m_, 1)) * even(cap_), cc.st),
-          bt(static_cast<std::size_t>(std::max<std::int64_t>(n_, 1)) * even(cap_), cc.st),
+          bt(static_cast<std::size_t>(std::max<std::int64_t>(nb_store_ < 0 ? n_ : nb_store_, 1)) * even(cap_), cc.st),
           d_e(cc.d_small + static_cast<std::size_t>(kSlot) * kNumSlots + 1) {}
 
     MatView qk() const { return MatView{q.p, m, k, ld, true}; }
-    MatView btk() const { return MatView{bt.p, n, k, ld, true}; }
+    MatView btk() const { return MatView{bt.p, nb, k, ld, true}; }
     MatView qslot(std::int64_t w) const { return MatView{q.p + k, m, w, ld, true}; }
-    MatView btslot(std::int64_t w) const { return MatView{bt.p + k, n, w, ld, true}; }
+    MatView btslot(std::int64_t w) const { return MatView{bt.p + k, nb, w, ld, true}; }
 
     // Rows of B_i enter E one by one: enqueue the device step and the
     // read-back of its result (and of the block's lazy CholQR statuses), then one sync.
     void indicator_enqueue(int d, bool check) {
         double* norms = c.d_small + static_cast<std::size_t>(kNorms) * kSlot;
         column_sumsq(c.st, c.ws_red, btslot(d), norms);
+        if (nsh) c.allreduce(norms, static_cast<std::size_t>(d));  // row norms of B_i over the column blocks
         indicator_step(c.st, d_e, norms, d, eps2, check ? 1 : 0, c.d_ind);
         QB_CUDA(cudaMemcpyAsync(c.h_ind, c.d_ind, sizeof(IndicatorOut), cudaMemcpyDeviceToHost, c.st));
     }
@@ -997,7 +1024,13 @@ std::unique_ptr<Result> finish(State& s, Matrix& a, std::int64_t passes0, int te
     r->rank = s.k;
     r->ld = s.ld;
     r->q = std::move(s.q);
-    r->bt = std::move(s.bt);
+    if (s.nsh) {  // the column blocks of B back on every rank (the result contract: B replicated)
+        DBuf full(static_cast<std::size_t>(std::max<std::int64_t>(s.n_pad, 1)) * s.ld, s.c.st);
+        s.c.all_gather(s.bt.p, full.p, static_cast<std::size_t>(s.nb_store * s.ld));
+        r->bt = std::move(full);
+    } else {
+        r->bt = std::move(s.bt);
+    }
     r->e = s.get_e();
     r->norm_a_sq = norm_a_sq;
     r->passes = a.passes - passes0;
@@ -1020,8 +1053,18 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
         cap = std::min(cap, p.k + p.s);
     }
     const std::int64_t passes0 = a.passes;
-    State s(c, eng, m, n, cap);
     const bool sharded = c.world > 1;
+    // Column-sharded n-side (world > 1; QBFAC_NSHARD=0 keeps B replicated): this rank owns the
+    // column block [rank blk, rank blk + blk) of B and of every n-side block (Omega_i rows for the
+    // B Omega_i product, Z, B_i^T); A^T passes reduce-scatter instead of allreducing n x b, the
+    // k x b products B X are partial sums allreduced, Z is all-gathered once per power step for
+    // the A Z pass, and B is gathered once at the end. n-side work per rank: 1 / world.
+    const char* nsh_env = std::getenv("QBFAC_NSHARD");
+    const bool nsh = sharded && !(nsh_env && nsh_env[0] == '0');
+    const std::int64_t blk = nsh ? ceil_div(n, c.world) : n, n_pad = blk * (nsh ? c.world : 1);
+    const std::int64_t c0 = nsh ? blk * c.rank : 0;
+    const std::int64_t nl = nsh ? std::max<std::int64_t>(0, std::min(blk, n - c0)) : n;
+    State s = nsh ? State(c, eng, m, n, cap, nl, blk, n_pad) : State(c, eng, m, n, cap);
     const double norm_a_sq = eng.frob_device(s.d_e);   // Alg. 2 step 2, +1 pass
     a.passes += 1;
     s.eps2 = p.eps_abs * p.eps_abs;
@@ -1054,7 +1097,8 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
     const std::int64_t lyz = round_up(bpad, 4);
     DBuf y(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * lyz, c.st);
     DBuf tmp(static_cast<std::size_t>(std::max<std::int64_t>(std::max<std::int64_t>(m, n), 1)) * bpad, c.st);
-    DBuf z(p.power > 0 ? static_cast<std::size_t>(n) * lyz : 0, c.st);
+    DBuf z(p.power > 0 ? static_cast<std::size_t>(blk) * lyz : 0, c.st);
+    DBuf zfull(nsh && p.power > 0 ? static_cast<std::size_t>(n_pad) * lyz : 0, c.st);
     DBuf mbuf(static_cast<std::size_t>(std::max<std::int64_t>(cap, 1)) * bpad, c.st);
     double e_host = norm_a_sq;
     while (true) {
@@ -1083,23 +1127,37 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             // step 5: Y = A Omega_i - Q (B Omega_i)   (Omega_i drawn with its batch above)
             eng.apply(omv, yv); a.passes += 1;
             if (s.k > 0) {
-                eng.gemm(1.0, s.btk().t(), omv, 0.0, mv);
+                eng.gemm(1.0, s.btk().t(), omv.rows_range(c0, nl), 0.0, mv);  // B Omega_i (partial if nsh)
+                if (nsh) eng.allreduce_view(mv);
                 eng.gemm(-1.0, s.qk(), mv, 1.0, yv);
             }
             // per-block power iteration with deflation at every application
             for (std::int64_t it = 0; it < p.power; ++it) {
                 eng.orth_block(yv, yv, kR1, kR1inv, sharded, tmp, false);
-                MatView zv{z.p, n, bi, lyz, true};
-                eng.apply_t(yv, zv); a.passes += 1;
+                MatView zv{z.p, blk, bi, lyz, true};   // this rank's rows of Z (all n when replicated)
+                MatView zr = zv.rows_range(0, nl);
+                if (nsh) eng.apply_t_rs(yv, zv, n_pad, blk);
+                else eng.apply_t(yv, zv);
+                a.passes += 1;
                 if (s.k > 0) {
                     eng.gemm(1.0, s.qk().t(), yv, 0.0, mv);
                     eng.allreduce_view(mv);
-                    eng.gemm(-1.0, s.btk(), mv, 1.0, zv);
+                    eng.gemm(-1.0, s.btk(), mv, 1.0, zr);
                 }
-                eng.orth_block(zv, zv, kR1, kR1inv, false, tmp, false);
-                eng.apply(zv, yv); a.passes += 1;
+                if (nsh) {
+                    eng.geo_rows = n_pad;
+                    eng.geo_row0 = c0;
+                    eng.orth_block(zv, zv, kR1, kR1inv, true, tmp, false);  // rows of Z split over the ranks
+                    eng.geo_rows = -1;
+                    c.all_gather(z.p, zfull.p, static_cast<std::size_t>(blk * lyz));
+                    eng.apply(MatView{zfull.p, n, bi, lyz, true}, yv); a.passes += 1;
+                } else {
+                    eng.orth_block(zv, zv, kR1, kR1inv, false, tmp, false);
+                    eng.apply(zv, yv); a.passes += 1;
+                }
                 if (s.k > 0) {
-                    eng.gemm(1.0, s.btk().t(), zv, 0.0, mv);
+                    eng.gemm(1.0, s.btk().t(), zr, 0.0, mv);
+                    if (nsh) eng.allreduce_view(mv);
                     eng.gemm(-1.0, s.qk(), mv, 1.0, yv);
                 }
             }
@@ -1120,8 +1178,9 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
                 if (attempt == 0 && !eng.lazy_ok()) continue;
                 break;
             }
-            // step 7: B_i^T = A^T Q_i (+1 pass)
-            eng.apply_t(s.qslot(d), s.btslot(d));
+            // step 7: B_i^T = A^T Q_i (+1 pass; this rank's column block of B_i when nsh)
+            if (nsh) eng.apply_t_rs(s.qslot(d), s.btslot(d), n_pad, blk);
+            else eng.apply_t(s.qslot(d), s.btslot(d));
             a.passes += 1;
             s.indicator_enqueue(d, fixed_prec);
             eng.fetch_lazy();

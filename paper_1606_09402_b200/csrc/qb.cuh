@@ -71,6 +71,16 @@ struct Context {
     void allreduce(double* p, std::size_t count) {
         if (comm) comm->allreduce_sum(p, count, st);
     }
+    void reduce_scatter(const double* send, double* recv, std::size_t recvcount) {
+        if (comm) comm->reduce_scatter_sum(send, recv, recvcount, st);
+        else if (recvcount && recv != send)
+            QB_CUDA(cudaMemcpyAsync(recv, send, recvcount * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    void all_gather(const double* send, double* recv, std::size_t sendcount) {
+        if (comm) comm->all_gather(send, recv, sendcount, st);
+        else if (sendcount && recv != send)
+            QB_CUDA(cudaMemcpyAsync(recv, send, sendcount * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
 };
 
 struct Matrix {

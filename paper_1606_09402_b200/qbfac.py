@@ -503,8 +503,11 @@ class MatrixHandle:
                                                        int(transpose_a), C.c_void_p(y_ptr), ldy))
 
     def free(self):
+        # a handle whose context is already closed (e.g. finalised after it in a garbage cycle at
+        # shutdown) is dropped, not freed: its device memory went with the context's device state
         if getattr(self, "_h", None):
-            lib().qbfac_gpu_matrix_free(self._h)
+            if getattr(self.ctx, "_h", None):
+                lib().qbfac_gpu_matrix_free(self._h)
             self._h = None
 
     def __del__(self):
@@ -578,7 +581,8 @@ class DeviceResult:
 
     def free(self):
         if getattr(self, "_h", None):
-            lib().qbfac_gpu_result_free(self._h)
+            if getattr(self.ctx, "_h", None):
+                lib().qbfac_gpu_result_free(self._h)
             self._h = None
 
     def __del__(self):
