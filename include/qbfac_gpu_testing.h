@@ -13,6 +13,7 @@
  *   qbfac_gpu_test_colsumsq  per-column sums of squares (the indicator's row norms)
  *   qbfac_gpu_test_create_local_group  in-process rank group on one GPU (sharded-engine tests)
  *   qbfac_gpu_test_allreduce the context's allreduce (NCCL, or the local group) on a device buffer
+ *   qbfac_gpu_test_collective its reduce-scatter / all-gather (the column-sharded n-side of EI)
  *   qbfac_gpu_test_chol_wide_trace  per-step stamps of the wide Cholesky
  *   qbfac_gpu_test_panel_trace  per-phase %globaltimer stamps (ns) of the last CholQR2 panel launch
  *   qbfac_gpu_test_csr_spmm  CSR pass Y = alpha A X + beta Y on device arrays
@@ -51,6 +52,9 @@ int qbfac_gpu_test_create_local_group(int device, int world, qbfac_gpu_ctx** out
 /* In-place sum over the context's ranks of count doubles at dev (ncclAllReduce for an NCCL
    context, including a one-rank communicator made with qbfac_gpu_create_dist(dev, 0, 1, id)). */
 int qbfac_gpu_test_allreduce(qbfac_gpu_ctx* ctx, double* dev, int64_t count);
+/* op 1: recv (count) = this rank's block of the sum over ranks of send (world * count), ncclReduceScatter;
+   op 2: recv (world * count) = every rank's send (count) in rank order, ncclAllGather. */
+int qbfac_gpu_test_collective(qbfac_gpu_ctx* ctx, int op, const double* send, double* recv, int64_t count);
 /* 64 x 4 %globaltimer stamps (ns) per step k of the last chol_wide launch (CTA 0): step start, phase 2
    done, phase 3 done (incl. the next diagonal Cholesky on CTA 0), step end */
 int qbfac_gpu_test_chol_wide_trace(qbfac_gpu_ctx* ctx, unsigned long long* out);

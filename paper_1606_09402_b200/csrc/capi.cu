@@ -560,6 +560,17 @@ int qbfac_gpu_test_allreduce(qbfac_gpu_ctx* ctx, double* dev, int64_t count) {
     });
 }
 
+int qbfac_gpu_test_collective(qbfac_gpu_ctx* ctx, int op, const double* send, double* recv, int64_t count) {
+    if (!ctx) return QBFAC_ERROR;
+    return guard(ctx, [&] {
+        if (!ctx->c->comm) throw qbgpu::QbError(qbgpu::kError, "context has no communicator");
+        if (op == 1) ctx->c->reduce_scatter(send, recv, static_cast<std::size_t>(count));
+        else if (op == 2) ctx->c->all_gather(send, recv, static_cast<std::size_t>(count));
+        else throw qbgpu::QbError(qbgpu::kDimensionError, "collective: op must be 1 (reduce-scatter) or 2 (all-gather)");
+        QB_CUDA(cudaStreamSynchronize(ctx->c->st));
+    });
+}
+
 int qbfac_gpu_test_chol_wide_trace(qbfac_gpu_ctx* ctx, unsigned long long* out) {
     return guard(ctx, [&] {
         QB_CUDA(cudaStreamSynchronize(ctx->c->st));

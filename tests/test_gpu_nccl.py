@@ -38,6 +38,12 @@ def test_nccl_one_rank_communicator():
     torch.cuda.synchronize()
     ctx.check(L.qbfac_gpu_test_allreduce(ctx.handle, C.c_void_p(x.data_ptr()), 1000))
     assert torch.equal(x, torch.arange(1000, dtype=torch.float64, device="cuda"))
+    L.qbfac_gpu_test_collective.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64]
+    for op in (1, 2):  # ncclReduceScatter / ncclAllGather on the one-rank communicator: identity
+        y = torch.zeros(1000, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        ctx.check(L.qbfac_gpu_test_collective(ctx.handle, op, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1000))
+        assert torch.equal(x, y)
     a = matgen.synthesize(400, 300, matgen.spectrum("exp_decay", 300, tau=9.0), 3)
     eps = 1e-5 * np.linalg.norm(a)
     plain = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, qbfac.default_context()),

@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 __global__ void __launch_bounds__(256) gather_kernel(const double* __restrict__ x, int w, const int* __restrict__ idx,
@@ -38,8 +39,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const double* __restrict__ 
     out[blockIdx.x * 256 + threadIdx.x] = acc[0] + acc[1] + acc[2] + acc[3];
 }
 
-int main() {
-    const int w = 100;
+int main(int argc, char** argv) {
+    const int w = argc > 1 ? std::atoi(argv[1]) : 100;
     const long long nidx = 1LL << 26;  // 67M gathers per launch
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -48,7 +49,7 @@ int main() {
     double *dout, *dx;
     cudaMalloc(&didx, nidx * sizeof(int));
     cudaMalloc(&dout, 16LL * sms * 256 * sizeof(double));
-    for (long long rows : {40000LL, 80000LL, 150000LL, 500000LL, 5000000LL}) {
+    for (long long rows : {50000LL, 80000LL, 150000LL, 500000LL, 5000000LL}) {
         std::uint64_t s = 88172645463325252ULL;
         for (long long i = 0; i < nidx; ++i) {
             s ^= s << 13; s ^= s >> 7; s ^= s << 17;
