@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--n", type=int, default=50000)
     ap.add_argument("--cap", type=int, default=1000)
     ap.add_argument("--only", default="ABCD")
+    ap.add_argument("--k", type=int, default=0, help="one rank k only")
     args = ap.parse_args()
     import torch
 
@@ -60,15 +61,17 @@ def main():
         return e0.elapsed_time(e1) / 1e3 / reps
 
     peak_tf = 35.4
-    tot = {"A": 0.0, "B": 0.0, "C": 0.0, "D": 0.0}
-    ideal = {"A": 0.0, "B": 0.0, "C": 0.0, "D": 0.0}
+    tot = {"A": 0.0, "B": 0.0, "C": 0.0, "D": 0.0, "E": 0.0}
+    ideal = {"A": 0.0, "B": 0.0, "C": 0.0, "D": 0.0, "E": 0.0}
     print(f"m={m} n={n} b={b}: time (us) and TFLOP/s per product", flush=True)
-    for k in range(50, cap, 50):
+    for k in ([args.k] if args.k else range(50, cap, 50)):
         ops = {
             # Q^T Y: A = Q^T (k x m col-major view of row-major Q, ld cap)
             "A": (lambda: gemm(1.0, q, k, m, cap, 0, y, b, lyz, 1, 0.0, mv, b, 1), 2.0 * m * k * b, 2),
             # Y -= Q M
             "B": (lambda: gemm(-1.0, q, m, k, cap, 1, mv, b, b, 1, 1.0, y, lyz, 1), 2.0 * m * k * b, 3),
+            # Y = -Q M (beta = 0: no read of Y)
+            "E": (lambda: gemm(-1.0, q, m, k, cap, 1, mv, b, b, 1, 0.0, y, lyz, 1), 2.0 * m * k * b, 0),
             # M = (B^T)^T Omega: A = B^T^T (k x n col-major view, ld cap)
             "C": (lambda: gemm(1.0, bt, k, n, cap, 0, z, b, lyz, 1, 0.0, mv, b, 1), 2.0 * n * k * b, 2),
             # Z -= B^T M
