@@ -1476,7 +1476,14 @@ struct JacobiBlockArgs {
     unsigned* gbar;
     unsigned* rotated;
     int* sweeps_out;
+    int trace;  // QBFAC_JACOBI_TRACE=1: CTA 0 prints its per-phase time split at the end
 };
+
+__device__ __forceinline__ unsigned long long jb_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ void circle_pair(int round, int t, int n, int& a, int& b) {
     if (t == 0) {
@@ -1491,18 +1498,24 @@ __device__ __forceinline__ void circle_pair(int round, int t, int n, int& a, int
 
 constexpr int kJbMaxCols = 16;  // 2 nb <= 16
 
-__global__ void __launch_bounds__(256) jacobi_block_kernel(JacobiBlockArgs p) {
+// 16 warps per CTA: the staging, write-back and W-update loops are latency-bound (r = 1000:
+// 8 -> 16 warps took the Jacobi kernel 130 -> 106 ms; `QBFAC_JACOBI_TRACE=1` prints the split)
+constexpr int kJbThreads = 512;
+
+__global__ void __launch_bounds__(kJbThreads) jacobi_block_kernel(JacobiBlockArgs p) {
     extern __shared__ __align__(16) double jsm[];
     const int r = p.r, nb = p.nb, nc = 2 * nb;
     double* cols = jsm;                                   // nc columns of r (column c at cols + c r)
     double* V = jsm + static_cast<std::size_t>(nc) * r;  // nc x nc, column-major
     __shared__ unsigned s_cnt;
+    unsigned long long ph[5] = {0, 0, 0, 0, 0};  // per-phase time (thread 0; printed when p.trace)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
     const int half = p.nblk / 2;
     int sweep = 0;
     for (; sweep < p.max_sweeps; ++sweep) {
         for (int step = 0; step < p.nblk - 1; ++step) {
             for (int t = blockIdx.x; t < half; t += gridDim.x) {
+                unsigned long long tp = jb_now();
                 int bi, bj;
                 circle_pair(step, t, p.nblk, bi, bj);
                 const int i0 = bi * nb, j0 = bj * nb;
@@ -1531,6 +1544,7 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(JacobiBlockArgs p) {
                 for (int idx = tid; idx < nc * nc; idx += blockDim.x) V[idx] = (idx % nc == idx / nc) ? 1.0 : 0.0;
                 if (tid == 0) s_cnt = 0;
                 __syncthreads();
+                if (tid == 0) { const unsigned long long q = jb_now(); ph[0] += q - tp; tp = q; }
                 for (int rd = 0; rd < nc - 1; ++rd) {
                     for (int q = warp; q < nb; q += nwarps) {
                         int a, b;
@@ -1568,10 +1582,12 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(JacobiBlockArgs p) {
                     }
                     __syncthreads();
                 }
+                if (tid == 0) { const unsigned long long q = jb_now(); ph[1] += q - tp; tp = q; }
                 for (int idx = tid; idx < nc * r; idx += blockDim.x) {
                     const int c = idx / r, i = idx - c * r, g = gcol(c);
                     if (g >= 0) p.nmat[static_cast<std::int64_t>(g) * r + i] = cols[idx];
                 }
+                if (tid == 0) { const unsigned long long q = jb_now(); ph[2] += q - tp; tp = q; }
                 if (s_cnt) {
                     for (int i = tid; i < r; i += blockDim.x) {
                         double wv[kJbMaxCols];
@@ -1595,12 +1611,20 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(JacobiBlockArgs p) {
                     if (tid == 0) atomicAdd(p.rotated + sweep, s_cnt);
                 }
                 __syncthreads();
+                if (tid == 0) { const unsigned long long q = jb_now(); ph[3] += q - tp; }
             }
+            const unsigned long long tb = jb_now();
             grid_barrier(p.gbar, gridDim.x);
+            if (tid == 0) ph[4] += jb_now() - tb;
         }
         if (*reinterpret_cast<volatile unsigned*>(p.rotated + sweep) == 0) break;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *p.sweeps_out = sweep;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *p.sweeps_out = sweep;
+        if (p.trace)
+            printf("jacobi_block r=%d nb=%d CTAs=%d sweeps=%d: load %.1f  inner %.1f  writeback %.1f  W %.1f  barrier %.1f us\n",
+                   r, nb, gridDim.x, sweep, ph[0] * 1e-3, ph[1] * 1e-3, ph[2] * 1e-3, ph[3] * 1e-3, ph[4] * 1e-3);
+    }
 }
 
 // C = A * B for upper-triangular n x n operands staged in shared memory; blockIdx.x
@@ -2071,11 +2095,12 @@ int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, 
             return true;
         });
         int per_sm = 0;
-        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_block_kernel, 256, smem));
+        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_block_kernel, kJbThreads, smem));
         const int gb = std::max(1, std::min(nblk / 2, std::max(per_sm, 1) * gemm_num_sms()));
-        JacobiBlockArgs a{nmat, w, r, nb, nblk, max_sweeps, 1e-15, gbar, rotated, sweeps};
+        const char* tr = std::getenv("QBFAC_JACOBI_TRACE");
+        JacobiBlockArgs a{nmat, w, r, nb, nblk, max_sweeps, 1e-15, gbar, rotated, sweeps, tr && tr[0] == '1' ? 1 : 0};
         void* args[] = {&a};
-        QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_block_kernel), gb, 256, args, smem, st));
+        QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_block_kernel), gb, kJbThreads, args, smem, st));
     } else {
         JacobiArgs a{nmat, w, r, rp, max_sweeps, 1e-15, gbar, rotated, sweeps};
         void* args[] = {&a};
