@@ -23,68 +23,14 @@ namespace qbgpu {
 
 namespace {
 
-// L2 eviction policies (createpolicy + .L2::cache_hint): the gathered rows of X are the only
-// data of a CSR pass that is reused; A's column indices / values and Y stream through once.
-// HINT bit 0 marks the X gathers evict_last, bit 1 the streams (A's indices / values, Y)
-// evict_first, so the streams stop displacing X.
-__device__ __forceinline__ std::uint64_t pol_evict_last() {
-    std::uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ std::uint64_t pol_evict_first() {
-    std::uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-template <int HINT>
-__device__ __forceinline__ double ld_x(const double* p, std::uint64_t pol) {
-    if constexpr ((HINT & 1) == 0) {
-        return __ldg(p);
-    } else {
-        double v;
-        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-        return v;
-    }
-}
-template <int HINT>
-__device__ __forceinline__ std::int32_t ld_ci(const std::int32_t* p, std::uint64_t pol) {
-    if constexpr ((HINT & 2) == 0) {
-        return __ldg(p);
-    } else {
-        std::int32_t v;
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-        return v;
-    }
-}
-template <int HINT>
-__device__ __forceinline__ double ld_v(const double* p, std::uint64_t pol) {
-    if constexpr ((HINT & 2) == 0) {
-        return __ldg(p);
-    } else {
-        double v;
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-        return v;
-    }
-}
-template <int HINT>
-__device__ __forceinline__ void st_y(double* p, double v, std::uint64_t pol) {
-    if constexpr ((HINT & 2) == 0) {
-        *p = v;
-    } else {
-        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-    }
-}
-
 // acc += sum_{e in [e0, e1)} v[e] * X[ci[e], :] for this lane's columns. Lanes load 32
 // (col, val) pairs at once and broadcast them; four nonzeros are gathered per step
 // into four independent accumulator sets (more loads in flight, no serial FMA chain),
 // combined in a fixed order at the end (deterministic).
-template <int NQ, int HINT = 0>
+template <int NQ>
 __device__ __forceinline__ void row_dot(const std::int32_t* __restrict__ ci, const double* __restrict__ v,
                                         const double* __restrict__ x, std::int64_t ldx, int w, std::int64_t e0,
-                                        std::int64_t e1, int lane, double (&acc)[NQ], std::uint64_t pol_x = 0,
-                                        std::uint64_t pol_s = 0) {
+                                        std::int64_t e1, int lane, double (&acc)[NQ]) {
     double a1[NQ], a2[NQ], a3[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) a1[q] = a2[q] = a3[q] = 0.0;
@@ -93,8 +39,8 @@ __device__ __forceinline__ void row_dot(const std::int32_t* __restrict__ ci, con
         std::int32_t my_c = 0;
         double my_v = 0.0;
         if (lane < cnt) {
-            my_c = ld_ci<HINT>(ci + eb + lane, pol_s);
-            my_v = ld_v<HINT>(v + eb + lane, pol_s);
+            my_c = __ldg(ci + eb + lane);
+            my_v = __ldg(v + eb + lane);
         }
         int j = 0;
         for (; j + 4 <= cnt; j += 4) {
@@ -109,10 +55,10 @@ __device__ __forceinline__ void row_dot(const std::int32_t* __restrict__ ci, con
             for (int q = 0; q < NQ; ++q) {
                 const int col = lane + 32 * q;
                 const bool ok = col < w;
-                g0[q] = ok ? ld_x<HINT>(x0 + col, pol_x) : 0.0;
-                g1[q] = ok ? ld_x<HINT>(x1 + col, pol_x) : 0.0;
-                g2[q] = ok ? ld_x<HINT>(x2 + col, pol_x) : 0.0;
-                g3[q] = ok ? ld_x<HINT>(x3 + col, pol_x) : 0.0;
+                g0[q] = ok ? __ldg(x0 + col) : 0.0;
+                g1[q] = ok ? __ldg(x1 + col) : 0.0;
+                g2[q] = ok ? __ldg(x2 + col) : 0.0;
+                g3[q] = ok ? __ldg(x3 + col) : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
@@ -128,7 +74,7 @@ __device__ __forceinline__ void row_dot(const std::int32_t* __restrict__ ci, con
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const int col = lane + 32 * q;
-                if (col < w) acc[q] = fma(a, ld_x<HINT>(xr + col, pol_x), acc[q]);
+                if (col < w) acc[q] = fma(a, __ldg(xr + col), acc[q]);
             }
         }
     }
@@ -295,16 +241,13 @@ __global__ void csr_heavy_combine_kernel(std::int64_t nrows, const std::int64_t*
     }
 }
 
-template <int NQ, int HINT = 0>
+template <int NQ>
 __global__ void __launch_bounds__(256)
 csr_spmm_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const std::int32_t* __restrict__ ci,
                 const double* __restrict__ v, const double* __restrict__ x, std::int64_t ldx,
                 double* __restrict__ y, std::int64_t ldy, int w, double alpha, double beta, std::int64_t heavy_thr,
                 std::int64_t nseg, const std::int64_t* __restrict__ seg, double* __restrict__ partial) {
     pdl_wait();
-    std::uint64_t pol_x = 0, pol_s = 0;
-    if constexpr ((HINT & 1) != 0) pol_x = pol_evict_last();
-    if constexpr ((HINT & 2) != 0) pol_s = pol_evict_first();
     const int lane = threadIdx.x & 31;
     const std::int64_t warp = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -314,7 +257,7 @@ csr_spmm_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const st
         double acc[NQ];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-        row_dot<NQ, HINT>(ci, v, x, ldx, w, seg[nseg + s], seg[2 * nseg + s], lane, acc, pol_x, pol_s);
+        row_dot<NQ>(ci, v, x, ldx, w, seg[nseg + s], seg[2 * nseg + s], lane, acc);
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             const int col = lane + 32 * q;
@@ -327,14 +270,14 @@ csr_spmm_kernel(std::int64_t rows, const std::int64_t* __restrict__ rp, const st
         for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
         const std::int64_t e0 = rp[i], e1 = rp[i + 1];
         if (e1 - e0 > heavy_thr) continue;  // heavy rows: segment kernels
-        row_dot<NQ, HINT>(ci, v, x, ldx, w, e0, e1, lane, acc, pol_x, pol_s);
+        row_dot<NQ>(ci, v, x, ldx, w, e0, e1, lane, acc);
         double* yr = y + i * ldy;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             const int col = lane + 32 * q;
             if (col < w) {
                 const double r = alpha * acc[q];
-                st_y<HINT>(yr + col, beta == 0.0 ? r : r + beta * yr[col], pol_s);
+                yr[col] = beta == 0.0 ? r : r + beta * yr[col];
             }
         }
     }
@@ -509,21 +452,13 @@ void spmm_launch2(cudaStream_t st, const CsrView& a, const double* x, std::int64
     }
 }
 
-int spmm_hint() {
-    const char* e = std::getenv("QBFAC_SPMM_HINT");
-    return e ? std::atoi(e) & 3 : 0;
-}
-
 template <int NQ>
 void spmm_launch(cudaStream_t st, const CsrView& a, const double* x, std::int64_t ldx, double* y, std::int64_t ldy,
                  int w, double alpha, double beta, int sms, double* partial) {
     const int threads = 256;
     const int blocks = static_cast<int>(std::max<std::int64_t>(
         1, std::min<std::int64_t>(ceil_div((a.rows + a.heavy.nseg) * 32, threads), 16L * sms)));
-    const int hint = spmm_hint();
-    launch_pdl(hint == 1 ? csr_spmm_kernel<NQ, 1> : hint == 2 ? csr_spmm_kernel<NQ, 2> : hint == 3 ? csr_spmm_kernel<NQ, 3>
-                                                                                                 : csr_spmm_kernel<NQ, 0>,
-               dim3(blocks), dim3(threads), 0, st, a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha,
+    launch_pdl(csr_spmm_kernel<NQ>, dim3(blocks), dim3(threads), 0, st, a.rows, a.rp, a.ci, a.v, x, ldx, y, ldy, w, alpha,
                beta, a.heavy.thr, a.heavy.nseg, static_cast<const std::int64_t*>(a.heavy.seg), partial);
     QB_LAUNCH_CHECK();
     if (a.heavy.nseg > 0) {
