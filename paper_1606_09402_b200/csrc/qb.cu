@@ -978,7 +978,14 @@ struct State {
           nb_store(nb_store_ < 0 ? n_ : nb_store_), n_pad(n_pad_), nsh(nb_ >= 0),
           q(static_cast<std::size_t>(std::max<std::int64_t>(m_, 1)) * even(cap_), cc.st),
           bt(static_cast<std::size_t>(std::max<std::int64_t>(nb_store_ < 0 ? n_ : nb_store_, 1)) * even(cap_), cc.st),
-          d_e(cc.d_small + static_cast<std::size_t>(kSlot) * kNumSlots + 1) {}
+          d_e(cc.d_small + static_cast<std::size_t>(kSlot) * kNumSlots + 1) {
+        QB_CUDA(cudaEventCreateWithFlags(&ind_ev, cudaEventDisableTiming));
+    }
+    ~State() { cudaEventDestroy(ind_ev); }
+    State(const State&) = delete;
+    State& operator=(const State&) = delete;
+    cudaEvent_t ind_ev = nullptr;  // marks the indicator read-back when later work is queued behind it
+    bool ind_ev_armed = false;
 
     MatView qk() const { return MatView{q.p, m, k, ld, true}; }
     MatView btk() const { return MatView{bt.p, nb, k, ld, true}; }
@@ -994,8 +1001,16 @@ struct State {
         indicator_step(c.st, d_e, norms, d, eps2, check ? 1 : 0, c.d_ind);
         QB_CUDA(cudaMemcpyAsync(c.h_ind, c.d_ind, sizeof(IndicatorOut), cudaMemcpyDeviceToHost, c.st));
     }
+    // Everything enqueued so far (the indicator and status read-backs) is marked by an event, so
+    // work queued after it (the next block's first pass) keeps the GPU busy while the host waits.
+    void indicator_mark() {
+        QB_CUDA(cudaEventRecord(ind_ev, c.st));
+        ind_ev_armed = true;
+    }
     std::pair<int, bool> indicator_finish() {
-        QB_CUDA(cudaStreamSynchronize(c.st));
+        if (ind_ev_armed) QB_CUDA(cudaEventSynchronize(ind_ev));
+        else QB_CUDA(cudaStreamSynchronize(c.st));
+        ind_ev_armed = false;
         return {c.h_ind->keep, c.h_ind->met != 0};
     }
     std::pair<int, bool> indicator(int d, bool check) {
@@ -1101,6 +1116,15 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
     DBuf zfull(nsh && p.power > 0 ? static_cast<std::size_t>(n_pad) * lyz : 0, c.st);
     DBuf mbuf(static_cast<std::size_t>(std::max<std::int64_t>(cap, 1)) * bpad, c.st);
     double e_host = norm_a_sq;
+    // The next block's first pass Y = A Omega_{i+1} does not depend on block i's outcome: it is
+    // queued behind block i's indicator read-back, so the GPU keeps working while the host waits
+    // for the stop decision (QBFAC_EI_PREFETCH=0 disables). Discarded when block i terminates or
+    // is recomputed; counted as a pass only when the next block uses it.
+    static const bool prefetch_on = [] {
+        const char* e = std::getenv("QBFAC_EI_PREFETCH");
+        return !(e && e[0] == '0');
+    }();
+    bool y_pre = false;
     while (true) {
         if (s.k >= cap) { term = 0; break; }
         const std::int64_t bi = std::min(p.b, cap - s.k);
@@ -1108,7 +1132,7 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
         const std::int64_t passes_before = a.passes;
         // blocks before the last are full width, so block j starts at draw g_used = j * n * bmax
         const std::int64_t jblk = g_used / (n * bmax);
-        if (batch_first < 0 || jblk >= batch_first + nb_batch || g_used % (n * bmax) != 0) {
+        if (batch_first < 0 || jblk < batch_first || jblk >= batch_first + nb_batch || g_used % (n * bmax) != 0) {
             batch_first = jblk;
             batch_cols = std::min(nb_batch * bmax, cap - s.k);
             MatView all{om.p, n, batch_cols, ldom, true};
@@ -1125,7 +1149,9 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             a.passes = passes_before;
             eng.begin_block(/*optimistic=*/true, /*force_hh=*/attempt > 0);
             // step 5: Y = A Omega_i - Q (B Omega_i)   (Omega_i drawn with its batch above)
-            eng.apply(omv, yv); a.passes += 1;
+            if (!(attempt == 0 && y_pre)) eng.apply(omv, yv);
+            y_pre = false;
+            a.passes += 1;
             if (s.k > 0) {
                 eng.gemm(1.0, s.btk().t(), omv.rows_range(c0, nl), 0.0, mv);  // B Omega_i (partial if nsh)
                 if (nsh) eng.allreduce_view(mv);
@@ -1184,8 +1210,20 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             a.passes += 1;
             s.indicator_enqueue(d, fixed_prec);
             eng.fetch_lazy();
+            if (prefetch_on && attempt == 0 && d == bi && bi == bmax) {
+                // next block (if this one neither terminates nor is recomputed): k + bi columns,
+                // Omega at draw offset g_used + n bi, i.e. block jblk + 1 of the batch
+                const std::int64_t bn = std::min(p.b, cap - (s.k + bi));
+                if (bn > 0 && jblk + 1 < batch_first + nb_batch && (jblk + 1 - batch_first) * bmax + bn <= batch_cols) {
+                    s.indicator_mark();
+                    eng.apply(MatView{om.p + (jblk + 1 - batch_first) * bmax, n, bn, ldom, true},
+                              MatView{y.p, m, bn, lyz, true});
+                    y_pre = true;
+                }
+            }
             std::tie(keep, met) = s.indicator_finish();
             if (attempt == 0 && !eng.lazy_ok()) {  // every rank sees the same (reduced) statuses
+                y_pre = false;  // the block is recomputed (Y overwritten)
                 s.set_e(e_host);  // undo this block's indicator update
                 continue;
             }
