@@ -303,6 +303,21 @@ void make_tmap(CUtensorMap* map, const double* base, std::int64_t inner, std::in
     if (r != CUDA_SUCCESS) throw QbError(kError, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
 }
 
+// Resident CTAs per SM of one warp-specialised instance (opts its shared memory in once per device).
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int NP>
+int ws_per_sm() {
+    using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
+    auto kern = dgemm_ws_kernel<BM, BN, BK, WM, WN, STAGES, AR, BR, NP>;
+    constexpr int smem = T::SMEM_BYTES + 2 * STAGES * 8;
+    static PerDevice<int> setup;
+    return setup.get([&] {
+        int v = 0;
+        QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, (WM * WN + NP) * 32, smem));
+        return v < 1 ? 1 : v;
+    });
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AR, bool BR, int NP>
 void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, std::int64_t ldc, bool c_row, int M,
                int N, int K, int splits, int klen, double alpha, double beta, double* partial, int flags,
@@ -310,13 +325,7 @@ void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, s
     using T = Tile<BM, BN, BK, WM, WN, STAGES, AR, BR>;
     auto kern = dgemm_ws_kernel<BM, BN, BK, WM, WN, STAGES, AR, BR, NP>;
     constexpr int smem = T::SMEM_BYTES + 2 * STAGES * 8;
-    static PerDevice<int> setup;
-    const int per_sm = setup.get([&] {
-        int v = 0;
-        QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, (WM * WN + NP) * 32, smem));
-        return v < 1 ? 1 : v;
-    });
+    const int per_sm = ws_per_sm<BM, BN, BK, WM, WN, STAGES, AR, BR, NP>();
     WsArgs p{};
     p.A = a.p; p.lda = a.ld; p.B = b.p; p.ldb = b.ld; p.C = c; p.ldc = ldc; p.c_row = c_row ? 1 : 0;
     p.M = M; p.N = N; p.K = K; p.k_split_len = klen; p.splits = splits;
@@ -357,6 +366,19 @@ void launch_ws(cudaStream_t st, const MatView& a, const MatView& b, double* c, s
     const int grid = static_cast<int>(std::min<std::int64_t>(items, gmax));
     launch_pdl(kern, dim3(grid), dim3((WM * WN + NP) * 32), smem, st, p);
     QB_LAUNCH_CHECK();
+}
+
+// ws_per_sm for the instance dispatch_ws would launch
+template <bool AR, bool BR>
+int ws_occupancy(int fam) {
+    constexpr int NP = (!AR && BR) ? 1 : 2;
+    if (fam == 0) return ws_per_sm<128, 128, 32, 2, 4, 3, AR, BR, NP>();
+    if (fam == 1) return ws_per_sm<128, 64, 32, 4, 2, 4, AR, BR, NP>();
+    if (fam == 3) return ws_per_sm<128, 56, 32, 8, 1, 4, AR, BR, 2>();
+    if (fam == 4) return ws_per_sm<128, 80, 32, 4, 2, 3, AR, BR, NP>();
+    if (fam == 5) return ws_per_sm<128, 112, 32, 4, 2, 3, AR, BR, NP>();
+    if (fam == 6) return ws_per_sm<128, 104, 32, 8, 1, 3, AR, BR, NP>();
+    return ws_per_sm<64, 32, 32, 2, 2, 4, AR, BR, 2>();
 }
 
 template <bool AR, bool BR>
@@ -521,8 +543,20 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     if (ws_path && fam == Family::kSkinny56 && !a.rowmajor) bn = 64;
     const std::int64_t tiles = output_tiles(M, N, bm, bn, flags);
     const int sms = gemm_num_sms();
-    // Resident CTAs per SM ~1 for the wide/skinny tiles, ~3 for narrow.
-    const std::int64_t want = (fam == Family::kNarrow ? 3 : 1) * static_cast<std::int64_t>(sms);
+    // the same famid dispatch_ws uses below
+    const int famid = fam == Family::kWide ? (bn == 112 ? 5 : bn == 104 ? 6 : 0) : fam == Family::kWide80 ? 4
+                      : fam == Family::kSkinny56 ? (a.rowmajor ? 3 : 1) : fam == Family::kSkinny ? 1 : 2;
+    // Resident CTAs per SM: the warp-specialised instance's real occupancy (the 64 x 32 tiles:
+    // 2 per SM, not 3 — splitting for 3 left a second partial wave); legacy kernels ~1, narrow ~3.
+    int resident = fam == Family::kNarrow ? 3 : 1;
+    static const bool occ_split = [] {
+        const char* e = std::getenv("QBFAC_GEMM_OCC_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    if (ws_path && occ_split)
+        resident = a.rowmajor ? (b.rowmajor ? ws_occupancy<true, true>(famid) : ws_occupancy<true, false>(famid))
+                              : (b.rowmajor ? ws_occupancy<false, true>(famid) : ws_occupancy<false, false>(famid));
+    const std::int64_t want = static_cast<std::int64_t>(resident) * sms;
     int splits = 1;
     if (tiles < want && !tiny) {
         const std::int64_t max_by_k = std::max<std::int64_t>(1, K / (4 * bk));  // >= 4 k-tiles/split
@@ -538,9 +572,7 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     if (splits > 1) partial = ws.get(static_cast<std::size_t>(splits) * M * N);
     if (ws_path) {
         // warp-specialised TMA/mbarrier pipeline (gemm_ws.cuh)
-        // the 56-wide tile measured slower than 64 on the TMA path (tools/gemm_bench.py): use 64 there
-        const int famid = fam == Family::kWide ? (bn == 112 ? 5 : bn == 104 ? 6 : 0) : fam == Family::kWide80 ? 4
-                          : fam == Family::kSkinny56 ? (a.rowmajor ? 3 : 1) : fam == Family::kSkinny ? 1 : 2;
+        // (the 56-wide tile measured slower than 64 on the TMA path for A column-major: famid 1 there)
         {
             if (a.rowmajor) {
                 if (b.rowmajor) dispatch_ws<true, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags, &ws);
