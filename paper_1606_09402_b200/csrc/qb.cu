@@ -1480,18 +1480,37 @@ int qb_to_svd(Context& c, Result& r, std::int64_t k, double* u_out, std::int64_t
     QB_LAUNCH_CHECK();
     gather_scale_kernel<<<blocks, 256, 0, st>>>(wm.p, static_cast<int>(rk), d_idx, nullptr, static_cast<int>(k), wk.p);
     QB_LAUNCH_CHECK();
-    // U = Q U_r(:, top k), V = Q_b W(:, top k), both column-major for the copy-out
+    // U = Q U_r(:, top k), V = Q_b W(:, top k), both column-major for the copy-out. The copies
+    // (8 (m + n) k bytes, the PCIe-bound part at large k) run on the copy stream behind the
+    // product that fills them: V first, then U in column chunks, so all but the first product
+    // and the last chunk's copy overlap.
     DBuf ud(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * k, st), vd(static_cast<std::size_t>(n) * k, st);
     MatView ukv{uk.p, rk, k, rk, false}, wkv{wk.p, rk, k, rk, false};
-    MatView udv{ud.p, m, k, std::max<std::int64_t>(m, 1), false}, vdv{vd.p, n, k, n, false};
-    eng.gemm(1.0, r.q_view(), ukv, 0.0, udv);
+    MatView vdv{vd.p, n, k, n, false};
+    cudaEvent_t ev;
+    QB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    auto copy_out = [&](double* dst, std::int64_t ldd, const double* src, std::int64_t rows, std::int64_t cols) {
+        QB_CUDA(cudaEventRecord(ev, st));
+        QB_CUDA(cudaStreamWaitEvent(c.st_copy, ev, 0));
+        QB_CUDA(cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, rows * sizeof(double), rows * sizeof(double),
+                                  static_cast<std::size_t>(cols), cudaMemcpyDeviceToHost, c.st_copy));
+    };
     eng.gemm(1.0, xv, wkv, 0.0, vdv);
-    if (m > 0)
-        QB_CUDA(cudaMemcpy2DAsync(u_out, ldu * sizeof(double), ud.p, m * sizeof(double), m * sizeof(double), k,
-                                  cudaMemcpyDeviceToHost, st));
-    QB_CUDA(cudaMemcpy2DAsync(v_out, ldv * sizeof(double), vd.p, n * sizeof(double), n * sizeof(double), k,
-                              cudaMemcpyDeviceToHost, st));
+    copy_out(v_out, ldv, vd.p, n, k);
+    if (m > 0) {
+        const std::int64_t nchunk = (m * k >= (std::int64_t{1} << 24)) ? 4 : 1;
+        const std::int64_t cw = ceil_div(k, nchunk);
+        for (std::int64_t c0 = 0; c0 < k; c0 += cw) {
+            const std::int64_t cn = std::min(cw, k - c0);
+            MatView ukc{uk.p + c0 * rk, rk, cn, rk, false};
+            MatView udc{ud.p + c0 * m, m, cn, m, false};
+            eng.gemm(1.0, r.q_view(), ukc, 0.0, udc);
+            copy_out(u_out + c0 * ldu, ldu, ud.p + c0 * m, m, cn);
+        }
+    }
+    QB_CUDA(cudaStreamSynchronize(c.st_copy));
     QB_CUDA(cudaStreamSynchronize(st));
+    QB_CUDA(cudaEventDestroy(ev));
     std::copy(sig.begin(), sig.end(), s_out);
     return sweeps;
 }

@@ -707,6 +707,25 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
 // a generation word in global memory (bar[0], bar[1]; zero-initialised once per context).
 // Waiting CTAs poll with __nanosleep backoff so the CTA doing serial work between barriers
 // (the Cholesky on CTA 0) does not compete with a storm of polling loads.
+// Tight-polling variant for kernels whose CTAs all wait (no CTA does serial work between
+// barriers): the backoff of grid_barrier would only add wake-up latency.
+__device__ __forceinline__ void grid_barrier_tight(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) {}
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1627,6 +1646,370 @@ __global__ void __launch_bounds__(kJbThreads) jacobi_block_kernel(JacobiBlockArg
     }
 }
 
+// ---- block one-sided Jacobi with a Gram-based inner solver (qb_to_svd at large r) ----------
+// Same outer schedule as jacobi_block_kernel (circle method over nb = 8 column blocks, one CTA per
+// block pair, one grid barrier per outer round), but the sequential inner rounds no longer touch
+// the r-long columns: the CTA forms the 16 x 16 Gram G = X^T X of the pair's staged columns once
+// (fresh, fixed-order dots), ONE warp diagonalises G by two-sided Jacobi rotations on the 16 x 16
+// shared-memory tile (`inner` cyclic sweeps, 8 disjoint rotations per round, each lane transforms
+// two 2 x 2 blocks of G in place) while accumulating V, and the whole CTA applies V once to the
+// columns of N (from shared memory) and of W (global). Convergence is judged on the fresh Gram
+// only (pairs with |g_pq| > tol sqrt(g_pp g_qq) before any rotation), so the stopping rule is the
+// scalar kernel's; a pair block with no such pair is left untouched.
+constexpr int kJgNc = 16;
+constexpr int kJgMaxCta = 2;  // CTAs per block pair (cluster size)
+constexpr int kJgGramWarps = 8;   // warps forming the Gram (one partial buffer each)
+constexpr int kJgInnerWarps = 6;  // warps of the inner two-sided Jacobi (2 on G, 4 on V)
+
+struct JacobiGramArgs {
+    double* nmat;
+    double* w;
+    int r, nblk, max_sweeps, inner;
+    double tol;
+    unsigned* gbar;
+    unsigned* rotated;
+    int* sweeps_out;
+    int trace;
+};
+
+// rows A and 15 - A of the upper triangle of G over this warp's row range (17 dots)
+template <int A>
+__device__ __forceinline__ void jg_gram_rows(const double* __restrict__ cols, int r, int i0, int i1, int lane,
+                                             double* __restrict__ out) {
+    constexpr int B = kJgNc - 1 - A;
+    double ra[kJgNc - A], rb[kJgNc - B];
+#pragma unroll
+    for (int c = 0; c < kJgNc - A; ++c) ra[c] = 0.0;
+#pragma unroll
+    for (int c = 0; c < kJgNc - B; ++c) rb[c] = 0.0;
+#pragma unroll 1
+    for (int i = i0 + lane; i < i1; i += 32) {
+        double x[kJgNc - A];
+#pragma unroll
+        for (int c = 0; c < kJgNc - A; ++c) x[c] = cols[static_cast<std::size_t>(A + c) * r + i];
+#pragma unroll
+        for (int c = 0; c < kJgNc - A; ++c) ra[c] = fma(x[0], x[c], ra[c]);
+#pragma unroll
+        for (int c = 0; c < kJgNc - B; ++c) rb[c] = fma(x[B - A], x[B - A + c], rb[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < kJgNc - A; ++c) {
+        double v = ra[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) out[A * kJgNc + A + c] = v;
+    }
+#pragma unroll
+    for (int c = 0; c < kJgNc - B; ++c) {
+        double v = rb[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) out[B * kJgNc + B + c] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kJbThreads, 1) jacobi_gram_kernel(JacobiGramArgs p) {
+    extern __shared__ __align__(16) double jsm[];
+    constexpr int NC = kJgNc, nb = NC / 2;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int crank = static_cast<int>(cluster.block_rank()), ncta = static_cast<int>(cluster.num_blocks());
+    const int r = p.r;
+    // this CTA's rows of the pair's columns: [row0, row0 + rl); slices start on even rows so a
+    // column slice is one 16-byte aligned bulk copy when r is even
+    const int rs = ((r + ncta - 1) / ncta + 1) & ~1;
+    const int row0 = min(r, crank * rs), rl = min(r, row0 + rs) - row0;
+    double* cols = jsm;                                        // NC column slices of N (column c at cols + c rs)
+    double* wcols = jsm + static_cast<std::size_t>(NC) * rs;  // the same slices of W (prefetched for the apply)
+    double* V = wcols + static_cast<std::size_t>(NC) * rs;    // NC x NC, column-major
+    double* G = V + NC * NC;                                   // NC x NC, symmetric
+    double* Gp = G + NC * NC;                                  // kJgGramWarps partial Grams (row steps w mod 8)
+    double* Gx = Gp + kJgGramWarps * NC * NC;                  // [parity][rank] partial Grams pushed by the cluster
+    __shared__ unsigned s_cnt;
+    __shared__ __align__(8) std::uint64_t s_bar, s_wbar;
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // per-phase time of the traced CTA (thread 0)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int half = p.nblk / 2;
+    const int cid = blockIdx.x / ncta, ncl = gridDim.x / ncta;
+    const int g8 = lane >> 2, t4 = lane & 3;  // DMMA m16n8k4 fragment coordinates
+    const bool bulk = (r & 1) == 0 && rl > 0;
+    const double tol2 = p.tol * p.tol;
+    unsigned parity = 0, visit = 0;
+    if (tid == 0) {
+        pb_init(&s_bar, 1);
+        pb_init(&s_wbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    int sweep = 0;
+    for (; sweep < p.max_sweeps; ++sweep) {
+        for (int step = 0; step < p.nblk - 1; ++step) {
+            for (int t = cid; t < half; t += ncl) {
+                unsigned long long tp = jb_now();
+                int bi, bj;
+                circle_pair(step, t, p.nblk, bi, bj);
+                const int i0 = bi * nb, j0 = bj * nb;
+                const int ni = max(0, min(nb, r - i0)), nj = max(0, min(nb, r - j0));
+                auto gcol = [&](int c) -> int {
+                    return c < nb ? (c < ni ? i0 + c : -1) : (c - nb < nj ? j0 + c - nb : -1);
+                };
+                if (bulk) {
+                    if (tid == 0) {
+                        // the columns were written by other CTAs (generic proxy) before the grid barrier
+                        asm volatile("fence.proxy.async;\n" ::: "memory");
+                        pb_arrive_tx(&s_bar, static_cast<unsigned>((ni + nj) * rl * 8));
+                        for (int c = 0; c < NC; ++c) {
+                            const int g = gcol(c);
+                            if (g >= 0)
+                                pb_bulk(cols + static_cast<std::size_t>(c) * rs,
+                                        p.nmat + static_cast<std::int64_t>(g) * r + row0, static_cast<unsigned>(rl * 8), &s_bar);
+                        }
+                        pb_arrive_tx(&s_wbar, static_cast<unsigned>((ni + nj) * rl * 8));
+                        for (int c = 0; c < NC; ++c) {
+                            const int g = gcol(c);
+                            if (g >= 0)
+                                pb_bulk(wcols + static_cast<std::size_t>(c) * rs,
+                                        p.w + static_cast<std::int64_t>(g) * r + row0, static_cast<unsigned>(rl * 8), &s_wbar);
+                        }
+                    }
+                    if (ni + nj < NC)
+                        for (int idx = tid; idx < NC * rl; idx += kJbThreads) {
+                            const int c = idx / rl;
+                            if (gcol(c) < 0) cols[static_cast<std::size_t>(c) * rs + (idx - c * rl)] = 0.0;
+                        }
+                } else {
+                    for (int base = tid; base < NC * rl; base += 8 * kJbThreads) {
+                        double v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int idx = base + u * kJbThreads;
+                            v[u] = 0.0;
+                            if (idx < NC * rl) {
+                                const int c = idx / rl, g = gcol(c);
+                                if (g >= 0) v[u] = p.nmat[static_cast<std::int64_t>(g) * r + row0 + (idx - c * rl)];
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int idx = base + u * kJbThreads;
+                            if (idx < NC * rl) {
+                                const int c = idx / rl;
+                                cols[static_cast<std::size_t>(c) * rs + (idx - c * rl)] = v[u];
+                            }
+                        }
+                    }
+                }
+                if (tid < NC * NC) V[tid] = (tid % NC == tid / NC) ? 1.0 : 0.0;
+                if (bulk) {
+                    pb_wait(&s_bar, parity);
+                    parity ^= 1u;
+                }
+                __syncthreads();
+                if (tid == 0) { const unsigned long long q = jb_now(); ph[5] += q - tp; tp = q; }
+                if (warp < kJgGramWarps) {
+                    // fresh Gram G = X^T X on the FP64 tensor pipe (m16n8k4: A = X^T, B = X, so the B
+                    // fragments are the A fragments); warp w takes the 4-row steps w, w + 8, ...
+                    double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
+                    const double* c0 = cols + static_cast<std::size_t>(g8) * rs;
+                    const double* c1 = cols + static_cast<std::size_t>(g8 + 8) * rs;
+                    for (int i = 4 * warp + t4; i < ((rl + 3) & ~3); i += 4 * kJgGramWarps) {
+                        const double v0 = i < rl ? c0[i] : 0.0, v1 = i < rl ? c1[i] : 0.0;
+                        dmma_16x8x4(acc0, v0, v1, v0);
+                        dmma_16x8x4(acc1, v0, v1, v1);
+                    }
+                    double* out = Gp + warp * NC * NC;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int m = g8 + (e >= 2 ? 8 : 0), n = 2 * t4 + (e & 1);
+                        out[m * NC + n] = acc0[e];
+                        out[m * NC + 8 + n] = acc1[e];
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) { const unsigned long long q = jb_now(); ph[6] += q - tp; tp = q; }
+                // every CTA pushes its partial into every CTA's Gx[visit parity][its rank]; one cluster
+                // barrier; the sum runs in rank order (identical G on every CTA). The buffer of this
+                // parity is rewritten two visits later, behind the next visit's cluster barrier.
+                {
+                    double* gx = Gx + (visit & 1u) * (kJgMaxCta * NC * NC);
+                    if (tid < NC * NC && tid / NC <= tid % NC) {
+                        double v = 0.0;
+#pragma unroll
+                        for (int w8 = 0; w8 < kJgGramWarps; ++w8) v += Gp[w8 * NC * NC + tid];  // fixed order
+                        for (int c = 0; c < ncta; ++c) cluster.map_shared_rank(gx, c)[crank * NC * NC + tid] = v;
+                    }
+                    cluster.sync();
+                    if (tid < NC * NC) {
+                        const int a = tid / NC, b = tid % NC;
+                        const int e = min(a, b) * NC + max(a, b);
+                        double sum = 0.0;
+                        for (int c = 0; c < ncta; ++c) sum += gx[c * NC * NC + e];
+                        G[tid] = sum;
+                    }
+                    ++visit;
+                    __syncthreads();
+                }
+                if (tid == 0) { const unsigned long long q = jb_now(); ph[0] += q - tp; tp = q; }
+                if (warp < kJgInnerWarps) {
+                    // pairs above the threshold in the fresh Gram (over 32 lanes; every inner warp
+                    // counts for itself). The first outer round of a sweep rotates all 120 pairs of the
+                    // 16 columns (circle order, 15 rounds); the others only the 64 cross pairs of the
+                    // two blocks (8 rounds): every global pair is then rotated exactly once per sweep,
+                    // as in the scalar kernel.
+                    const bool full = step == 0;
+                    unsigned cnt = 0;
+                    for (int e = lane; e < NC * (NC - 1) / 2; e += 32) {
+                        int a = 0, rem = e;
+                        while (rem >= NC - 1 - a) { rem -= NC - 1 - a; ++a; }
+                        const int b = a + 1 + rem;
+                        if (!full && !(a < nb && b >= nb)) continue;  // not rotated in this visit
+                        const double al = G[a * NC + a], be = G[b * NC + b], ga = G[a * NC + b];
+                        cnt += fabs(ga) > p.tol * sqrt(al * be) ? 1u : 0u;
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                    if (tid == 0) s_cnt = cnt;
+                    if (cnt) {
+                        // Two-sided Jacobi on G over kJgInnerWarps warps (every CTA of the cluster runs
+                        // the same sequence on the same G: identical V). Per round, lanes 0-7 of EVERY
+                        // inner warp compute the 8 rotations redundantly (no shared-memory hand-off):
+                        // cos 2t = |x| / h, h = sqrt(x^2 + y^2), x = g_bb - g_aa, y = 2 g_ab, from two
+                        // reciprocal square roots; the other lanes fetch (c, s) by shuffle. Warps 0-1:
+                        // one 2 x 2 block of G per lane (row pair qi x column pair qj, in place);
+                        // warps 2-5: one (row, pair) of V per lane. One named barrier per round.
+                        const int item = warp * 32 + lane;
+                        const bool isg = warp < 2;
+                        const int qi = isg ? item >> 3 : 0, qj = isg ? item & 7 : (item - 64) >> 4;
+                        const int vrow = (item - 64) & 15;
+                        for (int isw = 0; isw < p.inner; ++isw) {
+                            for (int rd = 0; rd < (full ? NC - 1 : nb); ++rd) {
+                                auto pair_of = [&](int q, int& a, int& b) {
+                                    if (full) {
+                                        circle_pair(rd, q, NC, a, b);
+                                    } else {
+                                        a = q;
+                                        b = nb + ((q + rd) & (nb - 1));
+                                    }
+                                };
+                                int ai, bi2, aj, bj2;
+                                pair_of(qi, ai, bi2);
+                                pair_of(qj, aj, bj2);
+                                // data of this lane's item (independent of the rotation parameters)
+                                double g00, g01, g10, g11;
+                                if (isg) {
+                                    g00 = G[ai * NC + aj]; g01 = G[ai * NC + bj2];
+                                    g10 = G[bi2 * NC + aj]; g11 = G[bi2 * NC + bj2];
+                                } else {
+                                    g00 = V[vrow + aj * NC]; g01 = V[vrow + bj2 * NC];
+                                    g10 = 0.0; g11 = 0.0;
+                                }
+                                double c = 1.0, sn = 0.0;
+                                {
+                                    int a, b;
+                                    pair_of(lane & (nb - 1), a, b);
+                                    const double al = G[a * NC + a], be = G[b * NC + b], ga = G[a * NC + b];
+                                    if (ga * ga > tol2 * (al * be)) {
+                                        const double x = be - al, y = 2.0 * ga;
+                                        const double rh = rsqrt(fma(x, x, y * y));
+                                        const double c2 = fma(0.5 * fabs(x), rh, 0.5);
+                                        const double rc = rsqrt(c2);
+                                        c = c2 * rc;
+                                        const double sa = 0.5 * fabs(y) * rh * rc;
+                                        sn = ((x >= 0.0) == (y >= 0.0)) ? sa : -sa;
+                                    }
+                                }
+                                const double cj = __shfl_sync(0xffffffffu, c, qj), sj = __shfl_sync(0xffffffffu, sn, qj);
+                                const double ci = __shfl_sync(0xffffffffu, c, qi), si = __shfl_sync(0xffffffffu, sn, qi);
+                                // every read of G for this round is done before any lane overwrites it
+                                asm volatile("bar.sync 2, %0;\n" ::"n"(kJgInnerWarps * 32) : "memory");
+                                if (isg) {
+                                    const double t00 = cj * g00 - sj * g01, t01 = sj * g00 + cj * g01;
+                                    const double t10 = cj * g10 - sj * g11, t11 = sj * g10 + cj * g11;
+                                    G[ai * NC + aj] = ci * t00 - si * t10;
+                                    G[ai * NC + bj2] = ci * t01 - si * t11;
+                                    G[bi2 * NC + aj] = si * t00 + ci * t10;
+                                    G[bi2 * NC + bj2] = si * t01 + ci * t11;
+                                } else {
+                                    V[vrow + aj * NC] = cj * g00 - sj * g01;
+                                    V[vrow + bj2 * NC] = sj * g00 + cj * g01;
+                                }
+                                asm volatile("bar.sync 2, %0;\n" ::"n"(kJgInnerWarps * 32) : "memory");
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) { const unsigned long long q = jb_now(); ph[1] += q - tp; tp = q; }
+                if (bulk) {  // the W slices have landed (waited for even when unused: the barrier phase must advance)
+                    pb_wait(&s_wbar, parity ^ 1u);
+                    if (tid == 0) { const unsigned long long q = jb_now(); ph[7] += q - tp; tp = q; }
+                }
+                if (s_cnt) {
+                    // N[rows, pair] = X V and W[rows, pair] = W[rows, pair] V on the FP64 tensor pipe:
+                    // 16-row tiles (m16n8k4, K = 16: four steps, two 8-column halves), V fragments held
+                    // in registers; the N slices come from shared memory, W's too when prefetched
+                    double bv[4][2];
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                        bv[ks][0] = V[(4 * ks + t4) + g8 * NC];
+                        bv[ks][1] = V[(4 * ks + t4) + (8 + g8) * NC];
+                    }
+                    int gk[4];
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) gk[ks] = gcol(4 * ks + t4);
+                    const int ntile = (rl + 15) >> 4;
+                    for (int tile = warp; tile < 2 * ntile; tile += kJbThreads / 32) {
+                        const bool isw = tile >= ntile;
+                        const int rbase = 16 * (isw ? tile - ntile : tile);
+                        const double* src = isw ? wcols : cols;
+                        double* dstm = isw ? p.w : p.nmat;
+                        const int ra = rbase + g8, rb = ra + 8;
+                        double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks) {
+                            double a0 = 0.0, a1 = 0.0;
+                            if (isw && !bulk) {
+                                if (gk[ks] >= 0) {
+                                    const double* wc = p.w + static_cast<std::int64_t>(gk[ks]) * r + row0;
+                                    if (ra < rl) a0 = wc[ra];
+                                    if (rb < rl) a1 = wc[rb];
+                                }
+                            } else if (gk[ks] >= 0) {
+                                const double* sc = src + static_cast<std::size_t>(4 * ks + t4) * rs;
+                                if (ra < rl) a0 = sc[ra];
+                                if (rb < rl) a1 = sc[rb];
+                            }
+                            dmma_16x8x4(acc0, a0, a1, bv[ks][0]);
+                            dmma_16x8x4(acc1, a0, a1, bv[ks][1]);
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int row = e >= 2 ? rb : ra;
+                            if (row >= rl) continue;
+                            const int n0 = 2 * t4 + (e & 1);
+                            const int ga = gcol(n0), gb2 = gcol(8 + n0);
+                            if (ga >= 0) dstm[static_cast<std::int64_t>(ga) * r + row0 + row] = acc0[e];
+                            if (gb2 >= 0) dstm[static_cast<std::int64_t>(gb2) * r + row0 + row] = acc1[e];
+                        }
+                    }
+                    if (tid == 0 && crank == 0) atomicAdd(p.rotated + sweep, s_cnt);
+                }
+                __syncthreads();
+                if (tid == 0) { const unsigned long long q = jb_now(); ph[3] += q - tp; }
+            }
+            const unsigned long long tb = jb_now();
+            grid_barrier_tight(p.gbar, gridDim.x);
+            if (tid == 0) ph[4] += jb_now() - tb;
+        }
+        if (*reinterpret_cast<volatile unsigned*>(p.rotated + sweep) == 0) break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.sweeps_out = sweep;
+    if (p.trace && blockIdx.x == (gridDim.x > ncta ? ncta : 0) && threadIdx.x == 0)
+        printf("jacobi_gram r=%d CTAs=%d cluster=%d inner=%d sweeps=%d (CTA %d): load %.1f  gram %.1f  exchange %.1f  inner %.1f  "
+               "w-wait %.1f  apply %.1f  barrier %.1f us\n",
+               r, gridDim.x, ncta, p.inner, sweep, blockIdx.x, ph[5] * 1e-3, ph[6] * 1e-3, ph[0] * 1e-3, ph[1] * 1e-3, ph[7] * 1e-3,
+               ph[3] * 1e-3, ph[4] * 1e-3);
+}
+
 // C = A * B for upper-triangular n x n operands staged in shared memory; blockIdx.x
 // selects one of two independent products so R = Rb*Ra and Rinv = Ra^{-1} Rb^{-1}
 // are formed in one launch.
@@ -2085,8 +2468,51 @@ int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, 
             nb = cand;
             break;
         }
+    // rotation threshold |g_pq| <= tol sqrt(g_pp g_qq): sqrt(r) eps (LAPACK dgesvj's choice), the
+    // rounding level of an r-long dot product; a tighter threshold only chases that noise
+    const double tol = std::max(1e-15, 2.220446049250313e-16 * std::sqrt(static_cast<double>(r)));
     const char* force_scalar = std::getenv("QBFAC_JACOBI_SCALAR");
-    if (nb > 0 && !(force_scalar && force_scalar[0] == '1')) {
+    const char* gram_env = std::getenv("QBFAC_JACOBI_GRAM");
+    const bool use_gram = nb == 8 && r <= 1568 && !(gram_env && gram_env[0] == '0');
+    if (use_gram && !(force_scalar && force_scalar[0] == '1')) {
+        const int nblk = static_cast<int>(2 * ceil_div(ceil_div(r, 8), 2));
+        // one cluster of 2 CTAs per block pair (each stages half of the rows) when the pairs fit the
+        // SMs twice; QBFAC_JACOBI_CLUSTER=1 keeps one CTA per pair
+        const char* cl_env = std::getenv("QBFAC_JACOBI_CLUSTER");
+        int ncta = cl_env ? std::max(1, std::min(kJgMaxCta, std::atoi(cl_env))) : kJgMaxCta;
+        if (r < 64) ncta = 1;
+        auto smem_for = [&](int nc) {
+            return static_cast<int>(
+                (2 * kJgNc * round_up(ceil_div(r, nc), 2) + (2 + kJgGramWarps + 2 * kJgMaxCta) * kJgNc * kJgNc) * 8);
+        };
+        if (smem_for(ncta) > 224 * 1024) ncta = kJgMaxCta;
+        const int smem = smem_for(ncta);
+        static PerDevice<bool> setup;
+        setup.get([] {
+            QB_CUDA(cudaFuncSetAttribute(jacobi_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+            return true;
+        });
+        const int gb = std::max(1, std::min(nblk / 2, gemm_num_sms() / ncta)) * ncta;
+        const char* tr = std::getenv("QBFAC_JACOBI_TRACE");
+        const char* in_env = std::getenv("QBFAC_JACOBI_INNER");
+        const int inner = in_env ? std::max(1, std::min(8, std::atoi(in_env))) : 1;
+        JacobiGramArgs a{nmat, w, r, nblk, max_sweeps, inner, tol, gbar, rotated, sweeps, tr && tr[0] == '1' ? 1 : 0};
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(gb));
+        cfg.blockDim = dim3(kJbThreads);
+        cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = static_cast<unsigned>(ncta);
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        QB_CUDA(cudaLaunchKernelEx(&cfg, jacobi_gram_kernel, a));
+    } else if (nb > 0 && !(force_scalar && force_scalar[0] == '1')) {
         const int nblk = static_cast<int>(2 * ceil_div(ceil_div(r, nb), 2));
         const int smem = static_cast<int>((2 * nb * static_cast<std::int64_t>(r) + 4 * nb * nb) * 8);
         static PerDevice<bool> setup;
@@ -2098,11 +2524,11 @@ int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, 
         QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_block_kernel, kJbThreads, smem));
         const int gb = std::max(1, std::min(nblk / 2, std::max(per_sm, 1) * gemm_num_sms()));
         const char* tr = std::getenv("QBFAC_JACOBI_TRACE");
-        JacobiBlockArgs a{nmat, w, r, nb, nblk, max_sweeps, 1e-15, gbar, rotated, sweeps, tr && tr[0] == '1' ? 1 : 0};
+        JacobiBlockArgs a{nmat, w, r, nb, nblk, max_sweeps, tol, gbar, rotated, sweeps, tr && tr[0] == '1' ? 1 : 0};
         void* args[] = {&a};
         QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_block_kernel), gb, kJbThreads, args, smem, st));
     } else {
-        JacobiArgs a{nmat, w, r, rp, max_sweeps, 1e-15, gbar, rotated, sweeps};
+        JacobiArgs a{nmat, w, r, rp, max_sweeps, tol, gbar, rotated, sweeps};
         void* args[] = {&a};
         QB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_svd_kernel), grid, 256, args, 0, st));
     }
