@@ -707,25 +707,6 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_wide_kernel(CholWideArgs
 // a generation word in global memory (bar[0], bar[1]; zero-initialised once per context).
 // Waiting CTAs poll with __nanosleep backoff so the CTA doing serial work between barriers
 // (the Cholesky on CTA 0) does not compete with a storm of polling loads.
-// Tight-polling variant for kernels whose CTAs all wait (no CTA does serial work between
-// barriers): the backoff of grid_barrier would only add wake-up latency.
-__device__ __forceinline__ void grid_barrier_tight(unsigned* bar, unsigned nblocks) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == nblocks - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g) {}
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -742,6 +723,25 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
                 __nanosleep(ns);
                 ns = ns < 512 ? 2 * ns : 512;
             }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+// Tight-polling variant for kernels whose CTAs all wait (no CTA does serial work between
+// barriers): the backoff of grid_barrier would only add wake-up latency.
+__device__ __forceinline__ void grid_barrier_tight(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) {}
         }
         __threadfence();
     }
