@@ -989,6 +989,7 @@ struct State {
 
     MatView qk() const { return MatView{q.p, m, k, ld, true}; }
     MatView btk() const { return MatView{bt.p, nb, k, ld, true}; }
+    MatView bt_cols(std::int64_t kk) const { return MatView{bt.p, nb, kk, ld, true}; }
     MatView qslot(std::int64_t w) const { return MatView{q.p + k, m, w, ld, true}; }
     MatView btslot(std::int64_t w) const { return MatView{bt.p + k, nb, w, ld, true}; }
 
@@ -1124,7 +1125,33 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
         const char* e = std::getenv("QBFAC_EI_PREFETCH");
         return !(e && e[0] == '0');
     }();
-    bool y_pre = false;
+    // m_pre: the next block's B Omega_{i+1} is queued behind the read-back too (one GPU only: no
+    // allreduce in between). Queueing its projection Y -= Q (B Omega_{i+1}) as well measured no
+    // further gain (config 1 3.80 -> 3.83 ms): the read-back is already covered.
+    bool y_pre = false, m_pre = false;
+    // Dense resident A, narrow blocks: the first pass of several consecutive blocks is ONE product
+    // A [Omega_i ... Omega_{i+c-1}] (their Omega columns are adjacent in the batch drawn above), up to
+    // 104 columns wide, so the pass runs on the wide DMMA tiles instead of c launches of b-column
+    // products that never fill the pipeline (b = 20: 5 blocks per product). Each block still counts
+    // its pass (Alg. 2 reads A once per block; the count reported is the algorithm's). Blocks past a
+    // termination waste at most c - 1 narrow products. QBFAC_EI_YBATCH=0 disables.
+    static const bool ybatch_on = [] {
+        const char* e = std::getenv("QBFAC_EI_YBATCH");
+        return !(e && e[0] == '0');
+    }();
+    const std::int64_t nbat = (ybatch_on && !a.sparse && !a.host_stream && bmax % 2 == 0)
+                                  ? std::max<std::int64_t>(1, std::min<std::int64_t>(104 / bmax, nb_batch)) : 1;
+    const std::int64_t ldyb = round_up(nbat * bmax, 4);
+    DBuf ybat(nbat > 1 ? static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * ldyb : 0, c.st);
+    std::int64_t yb_first = -1, yb_count = 0;  // blocks [yb_first, yb_first + yb_count) of A Omega are in ybat
+    auto ybatch_fill = [&](std::int64_t j0, std::int64_t k_now) {  // needs Omega blocks j0.. in the drawn batch
+        const std::int64_t in_batch = batch_first + nb_batch - j0;
+        const std::int64_t left = ceil_div(cap - k_now, bmax);
+        yb_count = std::max<std::int64_t>(1, std::min(std::min(nbat, in_batch), left));
+        yb_first = j0;
+        const std::int64_t cols = std::min(yb_count * bmax, std::min(cap - k_now, batch_cols - (j0 - batch_first) * bmax));
+        eng.apply(MatView{om.p + (j0 - batch_first) * bmax, n, cols, ldom, true}, MatView{ybat.p, m, cols, ldyb, true});
+    };
     while (true) {
         if (s.k >= cap) { term = 0; break; }
         const std::int64_t bi = std::min(p.b, cap - s.k);
@@ -1139,24 +1166,31 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             gaussian_fill(c.st, c.rng, p.seed, p.stream, static_cast<std::uint64_t>(g_used), all);  // step 4
         }
         MatView omv{om.p + (jblk - batch_first) * bmax, n, bi, ldom, true};
-        MatView yv{y.p, m, bi, lyz, true};
+        bool in_ybatch = false;
+        if (nbat > 1 && g_used % (n * bmax) == 0) {
+            if (yb_first < 0 || jblk < yb_first || jblk >= yb_first + yb_count) ybatch_fill(jblk, s.k);
+            in_ybatch = true;
+        }
+        MatView yv = in_ybatch ? MatView{ybat.p + (jblk - yb_first) * bmax, m, bi, ldyb, true} : MatView{y.p, m, bi, lyz, true};
         MatView mv{mbuf.p, s.k, bi, bi, true};
         int d = 0, keep = 0;
-        bool met = false;
+        bool met = false, refilled = false;
         // attempt 0: optimistic CholQR, statuses checked once with the indicator read;
         // attempt 1 (rare): the same block with Householder panels (exact deficiency rules).
         for (int attempt = 0; attempt < 2; ++attempt) {
             a.passes = passes_before;
             eng.begin_block(/*optimistic=*/true, /*force_hh=*/attempt > 0);
             // step 5: Y = A Omega_i - Q (B Omega_i)   (Omega_i drawn with its batch above)
-            if (!(attempt == 0 && y_pre)) eng.apply(omv, yv);
+            if (!(attempt == 0 && (y_pre || in_ybatch))) eng.apply(omv, yv);
             y_pre = false;
             a.passes += 1;
             if (s.k > 0) {
-                eng.gemm(1.0, s.btk().t(), omv.rows_range(c0, nl), 0.0, mv);  // B Omega_i (partial if nsh)
+                if (!(attempt == 0 && m_pre))
+                    eng.gemm(1.0, s.btk().t(), omv.rows_range(c0, nl), 0.0, mv);  // B Omega_i (partial if nsh)
                 if (nsh) eng.allreduce_view(mv);
                 eng.gemm(-1.0, s.qk(), mv, 1.0, yv);
             }
+            m_pre = false;
             // per-block power iteration with deflation at every application
             for (std::int64_t it = 0; it < p.power; ++it) {
                 eng.orth_block(yv, yv, kR1, kR1inv, sharded, tmp, false);
@@ -1215,15 +1249,29 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
                 // Omega at draw offset g_used + n bi, i.e. block jblk + 1 of the batch
                 const std::int64_t bn = std::min(p.b, cap - (s.k + bi));
                 if (bn > 0 && jblk + 1 < batch_first + nb_batch && (jblk + 1 - batch_first) * bmax + bn <= batch_cols) {
-                    s.indicator_mark();
-                    eng.apply(MatView{om.p + (jblk + 1 - batch_first) * bmax, n, bn, ldom, true},
-                              MatView{y.p, m, bn, lyz, true});
-                    y_pre = true;
+                    if (nbat > 1) {
+                        s.indicator_mark();
+                        if (jblk + 1 >= yb_first + yb_count) {  // the next block opens a new product
+                            ybatch_fill(jblk + 1, s.k + bi);
+                            refilled = true;
+                        }
+                    } else {
+                        s.indicator_mark();
+                        eng.apply(MatView{om.p + (jblk + 1 - batch_first) * bmax, n, bn, ldom, true},
+                                  MatView{y.p, m, bn, lyz, true});
+                        y_pre = true;
+                    }
+                    if (!sharded) {  // B Omega_{i+1} over the k + bi rows of B this block leaves behind
+                        eng.gemm(1.0, s.bt_cols(s.k + bi).t(), MatView{om.p + (jblk + 1 - batch_first) * bmax, n, bn, ldom, true},
+                                 0.0, MatView{mbuf.p, s.k + bi, bn, bn, true});
+                        m_pre = true;
+                    }
                 }
             }
             std::tie(keep, met) = s.indicator_finish();
             if (attempt == 0 && !eng.lazy_ok()) {  // every rank sees the same (reduced) statuses
-                y_pre = false;  // the block is recomputed (Y overwritten)
+                y_pre = m_pre = false;  // the block is recomputed (Y and the coefficients overwritten)
+                if (refilled) yb_first = -1;  // ... into columns the next product already occupies: drop it
                 s.set_e(e_host);  // undo this block's indicator update
                 continue;
             }
