@@ -16,6 +16,7 @@ timeout 900 ncu --set full --import-source on --clock-control none --profile-fro
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:csr_spmm -s 2 -c 1 -o $O/spmm_cfg5 python tools/spmm_bench.py --configs 5 > $O/ncu_spmm5.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:cholqr2 -s 1 -c 1 -o $O/panel_1e5x50 python tools/panel_one.py 100000 50 3 > $O/ncu_panel.log 2>&1
 timeout 600 python tools/svd_time.py > $O/svd_time.log 2>&1
+timeout 300 python tools/jacobi_gram.py > $O/jacobi_gram.log 2>&1
 timeout 600 python tools/gemm_bench.py > $O/gemm_bench.log 2>&1
 timeout 600 python tools/spmm_bench.py > $O/spmm_bench.log 2>&1
 timeout 300 python tools/panel_trace.py > $O/panel_trace.log 2>&1
