@@ -1533,8 +1533,6 @@ int qb_to_svd(Context& c, Result& r, std::int64_t k, double* u_out, std::int64_t
     // product that fills them: V first, then U in column chunks, so all but the first product
     // and the last chunk's copy overlap.
     DBuf ud(static_cast<std::size_t>(std::max<std::int64_t>(m, 1)) * k, st), vd(static_cast<std::size_t>(n) * k, st);
-    MatView ukv{uk.p, rk, k, rk, false}, wkv{wk.p, rk, k, rk, false};
-    MatView vdv{vd.p, n, k, n, false};
     cudaEvent_t ev;
     QB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     auto copy_out = [&](double* dst, std::int64_t ldd, const double* src, std::int64_t rows, std::int64_t cols) {
@@ -1543,19 +1541,20 @@ int qb_to_svd(Context& c, Result& r, std::int64_t k, double* u_out, std::int64_t
         QB_CUDA(cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, rows * sizeof(double), rows * sizeof(double),
                                   static_cast<std::size_t>(cols), cudaMemcpyDeviceToHost, c.st_copy));
     };
-    eng.gemm(1.0, xv, wkv, 0.0, vdv);
-    copy_out(v_out, ldv, vd.p, n, k);
-    if (m > 0) {
-        const std::int64_t nchunk = (m * k >= (std::int64_t{1} << 24)) ? 4 : 1;
+    // (column chunks: the first copy starts after a quarter of the first product)
+    auto product_out = [&](const MatView& left, const double* coef, double* dev, std::int64_t rows, double* host,
+                           std::int64_t ldh) {
+        const std::int64_t nchunk = (rows * k >= (std::int64_t{1} << 24)) ? 4 : 1;
         const std::int64_t cw = ceil_div(k, nchunk);
         for (std::int64_t c0 = 0; c0 < k; c0 += cw) {
             const std::int64_t cn = std::min(cw, k - c0);
-            MatView ukc{uk.p + c0 * rk, rk, cn, rk, false};
-            MatView udc{ud.p + c0 * m, m, cn, m, false};
-            eng.gemm(1.0, r.q_view(), ukc, 0.0, udc);
-            copy_out(u_out + c0 * ldu, ldu, ud.p + c0 * m, m, cn);
+            eng.gemm(1.0, left, MatView{const_cast<double*>(coef) + c0 * rk, rk, cn, rk, false}, 0.0,
+                     MatView{dev + c0 * rows, rows, cn, rows, false});
+            copy_out(host + c0 * ldh, ldh, dev + c0 * rows, rows, cn);
         }
-    }
+    };
+    product_out(xv, wk.p, vd.p, n, v_out, ldv);
+    if (m > 0) product_out(r.q_view(), uk.p, ud.p, m, u_out, ldu);
     QB_CUDA(cudaStreamSynchronize(c.st_copy));
     QB_CUDA(cudaStreamSynchronize(st));
     QB_CUDA(cudaEventDestroy(ev));

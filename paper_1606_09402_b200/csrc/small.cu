@@ -1668,6 +1668,7 @@ struct JacobiGramArgs {
     double tol;
     unsigned* gbar;
     unsigned* rotated;
+    unsigned* ver;  // per column block: CTA-visits completed (zeroed before the launch)
     int* sweeps_out;
     int trace;
 };
@@ -1734,6 +1735,7 @@ __global__ void __launch_bounds__(kJbThreads, 1) jacobi_gram_kernel(JacobiGramAr
     const bool bulk = (r & 1) == 0 && rl > 0;
     const double tol2 = p.tol * p.tol;
     unsigned parity = 0, visit = 0;
+    int gstep = 0;  // outer rounds completed (over all sweeps)
     if (tid == 0) {
         pb_init(&s_bar, 1);
         pb_init(&s_wbar, 1);
@@ -1752,6 +1754,18 @@ __global__ void __launch_bounds__(kJbThreads, 1) jacobi_gram_kernel(JacobiGramAr
                 auto gcol = [&](int c) -> int {
                     return c < nb ? (c < ni ? i0 + c : -1) : (c - nb < nj ? j0 + c - nb : -1);
                 };
+                // Block dataflow instead of a grid barrier per outer round: every block is visited once
+                // per round, by one cluster; ver[b] counts the CTA-visits of block b completed so far,
+                // so this visit may start once both of its blocks have seen ncta * (rounds so far).
+                const unsigned need = static_cast<unsigned>(ncta) * static_cast<unsigned>(gstep);
+                if (tid == 0) {
+                    volatile unsigned* vi = p.ver + bi;
+                    volatile unsigned* vj = p.ver + bj;
+                    while (*vi < need || *vj < need) {}
+                    __threadfence();
+                }
+                __syncthreads();
+                if (tid == 0) { const unsigned long long q = jb_now(); ph[4] += q - tp; tp = q; }
                 if (bulk) {
                     if (tid == 0) {
                         // the columns were written by other CTAs (generic proxy) before the grid barrier
@@ -1994,12 +2008,19 @@ __global__ void __launch_bounds__(kJbThreads, 1) jacobi_gram_kernel(JacobiGramAr
                     if (tid == 0 && crank == 0) atomicAdd(p.rotated + sweep, s_cnt);
                 }
                 __syncthreads();
-                if (tid == 0) { const unsigned long long q = jb_now(); ph[3] += q - tp; }
+                if (tid == 0) {  // this CTA's rows of both blocks are written: publish the visit
+                    __threadfence();
+                    atomicAdd(p.ver + bi, 1u);
+                    atomicAdd(p.ver + bj, 1u);
+                    const unsigned long long q = jb_now(); ph[3] += q - tp;
+                }
             }
-            const unsigned long long tb = jb_now();
-            grid_barrier_tight(p.gbar, gridDim.x);
-            if (tid == 0) ph[4] += jb_now() - tb;
+            ++gstep;
         }
+        // one grid barrier per sweep: the sweep's rotation count is complete
+        const unsigned long long tb = jb_now();
+        grid_barrier_tight(p.gbar, gridDim.x);
+        if (tid == 0) ph[4] += jb_now() - tb;
         if (*reinterpret_cast<volatile unsigned*>(p.rotated + sweep) == 0) break;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *p.sweeps_out = sweep;
@@ -2455,9 +2476,12 @@ int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, 
     const int grid = std::max(1, std::min(gemm_num_sms(), (rp / 2 + 7) / 8));
     unsigned* rotated = nullptr;
     int* sweeps = nullptr;
-    QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rotated), sizeof(unsigned) * (max_sweeps + 1) + sizeof(int), st));
+    const int nver = r / 8 + 4;  // per-block visit counters of the Gram-based kernel
+    const std::size_t ctl_bytes = sizeof(unsigned) * (max_sweeps + 1) + sizeof(int) + sizeof(unsigned) * nver;
+    QB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rotated), ctl_bytes, st));
     sweeps = reinterpret_cast<int*>(rotated + max_sweeps + 1);
-    QB_CUDA(cudaMemsetAsync(rotated, 0, sizeof(unsigned) * (max_sweeps + 1) + sizeof(int), st));
+    unsigned* ver = reinterpret_cast<unsigned*>(sweeps + 1);
+    QB_CUDA(cudaMemsetAsync(rotated, 0, ctl_bytes, st));
     // block Jacobi when 2 nb columns of N fit in shared memory (nb = 8, 4, 2 or 1)
     int nb = 0;
     const char* nb_env = std::getenv("QBFAC_JACOBI_NB");
@@ -2496,7 +2520,7 @@ int jacobi_svd(cudaStream_t st, double* nmat, double* w, int r, unsigned* gbar, 
         const char* tr = std::getenv("QBFAC_JACOBI_TRACE");
         const char* in_env = std::getenv("QBFAC_JACOBI_INNER");
         const int inner = in_env ? std::max(1, std::min(8, std::atoi(in_env))) : 1;
-        JacobiGramArgs a{nmat, w, r, nblk, max_sweeps, inner, tol, gbar, rotated, sweeps, tr && tr[0] == '1' ? 1 : 0};
+        JacobiGramArgs a{nmat, w, r, nblk, max_sweeps, inner, tol, gbar, rotated, ver, sweeps, tr && tr[0] == '1' ? 1 : 0};
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(gb));
         cfg.blockDim = dim3(kJbThreads);
