@@ -900,11 +900,6 @@ __device__ __forceinline__ void panel_trmm(const double* ys, const double* rs, d
 // Phase timestamps of the last panel launch (CTA 0, %globaltimer ns): read by
 // qbfac_gpu_test_panel_trace for the per-phase breakdown in profiles/.
 __device__ unsigned long long g_panel_trace[kPanelTraceSlots];
-__device__ __forceinline__ unsigned long long jb_now_early() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 __device__ __forceinline__ void panel_mark(int slot) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long t;
@@ -1202,7 +1197,6 @@ struct ClusterPanelCfg {
 
 template <int BP>
 __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_constant__ PanelArgs p, int rr) {
-    unsigned long long dbg_t0 = jb_now_early();
     pdl_wait();
     panel_mark(0);
     using C = PanelCfg<BP>;
@@ -1372,8 +1366,6 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
     // ---- Q = T R_b^{-1}
     product(true, false);
     panel_mark(10);
-    if (p.nstages == -7 && threadIdx.x == 0)
-        printf("cta %d start %llu end %llu (dur %.1f us)\n", crank, dbg_t0, jb_now_early(), (jb_now_early() - dbg_t0) * 1e-3);
 }
 
 template <int BP>
@@ -1387,7 +1379,6 @@ void launch_cholqr2_cluster(cudaStream_t st, PanelArgs& a) {
     });
     const int ncta = static_cast<int>(std::min<std::int64_t>(kClusterMaxCtas, std::max<std::int64_t>(1, ceil_div(a.rows, 128))));
     const int rr = static_cast<int>(ceil_div(a.rows, ncta));
-    if (std::getenv("QBFAC_PANEL_DEBUG")) a.nstages = -7;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(ncta));
     cfg.blockDim = dim3(256);
