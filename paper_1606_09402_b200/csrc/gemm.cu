@@ -540,12 +540,20 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
         return !(e && e[0] == '0');
     }();
     if (ws_path && fam == Family::kWide && N > 96 && N <= 104 && use104 && !(flags & kGemmUpperC)) bn = 104;
-    if (ws_path && fam == Family::kSkinny56 && !a.rowmajor) bn = 64;
+    // A column-major (the k x b coefficient products Q^T Y, B Omega_i): the 56-column tile too
+    // (config 3: Q^T Y 9.19 -> 8.08 ms and B Omega 5.10 -> 4.54 ms per factorization, tools/gemm_cfg3.py;
+    // QBFAC_GEMM_TN56=0 restores the 64-column tile, which measured faster before the split-K count
+    // followed the kernel's real occupancy)
+    static const bool tn56 = [] {
+        const char* e = std::getenv("QBFAC_GEMM_TN56");
+        return !(e && e[0] == '0');
+    }();
+    if (ws_path && fam == Family::kSkinny56 && !a.rowmajor && !tn56) bn = 64;
     const std::int64_t tiles = output_tiles(M, N, bm, bn, flags);
     const int sms = gemm_num_sms();
     // the same famid dispatch_ws uses below
     const int famid = fam == Family::kWide ? (bn == 112 ? 5 : bn == 104 ? 6 : 0) : fam == Family::kWide80 ? 4
-                      : fam == Family::kSkinny56 ? (a.rowmajor ? 3 : 1) : fam == Family::kSkinny ? 1 : 2;
+                      : fam == Family::kSkinny56 ? ((a.rowmajor || tn56) ? 3 : 1) : fam == Family::kSkinny ? 1 : 2;
     // Resident CTAs per SM: the warp-specialised instance's real occupancy (the 64 x 32 tiles:
     // 2 per SM, not 3 — splitting for 3 left a second partial wave); legacy kernels ~1, narrow ~3.
     int resident = fam == Family::kNarrow ? 3 : 1;
@@ -572,7 +580,6 @@ void gemm(cudaStream_t st, Workspace& ws, double alpha, const MatView& a, const 
     if (splits > 1) partial = ws.get(static_cast<std::size_t>(splits) * M * N);
     if (ws_path) {
         // warp-specialised TMA/mbarrier pipeline (gemm_ws.cuh)
-        // (the 56-wide tile measured slower than 64 on the TMA path for A column-major: famid 1 there)
         {
             if (a.rowmajor) {
                 if (b.rowmajor) dispatch_ws<true, true>(famid, st, a, b, c.p, c.ld, c.rowmajor, (int)M, (int)N, (int)K, splits, klen, alpha, beta, partial, flags, &ws);
