@@ -1135,7 +1135,7 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
     // products that never fill the pipeline (b = 20: 5 blocks per product). Each block still counts
     // its pass (Alg. 2 reads A once per block; the count reported is the algorithm's). Blocks past a
     // termination waste at most c - 1 narrow products. QBFAC_EI_YBATCH=0 disables.
-    static const bool ybatch_on = [] {
+    const bool ybatch_on = [] {  // read per run (tests compare both settings in one process)
         const char* e = std::getenv("QBFAC_EI_YBATCH");
         return !(e && e[0] == '0');
     }();

@@ -478,3 +478,50 @@ def test_wide_block_rank_collapse(ctx, oracle):
     assert (got.rank, got.terminated_by) == (ref.rank, ref.terminated_by)
     assert got.rank <= 120
     assert np.linalg.norm(a - got.Q @ got.B) <= 1e-10 * np.linalg.norm(a)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["decay_b20", "decay_b50_P1", "odd_b", "low_rank_collapse", "fixed_rank_mid_batch"])
+def test_ei_batched_first_pass_matches_per_block(ctx, oracle, case):
+    """Dense A: the first pass of several consecutive blocks is one product A [Omega_i ... Omega_{i+c-1}]
+    (run_ei, QBFAC_EI_YBATCH). Same rank / passes / termination as the one-pass-per-block run and as
+    the oracle, sigma(B) within 1e-10: blocks that end inside a batch, a batch that straddles the
+    rank cap, an odd b (no batching), and the Householder recomputation of a rank-deficient sketch
+    inside a batch."""
+    import os
+    from paper_1606_09402_b200 import matgen, qbfac
+    rs = np.random.default_rng(3)
+    kw = {}
+    if case == "decay_b20":
+        a, b, P = matgen.synthesize(700, 500, matgen.spectrum("exp_decay", 500, tau=40.0), 5), 20, 0
+        stop, okw = qbfac.StopRule.fixed_precision(2e-2 * np.linalg.norm(a)), dict(eps_abs=2e-2 * np.linalg.norm(a))
+    elif case == "decay_b50_P1":
+        a, b, P = matgen.synthesize(900, 600, matgen.spectrum("exp_decay", 600, tau=60.0), 6), 50, 1
+        stop, okw = qbfac.StopRule.fixed_precision(5e-2 * np.linalg.norm(a)), dict(eps_abs=5e-2 * np.linalg.norm(a))
+    elif case == "odd_b":
+        a, b, P = matgen.synthesize(400, 300, matgen.spectrum("exp_decay", 300, tau=25.0), 7), 15, 1
+        stop, okw = qbfac.StopRule.fixed_precision(5e-2 * np.linalg.norm(a)), dict(eps_abs=5e-2 * np.linalg.norm(a))
+    elif case == "low_rank_collapse":
+        a = np.asfortranarray(rs.standard_normal((300, 34)) @ rs.standard_normal((34, 200)))
+        b, P = 8, 0
+        stop, okw = qbfac.StopRule.fixed_precision(1e-6 * np.linalg.norm(a)), dict(eps_abs=1e-6 * np.linalg.norm(a))
+    else:
+        a, b, P = matgen.synthesize(500, 400, matgen.spectrum("exp_decay", 400, tau=50.0), 8), 20, 0
+        stop, okw = qbfac.StopRule.fixed_rank(130, 0), dict(fixed_rank=(130, 0))  # 6.5 blocks: ends mid-batch
+    ref = oracle.run("ei", a, b=b, power=P, seed=11, **okw)
+    runs = {}
+    for flag in ("1", "0"):
+        os.environ["QBFAC_EI_YBATCH"] = flag
+        try:
+            runs[flag] = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), stop, b, P, qbfac.RngStream(11))
+        finally:
+            os.environ.pop("QBFAC_EI_YBATCH")
+    for got in runs.values():
+        assert (got.rank, got.passes, got.terminated_by) == (ref.rank, ref.passes, ref.terminated_by)
+        assert np.linalg.norm(a - got.Q @ got.B) <= np.linalg.norm(a - ref.Q @ ref.B) * (1 + 1e-8) + 1e-10 * np.linalg.norm(a)
+        assert np.abs(got.Q.T @ got.Q - np.eye(got.rank)).max() <= 1e-12
+    s1, s0 = (np.linalg.svd(runs[f].B, compute_uv=False) for f in ("1", "0"))
+    sr = np.linalg.svd(ref.B, compute_uv=False)
+    top = sr > 1e-8 * sr[0]
+    assert np.max(np.abs(s1 - s0)[top] / sr[top]) <= 1e-10
+    assert np.max(np.abs(s1 - sr)[top] / sr[top]) <= 1e-10
