@@ -98,7 +98,7 @@ void panel_trace(unsigned long long* out);
 void chol_wide_trace(unsigned long long* out);  // 64 x 4 step stamps of the last chol_wide launch  // phase timestamps of the last panel launch
 void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t rows, int b, std::int64_t ldy,
                    double* t1, double* q, std::int64_t ldq, double* g, double* ra, double* rainv, double* rb,
-                   double* rbinv, SmallStatus* st0, SmallStatus* st1, unsigned* gbar);
+                   double* rbinv, SmallStatus* st0, SmallStatus* st1, unsigned* gbar, bool span_only = false);
 // C = A * B for upper-triangular b x b (col-major, ld); C must not alias.
 void trmm_upper_small(cudaStream_t st, const double* a, const double* b, double* c, int n,
                       std::int64_t ld);

@@ -615,8 +615,10 @@ public:
                s1.gram_dev <= kCholGramDevMax && std::isfinite(s0.diag_max) && std::isfinite(s1.diag_max);
     }
 
+    // span_only: the caller uses span(Y) only (a sketch inside the power iteration); the fused panel
+    // then stops after one CholQR pass when that pass is orthonormal to 1e-6 (cholqr2_panel).
     int orth_block(const MatView& y, const MatView& qout, int r_slot, int rinv_slot, bool sharded, DBuf& tmp,
-                   bool need_r = true) {
+                   bool need_r = true, bool span_only = false) {
         const int b = static_cast<int>(y.cols);
         const std::int64_t rows = y.rows;
         if (b == 0) return 0;
@@ -631,7 +633,7 @@ public:
             // only when the statuses are checked lazily: the Householder redo restarts the block).
             if (!sharded && rows > 0 && y.rowmajor && qout.rowmajor && (lazy || qout.p != y.p)) {
                 cholqr2_panel(st_, c_.ws_panel, y.p, rows, b, y.ld, t1.p, qout.p, qout.ld, slot(kG), slot(kRa),
-                              slot(kRainv), slot(kRb), slot(kRbinv), st0, st1, c_.d_gbar);
+                              slot(kRainv), slot(kRb), slot(kRbinv), st0, st1, c_.d_gbar, span_only);
                 bool ok = true;
                 if (lazy) {
                     ++lazy_n;
@@ -1129,6 +1131,12 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
     // allreduce in between). Queueing its projection Y -= Q (B Omega_{i+1}) as well measured no
     // further gain (config 1 3.80 -> 3.83 ms): the read-back is already covered.
     bool y_pre = false, m_pre = false;
+    // The sketches inside the power iteration (Y before the A^T pass, Z before the A pass) only
+    // pass their span on; their orth may stop after one CholQR pass (QBFAC_EI_SPAN_ORTH=0: always two).
+    const bool span_only = [] {
+        const char* e = std::getenv("QBFAC_EI_SPAN_ORTH");
+        return !(e && e[0] == '0');
+    }();
     // Dense resident A, narrow blocks: the first pass of several consecutive blocks is ONE product
     // A [Omega_i ... Omega_{i+c-1}] (their Omega columns are adjacent in the batch drawn above), up to
     // 104 columns wide, so the pass runs on the wide DMMA tiles instead of c launches of b-column
@@ -1193,7 +1201,7 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             m_pre = false;
             // per-block power iteration with deflation at every application
             for (std::int64_t it = 0; it < p.power; ++it) {
-                eng.orth_block(yv, yv, kR1, kR1inv, sharded, tmp, false);
+                eng.orth_block(yv, yv, kR1, kR1inv, sharded, tmp, false, span_only);
                 MatView zv{z.p, blk, bi, lyz, true};   // this rank's rows of Z (all n when replicated)
                 MatView zr = zv.rows_range(0, nl);
                 if (nsh) eng.apply_t_rs(yv, zv, n_pad, blk);
@@ -1207,12 +1215,12 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
                 if (nsh) {
                     eng.geo_rows = n_pad;
                     eng.geo_row0 = c0;
-                    eng.orth_block(zv, zv, kR1, kR1inv, true, tmp, false);  // rows of Z split over the ranks
+                    eng.orth_block(zv, zv, kR1, kR1inv, true, tmp, false, span_only);  // rows of Z split over the ranks
                     eng.geo_rows = -1;
                     c.all_gather(z.p, zfull.p, static_cast<std::size_t>(blk * lyz));
                     eng.apply(MatView{zfull.p, n, bi, lyz, true}, yv); a.passes += 1;
                 } else {
-                    eng.orth_block(zv, zv, kR1, kR1inv, false, tmp, false);
+                    eng.orth_block(zv, zv, kR1, kR1inv, false, tmp, false, span_only);
                     eng.apply(zv, yv); a.passes += 1;
                 }
                 if (s.k > 0) {

@@ -202,6 +202,13 @@ __global__ void __launch_bounds__(kRedThreads) colsumsq_stage2(const double* __r
 
 constexpr int kCholThreads = 288;  // 9 warps: 8 DMMA warps + 1
 constexpr double kFirstOrderDev = 1e-8;
+// One CholQR pass leaves ||Q^T Q - I|| ~ u kappa(Y)^2. Where only span(Y) matters (the sketches inside
+// the power iteration: the next pass multiplies them by A or A^T and re-orthonormalises), the second
+// pass is skipped when that loss is <= 1e-6, kappa estimated by the diagonal ratio of R_a — the rule
+// orth_wide_cholqr2 applies to randQB_FP's power-step sketches (qb.cu).
+__device__ __forceinline__ bool span_pass_enough(double dmin, double dmax) {
+    return dmin > 0.0 && 2.220446049250313e-16 * dmax * dmax <= 1e-6 * dmin * dmin;
+}
 
 // 1/x to full double precision: MUFU reciprocal seed + two Newton steps (no IEEE
 // division slow path on the Cholesky's critical path).
@@ -765,6 +772,8 @@ struct PanelArgs {
     SmallStatus *st0, *st1;
     unsigned* gbar;  // grid barrier words
     int nstages;     // sub-tile ring depth (<= PanelCfg<BP>::STAGES; fewer -> 2 CTAs per SM)
+    int span_only;   // the caller needs span(Y) only (a power-iteration sketch): stop after the first
+                     // pass when its loss of orthogonality u kappa^2 (kappa from diag(R_a)) is <= 1e-6
 };
 
 template <int BP>
@@ -1088,7 +1097,9 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
     // A near-orthonormal panel (Gram within 1e-8 of I: every re-orthogonalisation) needs one
     // pass: Q = Y Ra^{-1} is orthonormal to O(u) already, so phase B writes Q and the second
     // Gram / Cholesky / product are skipped (Rb = I, its status reports a clean identity).
-    const bool one_pass = __ldcg(&p.st0->gram_dev) <= kFirstOrderDev && __ldcg(&p.st0->breakdown) == 0;
+    const bool one_pass = __ldcg(&p.st0->breakdown) == 0 &&
+                          (__ldcg(&p.st0->gram_dev) <= kFirstOrderDev ||
+                           (p.span_only && span_pass_enough(__ldcg(&p.st0->diag_min), __ldcg(&p.st0->diag_max))));
     if (one_pass) {
         stage_r(p.rainv);
         sub_loop(p.y, p.ldy, p.use_tm_y ? &p.tm_y : nullptr, [&](double* cur, std::int64_t r0) {
@@ -1337,7 +1348,8 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
     for (int sub = 0; sub < nsub; ++sub) panel_gram<BP>(ys + sub * C::SUB * K::LD, acc, fm, fn, nvf);
     panel_mark(1);
     gram_reduce_factor(p.st0, p.ra, p.rainv, true);
-    const bool one_pass = sst.gram_dev <= kFirstOrderDev && sst.breakdown == 0;
+    const bool one_pass = sst.breakdown == 0 &&
+                          (sst.gram_dev <= kFirstOrderDev || (p.span_only && span_pass_enough(sst.diag_min, sst.diag_max)));
     stage_r();
     if (one_pass) {  // near-orthonormal Y: Q = Y R_a^{-1}, R_b = I (as the panel kernel)
         product(true, false);
@@ -2435,10 +2447,11 @@ void launch_cholqr2_panel(cudaStream_t st, PanelArgs& a, int grid_cap) {
 
 void cholqr2_panel(cudaStream_t st, Workspace& ws, const double* y, std::int64_t rows, int b, std::int64_t ldy,
                    double* t1, double* q, std::int64_t ldq, double* g, double* ra, double* rainv, double* rb,
-                   double* rbinv, SmallStatus* st0, SmallStatus* st1, unsigned* gbar) {
+                   double* rbinv, SmallStatus* st0, SmallStatus* st1, unsigned* gbar, bool span_only) {
     if (b < 1 || b > kSmallMax) throw QbError(kDimensionError, "cholqr2_panel: width out of range");
     const int bp = static_cast<int>(round_up(b, 16));
     PanelArgs a{};
+    a.span_only = span_only ? 1 : 0;
     a.y = y; a.ldy = ldy; a.t1 = t1; a.q = q; a.ldq = ldq; a.rows = rows; a.b = b;
     a.g = g; a.ra = ra; a.rainv = rainv; a.rb = rb; a.rbinv = rbinv; a.st0 = st0; a.st1 = st1; a.gbar = gbar;
     if (bp <= 32 && rows > 0 && rows <= static_cast<std::int64_t>(kClusterMaxCtas) * kClusterRowsPerCta &&
