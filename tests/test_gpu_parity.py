@@ -525,3 +525,43 @@ def test_ei_batched_first_pass_matches_per_block(ctx, oracle, case):
     top = sr > 1e-8 * sr[0]
     assert np.max(np.abs(s1 - s0)[top] / sr[top]) <= 1e-10
     assert np.max(np.abs(s1 - sr)[top] / sr[top]) <= 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["csr_P2", "dense_P1", "dense_steep_P2"])
+def test_ei_span_only_sketch_orth_matches_two_pass(ctx, oracle, case):
+    """The sketches inside the power iteration are orthonormalised by one CholQR pass when that pass
+    is orthonormal to 1e-6 (run_ei, QBFAC_EI_SPAN_ORTH; device-side decision in the fused panel).
+    Same rank / passes / termination as with both passes everywhere and as the oracle, sigma(B)
+    within 1e-10 — including a steep spectrum whose later blocks are too ill-conditioned for the
+    one-pass rule (the panel then runs both passes on its own)."""
+    import os
+    from paper_1606_09402_b200 import matgen, qbfac
+    if case == "csr_P2":
+        csr = matgen.csr_uniform(4000, 2500, 25, seed=21)
+        eps = 0.45 * np.sqrt(oracle.csr_frob_sq(csr))
+        ref = oracle.run("ei", csr=csr, b=32, power=2, eps_abs=eps, max_rank=320, seed=5)
+        make = lambda: qbfac.rand_qb_ei(qbfac.MatrixHandle.csr(*csr, ctx=ctx), qbfac.StopRule.fixed_precision(eps), 32, 2,
+                                        qbfac.RngStream(5), max_rank=320)
+    else:
+        tau = 60.0 if case == "dense_P1" else 6.0
+        P = 1 if case == "dense_P1" else 2
+        a = matgen.synthesize(800, 500, matgen.spectrum("exp_decay", 500, tau=tau), 9)
+        eps = (5e-2 if case == "dense_P1" else 1e-6) * np.linalg.norm(a)
+        ref = oracle.run("ei", a, b=25, power=P, eps_abs=eps, seed=5)
+        make = lambda: qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), qbfac.StopRule.fixed_precision(eps), 25, P,
+                                        qbfac.RngStream(5))
+    runs = {}
+    for flag in ("1", "0"):
+        os.environ["QBFAC_EI_SPAN_ORTH"] = flag
+        try:
+            runs[flag] = make()
+        finally:
+            os.environ.pop("QBFAC_EI_SPAN_ORTH")
+    sr = np.linalg.svd(ref.B, compute_uv=False)
+    top = sr > 1e-7 * sr[0]
+    for got in runs.values():
+        assert (got.rank, got.passes, got.terminated_by) == (ref.rank, ref.passes, ref.terminated_by)
+        assert np.abs(got.Q.T @ got.Q - np.eye(got.rank)).max() <= 1e-12
+        sg = np.linalg.svd(got.B, compute_uv=False)
+        assert np.max(np.abs(sg - sr)[top] / sr[top]) <= 1e-10
