@@ -58,11 +58,12 @@ def test_k_too_large(ctx):
         r.svd(21)
 
 
-@pytest.mark.parametrize("rank", [333, 600, 1000, 1450])
+@pytest.mark.parametrize("rank", [333, 600, 1000, 1450, 1568, 1600])
 def test_block_jacobi_large_rank(ctx, rank):
-    """qb_to_svd at rank 333 (odd: plain column loads) / 600 / 1000 / 1450 (more block pairs than
-    2-CTA clusters fit) through the Gram-based block one-sided Jacobi (nb = 8 column blocks, one
-    2-CTA cluster per block pair): S equals the SVD of B to 1e-12 relative, U and V orthonormal,
+    """qb_to_svd at rank 333 (odd: plain column loads) / 600 / 1000 / 1450 and 1568 (more block pairs than
+    2-CTA clusters fit; 1568 is the largest rank whose column slices fit shared memory) through the
+    Gram-based block one-sided Jacobi (nb = 8 column blocks, one 2-CTA cluster per block pair), and
+    1600 through the column-rotating block kernel that remains above it: S equals the SVD of B to 1e-12 relative, U and V orthonormal,
     U S V^T = Q B, and the scalar Jacobi (QBFAC_JACOBI_SCALAR=1) agrees."""
     import os
     from paper_1606_09402_b200 import matgen, qbfac
