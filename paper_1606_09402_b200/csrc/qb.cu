@@ -1231,7 +1231,9 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
             }
             // orth, then re-orthogonalisation against Q (step 6)
             MatView qs = s.qslot(bi);
-            d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp, false);
+            // (when the re-orthogonalisation follows, this orth too only hands on a span: the
+            // projection is linear, and the second orth below is the one that makes Q_i orthonormal)
+            d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp, false, span_only && s.k > 0);
             if (d > 0 && s.k > 0) {
                 MatView qd = s.qslot(d);
                 MatView md{mbuf.p, s.k, d, d, true};

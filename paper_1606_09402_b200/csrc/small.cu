@@ -202,6 +202,11 @@ __global__ void __launch_bounds__(kRedThreads) colsumsq_stage2(const double* __r
 
 constexpr int kCholThreads = 288;  // 9 warps: 8 DMMA warps + 1
 constexpr double kFirstOrderDev = 1e-8;
+// A panel whose Gram is within 1e-2 of the identity is what the SECOND pass of CholQR2 is handed
+// anyway (it accepts up to kCholGramDevMax = 0.5): one pass with the true Cholesky factor leaves
+// u kappa^2 <= 1.02 u of orthogonality loss, so such a panel takes one pass (below 1e-8 the factor
+// is the first-order one, chol_tile_block).
+constexpr double kOnePassDev = 1e-2;
 // One CholQR pass leaves ||Q^T Q - I|| ~ u kappa(Y)^2. Where only span(Y) matters (the sketches inside
 // the power iteration: the next pass multiplies them by A or A^T and re-orthonormalises), the second
 // pass is skipped when that loss is <= 1e-6, kappa estimated by the diagonal ratio of R_a — the rule
@@ -1098,7 +1103,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
     // pass: Q = Y Ra^{-1} is orthonormal to O(u) already, so phase B writes Q and the second
     // Gram / Cholesky / product are skipped (Rb = I, its status reports a clean identity).
     const bool one_pass = __ldcg(&p.st0->breakdown) == 0 &&
-                          (__ldcg(&p.st0->gram_dev) <= kFirstOrderDev ||
+                          (__ldcg(&p.st0->gram_dev) <= kOnePassDev ||
                            (p.span_only && span_pass_enough(__ldcg(&p.st0->diag_min), __ldcg(&p.st0->diag_max))));
     if (one_pass) {
         stage_r(p.rainv);
@@ -1349,7 +1354,7 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
     panel_mark(1);
     gram_reduce_factor(p.st0, p.ra, p.rainv, true);
     const bool one_pass = sst.breakdown == 0 &&
-                          (sst.gram_dev <= kFirstOrderDev || (p.span_only && span_pass_enough(sst.diag_min, sst.diag_max)));
+                          (sst.gram_dev <= kOnePassDev || (p.span_only && span_pass_enough(sst.diag_min, sst.diag_max)));
     stage_r();
     if (one_pass) {  // near-orthonormal Y: Q = Y R_a^{-1}, R_b = I (as the panel kernel)
         product(true, false);
