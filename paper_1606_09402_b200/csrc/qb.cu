@@ -1301,6 +1301,10 @@ std::unique_ptr<Result> run_ei(Context& c, Matrix& a, const Params& p) {
 // ---- randQB_FP / fixed rank / single pass --------------------------------------------
 std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
     if (p.b < 1) throw QbError(kDimensionError, "rand_qb_fp: block size must be >= 1");
+    const bool fp_span_only = [] {
+        const char* e = std::getenv("QBFAC_EI_SPAN_ORTH");
+        return !(e && e[0] == '0');
+    }();
     if (a.host_stream && (p.alg != 3 || p.power != 0))
         throw QbError(kError, "host-streamed matrix: only single_pass_fp consumes a RowStream");
     Engine eng(c, a);
@@ -1401,7 +1405,9 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
                     eng.gemm(-1.0, s.qk(), m1v, 1.0, yv);
                 }
                 MatView qs = s.qslot(bi);
-                d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp);            // step 13
+                // step 13; when steps 14-15 follow, R_1 only has to satisfy Y = Q~ R_1 (B_i's formula
+                // below holds for any such pair), so this orth may stop after one pass like run_ei's
+                d = eng.orth_block(yv, qs, kR1, kR1inv, sharded, tmp, true, fp_span_only && reorth && s.k > 0);
                 int rinv_slot = kR1inv;
                 if (d > 0 && reorth && s.k > 0) {                                  // steps 14-15 (9a-9b)
                     MatView qd = s.qslot(d);
