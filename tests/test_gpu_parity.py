@@ -565,3 +565,23 @@ def test_ei_span_only_sketch_orth_matches_two_pass(ctx, oracle, case):
         assert np.abs(got.Q.T @ got.Q - np.eye(got.rank)).max() <= 1e-12
         sg = np.linalg.svd(got.B, compute_uv=False)
         assert np.max(np.abs(sg - sr)[top] / sr[top]) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_ei_batched_first_pass_over_async_upload(ctx, oracle):
+    """randQB_EI on a chunked asynchronous upload: the first (batched, 100-column) pass A [Omega_0 ... Omega_4]
+    consumes the row chunks as they land (Engine::apply over Matrix::pending) and the result equals the
+    resident-matrix run bit for bit in rank / passes and to 1e-12 in sigma(B)."""
+    from paper_1606_09402_b200 import matgen, qbfac
+    a = matgen.synthesize(1500, 600, matgen.spectrum("exp_decay", 600, tau=45.0), 12)
+    eps = 3e-2 * np.linalg.norm(a)
+    stop = qbfac.StopRule.fixed_precision(eps)
+    ref = oracle.run("ei", a, b=20, power=1, eps_abs=eps, seed=4)
+    g0 = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense(a, ctx), stop, 20, 1, qbfac.RngStream(4))
+    g1 = qbfac.rand_qb_ei(qbfac.MatrixHandle.dense_async(np.asfortranarray(a), ctx, chunk_rows=256), stop, 20, 1,
+                          qbfac.RngStream(4))
+    for got in (g0, g1):
+        assert (got.rank, got.passes, got.terminated_by) == (ref.rank, ref.passes, ref.terminated_by)
+    s0, s1 = np.linalg.svd(g0.B, compute_uv=False), np.linalg.svd(g1.B, compute_uv=False)
+    assert np.max(np.abs(s0 - s1) / s0[0]) <= 1e-12
+    assert np.linalg.norm(a - g1.Q @ g1.B) <= eps
