@@ -326,8 +326,26 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
         constexpr bool kPrefetchC = T::MI * T::NI * 4 <= 32;
         double cpre[kPrefetchC ? T::MI : 1][kPrefetchC ? T::NI : 1][4];
         const bool use_pre = kPrefetchC && p.beta != 0.0 && !p.partial;
+        const bool vec_c = !p.partial && p.c_row && (p.ldc & 1) == 0 && (reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0;
         if constexpr (kPrefetchC) {
-            if (use_pre) {
+            if (use_pre && vec_c) {  // 16-byte loads of the fragment's column pairs
+#pragma unroll
+                for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                    for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int row = m0 + wm * T::WTM + i * 16 + g + 8 * h;
+                            const int col = n0 + wn * T::WTN + j * 8 + 2 * t;
+                            double2 v = make_double2(0.0, 0.0);
+                            if (row < p.M && col + 1 < p.N)
+                                v = __ldcg(reinterpret_cast<const double2*>(p.C + static_cast<std::int64_t>(row) * p.ldc + col));
+                            else if (row < p.M && col < p.N)
+                                v.x = __ldcg(p.C + static_cast<std::int64_t>(row) * p.ldc + col);
+                            cpre[i][j][2 * h] = v.x;
+                            cpre[i][j][2 * h + 1] = v.y;
+                        }
+            } else if (use_pre) {
 #pragma unroll
                 for (int i = 0; i < T::MI; ++i)
 #pragma unroll
@@ -408,7 +426,40 @@ __global__ void __launch_bounds__((WM * WN + NP) * 32, 1) dgemm_ws_kernel(const 
                         acc[i][j][r] = v;
                     }
         }
-        // epilogue (registers -> global); the producer is already prefetching the next item
+        // epilogue (registers -> global); the producer is already prefetching the next item.
+        // Row-major C with an even, 16-byte aligned row stride: the fragment's column pairs (2t, 2t + 1)
+        // leave as one 16-byte store (a full half-sector per lane instead of two 8-byte pieces).
+        if (vec_c) {
+#pragma unroll
+            for (int i = 0; i < T::MI; ++i) {
+#pragma unroll
+                for (int j = 0; j < T::NI; ++j) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int row = m0 + wm * T::WTM + i * 16 + g + 8 * h;
+                        const int col = n0 + wn * T::WTN + j * 8 + 2 * t;
+                        if (row >= p.M || col >= p.N) continue;
+                        double* cp = p.C + static_cast<std::int64_t>(row) * p.ldc + col;
+                        double v0 = p.alpha * acc[i][j][2 * h], v1 = p.alpha * acc[i][j][2 * h + 1];
+                        if (p.beta != 0.0) {
+                            double o0, o1;
+                            if constexpr (kPrefetchC) {
+                                o0 = use_pre ? cpre[i][j][2 * h] : cp[0];
+                                o1 = use_pre ? cpre[i][j][2 * h + 1] : (col + 1 < p.N ? cp[1] : 0.0);
+                            } else {
+                                o0 = cp[0];
+                                o1 = col + 1 < p.N ? cp[1] : 0.0;
+                            }
+                            v0 += p.beta * o0;
+                            v1 += p.beta * o1;
+                        }
+                        if (col + 1 < p.N) *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+                        else cp[0] = v0;
+                    }
+                }
+            }
+            continue;
+        }
 #pragma unroll
         for (int i = 0; i < T::MI; ++i) {
 #pragma unroll
