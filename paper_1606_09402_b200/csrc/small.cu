@@ -911,6 +911,17 @@ __device__ __forceinline__ void panel_trmm(const double* ys, const double* rs, d
     }
 }
 
+// A DMMA accumulator's column pair (2t, 2t + 1) to row-major global memory: one 16-byte store when the
+// destination allows it (an 8-byte store per element touches every 32-byte sector twice).
+__device__ __forceinline__ void store_col_pair(double* dst, bool vec, bool ok0, bool ok1, double v0, double v1) {
+    if (vec && ok1) {
+        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+    } else {
+        if (ok0) dst[0] = v0;
+        if (ok1) dst[1] = v1;
+    }
+}
+
 // Phase timestamps of the last panel launch (CTA 0, %globaltimer ns): read by
 // qbfac_gpu_test_panel_trace for the per-phase breakdown in profiles/.
 __device__ unsigned long long g_panel_trace[kPanelTraceSlots];
@@ -934,6 +945,8 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const bool mma_warp = warp < 8;
+    const bool vec_q = (p.ldq & 1) == 0 && (reinterpret_cast<std::uintptr_t>(p.q) & 15) == 0;
+    const bool vec_t1 = (p.b & 1) == 0 && (reinterpret_cast<std::uintptr_t>(p.t1) & 15) == 0;
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
             pb_init(&full[s], 1);
@@ -1115,9 +1128,11 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
 #pragma unroll
                 for (int j = 0; j < C::MAXT; ++j)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int row = 16 * mi + g + (e >= 2 ? 8 : 0), col = 8 * (h + C::NG * j) + 2 * t + (e & 1);
-                        if (r0 + row < p.rows && col < p.b) p.q[(r0 + row) * p.ldq + col] = tacc[j][e];
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int row = 16 * mi + g + 8 * hh, col = 8 * (h + C::NG * j) + 2 * t;
+                        const bool rok = r0 + row < p.rows;
+                        store_col_pair(p.q + (r0 + row) * p.ldq + col, vec_q, rok && col < p.b, rok && col + 1 < p.b,
+                                       tacc[j][2 * hh], tacc[j][2 * hh + 1]);
                     }
             }
         });
@@ -1150,11 +1165,14 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
 #pragma unroll
             for (int j = 0; j < C::MAXT; ++j)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int row = 16 * mi + g + (e >= 2 ? 8 : 0), col = 8 * (h + C::NG * j) + 2 * t + (e & 1);
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int row = 16 * mi + g + 8 * hh, col = 8 * (h + C::NG * j) + 2 * t;
                     if (col >= BP) continue;
-                    cur[row * C::LD + col] = tacc[j][e];
-                    if (r0 + row < p.rows && col < p.b) p.t1[(r0 + row) * p.b + col] = tacc[j][e];
+                    cur[row * C::LD + col] = tacc[j][2 * hh];
+                    cur[row * C::LD + col + 1] = tacc[j][2 * hh + 1];
+                    const bool rok = r0 + row < p.rows;
+                    store_col_pair(p.t1 + (r0 + row) * p.b + col, vec_t1, rok && col < p.b, rok && col + 1 < p.b,
+                                   tacc[j][2 * hh], tacc[j][2 * hh + 1]);
                 }
         }
         consumer_sync();
@@ -1180,9 +1198,11 @@ __global__ void __launch_bounds__(kCholThreads, 1) cholqr2_panel_kernel(const __
 #pragma unroll
             for (int j = 0; j < C::MAXT; ++j)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int row = 16 * mi + g + (e >= 2 ? 8 : 0), col = 8 * (h + C::NG * j) + 2 * t + (e & 1);
-                    if (r0 + row < p.rows && col < p.b) p.q[(r0 + row) * p.ldq + col] = tacc[j][e];
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int row = 16 * mi + g + 8 * hh, col = 8 * (h + C::NG * j) + 2 * t;
+                    const bool rok = r0 + row < p.rows;
+                    store_col_pair(p.q + (r0 + row) * p.ldq + col, vec_q, rok && col < p.b, rok && col + 1 < p.b,
+                                   tacc[j][2 * hh], tacc[j][2 * hh + 1]);
                 }
         }
     });
@@ -1229,6 +1249,7 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
     double* ws = rs + BP * K::LD;            // in-CTA Cholesky workspace
     __shared__ SmallStatus sst;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const bool vec_q = (p.ldq & 1) == 0 && (reinterpret_cast<std::uintptr_t>(p.q) & 15) == 0;
     const std::int64_t r0 = static_cast<std::int64_t>(crank) * rr;
     const std::int64_t left = p.rows - r0;
     const int nr = left <= 0 ? 0 : static_cast<int>(left < rr ? left : rr);
@@ -1333,14 +1354,17 @@ __global__ void __launch_bounds__(256, 1) cholqr2_cluster_kernel(const __grid_co
 #pragma unroll
             for (int j = 0; j < C::MAXT; ++j)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int row = 16 * mi + g + (e >= 2 ? 8 : 0), col = 8 * (h + C::NG * j) + 2 * t + (e & 1);
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int row = 16 * mi + g + 8 * hh, col = 8 * (h + C::NG * j) + 2 * t;
                     if (col >= BP) continue;
                     if (to_q) {
                         const std::int64_t gr = r0 + sub * C::SUB + row;
-                        if (sub * C::SUB + row < nr && col < b) p.q[gr * p.ldq + col] = tacc[j][e];
+                        const bool rok = sub * C::SUB + row < nr;
+                        store_col_pair(p.q + gr * p.ldq + col, vec_q, rok && col < b, rok && col + 1 < b, tacc[j][2 * hh],
+                                       tacc[j][2 * hh + 1]);
                     } else {
-                        cur[row * K::LD + col] = tacc[j][e];
+                        cur[row * K::LD + col] = tacc[j][2 * hh];
+                        cur[row * K::LD + col + 1] = tacc[j][2 * hh + 1];
                     }
                 }
             __syncthreads();
