@@ -169,8 +169,9 @@ std::unique_ptr<Matrix> make_dense_async(Context& c, std::int64_t m, std::int64_
         QB_CUDA(cudaMemsetAsync(mat->a, 0, sizeof(double) * mat->lda * std::max<std::int64_t>(n, 1), c.st_copy));
     }
     if (m == 0 || n == 0) return mat;
-    // ~8 row chunks of whole 128-row GEMM tiles
-    if (chunk_rows <= 0) chunk_rows = std::max<std::int64_t>(1024, round_up(ceil_div(m, 8), 128));
+    // ~9 row chunks of whole 128-row GEMM tiles (896 rows at m = 8000: measured best for the config-2
+    // first pass with the per-chunk Gram behind it, tools/e2e_chunk_sweep.py)
+    if (chunk_rows <= 0) chunk_rows = std::max<std::int64_t>(896, round_up(ceil_div(m, 9), 128));
     for (std::int64_t r0 = 0; r0 < m; r0 += chunk_rows) {
         const std::int64_t rows = std::min(chunk_rows, m - r0);
         QB_CUDA(cudaMemcpy2DAsync(mat->a + r0, mat->lda * sizeof(double), a + r0, lda * sizeof(double),
@@ -372,6 +373,8 @@ public:
 
     // Y (m x w) = A X (X: n x w). Dense: DMMA GEMM; sparse: CSR SpMM.
     void apply(const MatView& x, const MatView& y, double alpha = 1.0, double beta = 0.0) {
+        const bool want_pregram = want_pregram_;
+        want_pregram_ = false;
         if (a_.host_stream) throw QbError(kError, "host-streamed matrix: only single_pass_fp consumes a RowStream");
         if (a_.sparse) {
             if (!x.rowmajor || !y.rowmajor) throw QbError(kInternal, "sparse pass needs row-major blocks");
@@ -393,7 +396,15 @@ public:
                 }
             }
         } else if (!a_.pending.empty()) {
-            // first pass over an asynchronously uploaded A: one GEMM per row chunk as it lands
+            // first pass over an asynchronously uploaded A: one GEMM per row chunk as it lands.
+            // When the caller orthonormalises Y next by the wide CholQR (request_pregram), the
+            // chunk's share of the Gram Y^T Y is accumulated behind its GEMM, in the gaps the copy
+            // leaves on the compute stream, and orth_wide_cholqr2 starts from that Gram.
+            const std::int64_t l = y.cols;
+            const bool pregram = want_pregram && pregram_enabled() && alpha == 1.0 && beta == 0.0 && y.rowmajor &&
+                                 y.ld == l && l > kSmallMax && c_.world == 1 && a_.pending.size() > 1;
+            const std::size_t ll = static_cast<std::size_t>(l) * l;
+            if (pregram && wide_.n < 3 * ll) wide_ = DBuf(3 * ll, st_);
             std::int64_t r0 = 0;
             for (auto& ch : a_.pending) {
                 QB_CUDA(cudaStreamWaitEvent(st_, ch.ready, 0));
@@ -402,8 +413,12 @@ public:
                 MatView yb = y.rowmajor ? MatView{y.p + r0 * y.ld, rows, y.cols, y.ld, true}
                                         : MatView{y.p + r0, rows, y.cols, y.ld, false};
                 gemm(alpha, ab, x, beta, yb);
+                if (pregram)
+                    qbgpu::gemm(st_, c_.ws_gemm, 1.0, yb.t(), yb, r0 == 0 ? 0.0 : 1.0, MatView{wide_.p, l, l, l, false},
+                                kGemmUpperC);
                 r0 = ch.row_end;
             }
+            if (pregram) pregram_for_ = y.p;
             a_.wait_resident(st_);
         } else {
             gemm(alpha, a_.dense_view(), x, beta, y);
@@ -868,7 +883,12 @@ public:
         for (int pass = 0; pass < 2; ++pass) {
             const MatView& src = pass == 0 ? x : y;
             const MatView& dst = pass == 0 ? y : x;
-            qbgpu::gemm(st_, c_.ws_gemm, 1.0, src.t(), src, 0.0, gv, kGemmUpperC);
+            if (pass == 0 && !sharded && pregram_for_ == x.p) {
+                // the Gram of X was accumulated chunk by chunk behind the upload's first pass
+            } else {
+                qbgpu::gemm(st_, c_.ws_gemm, 1.0, src.t(), src, 0.0, gv, kGemmUpperC);
+            }
+            pregram_for_ = nullptr;
             if (sharded) c_.allreduce(g, ll);
             double ratio = 0.0;
             if (!chol_blocked(g, l, r, rinv, pass == 0 ? INFINITY : kCholGramDevMax, &ratio)) {
@@ -912,6 +932,17 @@ public:
         }
     }
 
+    // The next apply() feeds orth_wide: over a chunked asynchronous upload it may accumulate the
+    // wide Gram per chunk (QBFAC_PREGRAM=0 switches this off).
+    void request_pregram() { want_pregram_ = true; }
+    static bool pregram_enabled() {
+        static const bool on = [] {
+            const char* e = std::getenv("QBFAC_PREGRAM");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
+
     std::int64_t hh_fallbacks = 0;
     std::int64_t wide_passes = 0;
     // Row geometry of a sharded panel for the Householder fallback: -1 = the rows of A; the
@@ -920,6 +951,8 @@ public:
 
 private:
     DBuf scratch_t_, stat_, tri_, wide_, wide_y_, wide_s_, wide_diag_, rs_full_, rs_loc_;
+    bool want_pregram_ = false;
+    const double* pregram_for_ = nullptr;  // X whose upper Gram wide_ already holds
     DBuf wslot_[kNumSlots];
     std::int64_t wld_ = 0;
     Context& c_;
@@ -1363,6 +1396,7 @@ std::unique_ptr<Result> run_fp(Context& c, Matrix& a, const Params& p) {
         MatView gv{g.p, m, l, l, true};
         MatView hv{h.p, n, l, l, true};
         for (std::int64_t it = 0; it < p.power; ++it) {                            // steps 3-6
+            if (!sharded) eng.request_pregram();
             eng.apply(omv, gv); a.passes += 1;
             eng.orth_wide(gv, sharded, wtmp, m2);
             eng.apply_t(gv, omv); a.passes += 1;

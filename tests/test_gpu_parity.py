@@ -273,7 +273,9 @@ def test_cfg3_full_size_vs_oracle_golden(ctx):
 @pytest.mark.parametrize("alg,chunk", [("fp", 0), ("fp", 96), ("ei", 200)])
 def test_async_upload_overlapped_first_pass(ctx, oracle, alg, chunk):
     """qbfac_gpu_matrix_dense_async: the first A*X pass consumes row chunks as their H2D copy
-    lands; the factorization matches the resident-A one (and the oracle)."""
+    lands; the factorization matches the resident-A one (and the oracle). With several chunks and a
+    sketch wider than the panel limit (fp, chunk 96: 6 ragged chunks, l = 200) the wide Gram is
+    accumulated per chunk behind the pass (Engine::request_pregram) instead of by one SYRK."""
     from paper_1606_09402_b200 import qbfac
     import torch
     a = _matrix2(500)
@@ -295,6 +297,33 @@ def test_async_upload_overlapped_first_pass(ctx, oracle, alg, chunk):
     s1, s2 = _sv(got_async.B), _sv(got_res.B)
     assert np.max(np.abs(s1 - s2) / s2) < 1e-12
     assert abs(got_async.error_indicator - got_res.error_indicator) <= 1e-12 * got_res.norm_a_sq
+
+
+def test_async_upload_chunked_gram_wide_sketch(ctx):
+    """randQB_FP (P = 1) over a chunked asynchronous upload with a sketch of l = 600 columns: the
+    first pass accumulates the 600 x 600 Gram per chunk (8 chunks of 384 rows, last one 312) behind
+    the chunk GEMMs and the wide CholQR starts from it. Q stays orthonormal, QB reproduces A to the
+    indicator, and rank / passes / sigma(B) equal the resident-A run (one-launch SYRK)."""
+    from paper_1606_09402_b200 import matgen, qbfac
+    import torch
+    m, n = 3000, 900
+    a = matgen.synthesize(m, n, matgen.spectrum("inv", n), 5)
+    eps = 5e-2 * np.linalg.norm(a)
+    pinned = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+    pinned.copy_(torch.as_tensor(np.ascontiguousarray(a.T)))
+    a_f = pinned.numpy().T
+    run = lambda h: qbfac.rand_qb_fp(h, eps, 50, 1, 600, qbfac.RngStream(42), max_rank=600)
+    got = run(qbfac.MatrixHandle.dense_async(a_f, ctx, chunk_rows=384))
+    res = run(qbfac.MatrixHandle.dense(a, ctx))
+    assert got.rank == res.rank and got.passes == res.passes == 4
+    assert got.terminated_by == res.terminated_by
+    q, b = got.Q, got.B
+    assert np.max(np.abs(q.T @ q - np.eye(got.rank))) < 1e-12
+    err2 = np.linalg.norm(a - q @ b) ** 2
+    assert abs(err2 - got.error_indicator) <= 1e-9 * got.norm_a_sq
+    s1, s2 = _sv(b), _sv(res.B)
+    assert np.max(np.abs(s1 - s2) / s2) < 1e-10
+    assert abs(got.error_indicator - res.error_indicator) <= 1e-12 * res.norm_a_sq
 
 
 def test_async_upload_rejects_non_finite(ctx):
