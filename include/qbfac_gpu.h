@@ -139,10 +139,11 @@ int qbfac_gpu_matrix_dense_shard(qbfac_gpu_ctx* ctx, int64_t m_global, int64_t r
                                  int64_t n, const double* a, int64_t lda, qbfac_gpu_matrix** out);
 /* CSR host arrays (validated as SparseCsrMatrix::from_parts). The transposed CSR
  * used for A^T products is built on the device. */
-/* Asynchronous dense upload: the copy is cut into row chunks (chunk_rows, 0 = ~8 chunks of
+/* Asynchronous dense upload: the copy is cut into row chunks (chunk_rows, 0 = ~9 chunks of
  * whole 128-row tiles) issued on the context's copy stream, and the first A*X pass of the
  * next run consumes each chunk as soon as it lands (H2D overlapped with the first pass;
- * pinned host memory gives a true overlap). `a` must stay valid and unchanged until a run
+ * pinned host memory gives a true overlap; when that pass feeds the wide CholQR of
+ * randQB_FP's power scheme, the sketch's Gram is accumulated per chunk behind it). `a` must stay valid and unchanged until a run
  * has consumed the matrix, qbfac_gpu_synchronize(), or qbfac_gpu_matrix_free(). The
  * DenseMatrix::from_data finiteness check (dense_matrix.cpp:17-18) happens at the first
  * norm computation instead of at upload. */
